@@ -1,0 +1,219 @@
+// reshard_b200 -- host C++ API of the B200-native live-handoff reshard path.
+//
+// Same names, argument meaning and error behaviour as the reference's
+// planning surface, so a caller such as GenerationMachine::run_switch
+// (proj/src/generation.cpp:242) compiles unchanged against this header:
+//   geometry   proj/include/reshard/shard_view.hpp:15-112
+//   model      proj/include/reshard/model_spec.hpp:13-87
+//   layout     proj/include/reshard/parallel_config.hpp:12-74
+//   topology   proj/include/reshard/topology.hpp:20-28
+//   plan       proj/include/reshard/transfer_plan.hpp:18-82
+//   planner    proj/include/reshard/planner.hpp:14-47
+//   chunking   proj/include/reshard/executor.hpp:43-44
+// Execution (the reference's execute_plan over a host Transport,
+// proj/include/reshard/executor.hpp:50-53) is replaced by the device engine
+// behind the C ABI in rs_reshard.h.
+//
+// Extension over the reference: TensorSpec::element_bytes (0 = the model's
+// bytes_per_element) so bf16 params and fp32 master/Adam state share one plan.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <iosfwd>
+#include <map>
+#include <optional>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace reshard {
+
+constexpr int kMaxDims = 8;
+
+struct Interval {
+  std::int64_t lo = 0;
+  std::int64_t hi = 0;
+  std::int64_t length() const { return hi - lo; }
+  bool operator==(const Interval&) const = default;
+};
+
+// Non-empty half-open hyper-rectangle; fixed capacity, no heap.
+class ShardView {
+ public:
+  ShardView() = default;
+  explicit ShardView(const std::vector<Interval>& bounds);  // throws std::invalid_argument
+  static ShardView full(const std::vector<std::int64_t>& shape);
+
+  std::size_t ndims() const { return nd_; }
+  const Interval& dim(std::size_t i) const;
+  std::vector<Interval> bounds() const { return {iv_.begin(), iv_.begin() + nd_}; }
+  std::int64_t element_count() const;
+  std::vector<std::int64_t> extents() const;
+  bool contains(const ShardView& other) const;
+  bool contains_point(const std::vector<std::int64_t>& p) const;
+  bool operator==(const ShardView& o) const;
+  std::string to_string() const;
+
+  // unchecked mutable access for planners that build boxes in place
+  Interval& raw(std::size_t i) { return iv_[i]; }
+  void set_ndims(std::size_t n) { nd_ = static_cast<std::uint8_t>(n); }
+
+ private:
+  std::uint8_t nd_ = 0;
+  std::array<Interval, kMaxDims> iv_{};
+};
+
+std::optional<ShardView> intersect(const ShardView& a, const ShardView& b);
+
+enum class TensorRole { kParameter, kOptimizerMoment1, kOptimizerMoment2 };
+const char* to_string(TensorRole r);
+
+struct TensorSpec {
+  std::string tensor_id;
+  int layer = 0;
+  std::vector<std::int64_t> shape;
+  std::optional<int> tp_shard_axis;
+  TensorRole role = TensorRole::kParameter;
+  std::int64_t element_bytes = 0;  // extension: 0 -> ModelSpec::bytes_per_element
+  std::int64_t element_count() const;
+};
+
+struct ModelSpec {
+  std::string name;
+  int num_layers = 1;
+  std::vector<TensorSpec> tensors;
+  std::int64_t bytes_per_element = 4;
+  double state_multiplier = 16.0;
+
+  std::int64_t element_bytes(const TensorSpec& t) const {
+    return t.element_bytes > 0 ? t.element_bytes : bytes_per_element;
+  }
+  std::int64_t total_param_elements() const;
+  double total_state_bytes() const;
+  std::int64_t total_tensor_bytes() const;
+  std::vector<std::string> validate() const;
+
+  // Shared spec text ("model ... / tensor ..." records); see specs.py.
+  static ModelSpec parse(const std::string& text);  // throws std::invalid_argument
+  std::string to_text() const;
+};
+
+struct RankCoord {
+  int tp = 0;
+  int pp = 0;
+  int dp = 0;
+  bool operator==(const RankCoord&) const = default;
+};
+
+// Rank-list position i -> tp = i % tp, dp = (i / tp) % dp, pp = i / (tp*dp).
+class ParallelConfig {
+ public:
+  ParallelConfig() = default;
+  ParallelConfig(std::uint64_t generation_id, int tp, int pp, int dp, std::vector<int> ranks,
+                 std::vector<int> layer_assignment);
+  static std::vector<int> default_layer_assignment(int num_layers, int pp);
+
+  std::uint64_t generation_id() const { return gen_; }
+  int tp() const { return tp_; }
+  int pp() const { return pp_; }
+  int dp() const { return dp_; }
+  int world_size() const { return static_cast<int>(ranks_.size()); }
+  const std::vector<int>& ranks() const { return ranks_; }
+  const std::vector<int>& layer_assignment() const { return stage_of_; }
+
+  bool contains(int rank) const { return index_.count(rank) != 0; }
+  int index_of(int rank) const;  // throws std::invalid_argument
+  RankCoord coord_of(int rank) const;
+  int rank_at(const RankCoord& c) const;
+  int stage_of_layer(int layer) const;
+  std::vector<int> stage_ranks(int stage) const;
+  bool same_layout(const ParallelConfig& o) const;
+  ParallelConfig with_generation(std::uint64_t gen) const;
+
+ private:
+  std::uint64_t gen_ = 0;
+  int tp_ = 1, pp_ = 1, dp_ = 1;
+  std::vector<int> ranks_;
+  std::vector<int> stage_of_;
+  std::unordered_map<int, int> index_;  // rank id -> position (first occurrence)
+};
+
+std::vector<std::string> validate_config(const ParallelConfig& config, const ModelSpec& model);
+
+std::optional<Interval> tp_block(std::int64_t axis_len, int tp_degree, int tp_index);
+std::optional<ShardView> view(const TensorSpec& tensor, const ParallelConfig& config, int rank);
+std::map<int, ShardView> owners(const TensorSpec& tensor, const ParallelConfig& config);
+
+struct TransferTask {
+  std::uint32_t tensor_index = 0;
+  int layer = 0;
+  int src_rank = 0;
+  int dst_rank = 0;
+  ShardView bounds;
+  std::int64_t byte_size = 0;
+  bool is_local() const { return src_rank == dst_rank; }
+};
+
+struct CarryoverRegion {
+  std::uint32_t tensor_index = 0;
+  int layer = 0;
+  int rank = 0;
+  ShardView bounds;
+  std::int64_t byte_size = 0;
+};
+
+struct LinkKey {
+  int src = 0;
+  int dst = 0;
+  bool operator<(const LinkKey& o) const { return src != o.src ? src < o.src : dst < o.dst; }
+  bool operator==(const LinkKey&) const = default;
+};
+
+class TransferPlan {
+ public:
+  std::uint64_t src_config_gen = 0;
+  std::uint64_t dst_config_gen = 0;
+  std::vector<std::string> tensor_ids;
+  std::map<int, std::vector<TransferTask>> tasks_by_layer;
+  std::map<int, std::vector<CarryoverRegion>> carryover_by_layer;
+
+  std::int64_t total_bytes() const;
+  std::int64_t task_count() const;
+  std::map<LinkKey, std::int64_t> per_link_bytes() const;
+  bool empty() const { return task_count() == 0; }
+  const std::string& tensor_id(std::uint32_t index) const { return tensor_ids.at(index); }
+};
+
+struct PlanCostSummary {
+  std::int64_t total_bytes = 0;
+  std::int64_t max_link_bytes = 0;
+  std::int64_t task_count = 0;
+};
+
+PlanCostSummary plan_cost_summary(const TransferPlan& plan);
+void write_plan(std::ostream& os, const TransferPlan& plan);
+TransferPlan read_plan(std::istream& is);
+
+struct PlanOptions {
+  bool balance_sources = false;
+};
+
+struct PlannerStats {
+  std::int64_t pairs_checked = 0;
+};
+
+TransferPlan compute_transfer_plan(const ParallelConfig& c_old, const ParallelConfig& c_new,
+                                   const ModelSpec& model, const PlanOptions& options = {},
+                                   PlannerStats* stats = nullptr);
+
+// Exact completeness check (same verdicts and messages as the reference's
+// brute-force oracle) computed on a coordinate-compressed cell grid, so it
+// runs on full-size plans in milliseconds instead of O(elements).
+std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelConfig& c_old,
+                                     const ParallelConfig& c_new, const ModelSpec& model);
+
+std::vector<ShardView> chunk_bounds(const ShardView& bounds, std::int64_t max_bytes,
+                                    std::int64_t bytes_per_element);
+
+}  // namespace reshard

@@ -1,0 +1,162 @@
+/*
+ * rs_reshard.h -- C ABI of the B200-native live-handoff reshard path
+ * (libreshard_b200.so).  Plain pointers and sizes only; no exceptions cross
+ * it.  Status codes mirror the SPEC exit classes:
+ *   RS_OK 0, RS_EDOMAIN 1 (validation / bad argument),
+ *   RS_EINTEGRITY 2 (plan or data integrity), RS_ESYSTEM 3 (CUDA / system).
+ * rs_last_error() returns the calling thread's last message.
+ *
+ * Entry points and the reference interface each one replaces:
+ *   rs_plan_compute    compute_transfer_plan   proj/include/reshard/planner.hpp:35-38
+ *   rs_plan_verify     verify_plan             proj/include/reshard/planner.hpp:44-47
+ *   rs_plan_write      write_plan              proj/include/reshard/transfer_plan.hpp:81
+ *   rs_plan_read       read_plan               proj/include/reshard/transfer_plan.hpp:82
+ *   rs_plan_summary    plan_cost_summary       proj/include/reshard/transfer_plan.hpp:77
+ *   rs_validate_config validate_config         proj/include/reshard/parallel_config.hpp:73-74
+ *   rs_view            view / tp_block         proj/include/reshard/topology.hpp:20-25
+ *   rs_chunk_bounds    chunk_bounds            proj/include/reshard/executor.hpp:43-44
+ *   rs_engine_create   Transport (+ staging B) proj/include/reshard/transport.hpp:25-48
+ *   rs_store_*         ShardStore              proj/include/reshard/shard_store.hpp:19-47
+ *   rs_fill_pattern    ShardStore::fill_pattern proj/include/reshard/shard_store.hpp:34
+ *   rs_verify_pattern  gather-reslice oracle compare (SPEC.md cmd_verify)
+ *   rs_execute         execute_plan            proj/include/reshard/executor.hpp:50-53
+ *   rs_execute_host    execute_plan on host ShardStore buffers (H2D/D2H inside)
+ */
+#ifndef RS_RESHARD_H
+#define RS_RESHARD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_OK 0
+#define RS_EDOMAIN 1
+#define RS_EINTEGRITY 2
+#define RS_ESYSTEM 3
+
+#define RS_SRC 0 /* store of the source configuration C_old */
+#define RS_DST 1 /* store of the destination configuration C_new */
+
+#define RS_MODE_DIRECT 0 /* every byte moved straight src -> dst (peer stores), zero staging */
+#define RS_MODE_STAGED 1 /* remote frames through bounded per-link staging rings */
+
+typedef struct rs_plan rs_plan;
+typedef struct rs_engine rs_engine;
+
+typedef struct {
+  uint64_t generation_id;
+  int32_t tp, pp, dp;
+  int32_t num_ranks;
+  const int32_t* ranks;       /* ordered rank ids (placement is semantic) */
+  const int32_t* layer_stage; /* num_layers entries, or NULL: default ceil split */
+} rs_config;
+
+typedef struct {
+  int32_t balance_sources;
+} rs_plan_options;
+
+typedef struct {
+  int64_t total_bytes;     /* remote + local task bytes (TransferPlan::total_bytes) */
+  int64_t max_link_bytes;  /* max over remote (src,dst) links */
+  int64_t task_count;
+  int64_t remote_bytes;
+  int64_t local_bytes;
+  int64_t carryover_bytes;
+  int64_t carryover_count;
+  int64_t pairs_checked;
+  int32_t num_tensors;
+  int32_t num_layers_with_work;
+} rs_plan_summary_t;
+
+typedef struct {
+  int32_t num_devices;      /* CUDA ordinals this process drives */
+  const int32_t* device_ids;
+  int64_t staging_bytes;    /* per-destination-rank staging budget B */
+  int32_t mode;             /* RS_MODE_* */
+  int32_t slots_per_link;   /* ring depth K (>= 2), STAGED */
+  int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
+  int32_t strict_layers;    /* 1: one launch per layer (layer barrier), 0: fused */
+  int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
+  int32_t blocks_per_sm;    /* 0: occupancy maximum */
+  int32_t reserved;
+} rs_engine_options;
+
+typedef struct {
+  int32_t ok;
+  int32_t failed_layer;       /* -1: none */
+  int64_t peak_staging_bytes; /* max over destination ranks of resident ring capacity */
+  int64_t bytes_moved;        /* remote (cross-rank) task bytes */
+  int64_t local_copy_bytes;   /* local task bytes */
+  int64_t carryover_bytes;    /* carryover bytes materialised */
+  int32_t layers_processed;
+  int32_t kernel_launches;
+  double device_ms;           /* CUDA-event time of the run on the slowest device */
+  double host_ms;             /* host wall time of the call */
+  char error[512];
+} rs_exec_report;
+
+const char* rs_last_error(void);
+const char* rs_version(void);
+
+/* ----------------------------------------------------------------- planning */
+int rs_validate_config(const char* model_spec, const rs_config* cfg, char* buf, size_t cap,
+                       size_t* needed, int32_t* num_violations);
+int rs_view(const char* model_spec, const rs_config* cfg, int32_t tensor_index, int32_t rank,
+            int64_t* lo, int64_t* hi, int32_t* present);
+int rs_plan_compute(const char* model_spec, const rs_config* c_old, const rs_config* c_new,
+                    const rs_plan_options* opts, rs_plan** out);
+int rs_plan_read(const char* model_spec, const char* plan_text, rs_plan** out);
+int rs_plan_write(const rs_plan* plan, char* buf, size_t cap, size_t* needed);
+int rs_plan_summary(const rs_plan* plan, rs_plan_summary_t* out);
+int rs_plan_verify(const rs_plan* plan, const rs_config* c_old, const rs_config* c_new, char* buf,
+                   size_t cap, size_t* needed, int32_t* num_violations);
+void rs_plan_destroy(rs_plan* plan);
+int rs_chunk_bounds(int32_t ndims, const int64_t* lo, const int64_t* hi, int64_t max_bytes,
+                    int64_t bytes_per_element, int64_t* out_lo, int64_t* out_hi, int64_t cap,
+                    int64_t* count);
+
+/* ------------------------------------------------------------------- engine */
+int rs_engine_create(const rs_engine_options* opts, rs_engine** out);
+void rs_engine_destroy(rs_engine* e);
+
+/* Shard stores.  rank_device[i] = engine device slot of cfg->ranks[i]. */
+int rs_store_layout(rs_engine* e, int32_t which, const char* model_spec, const rs_config* cfg,
+                    const int32_t* rank_device);
+int rs_store_alloc(rs_engine* e, int32_t which);      /* one arena per device */
+int rs_store_bind(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, void* dptr,
+                  int64_t nbytes);                     /* caller-owned device memory */
+int rs_store_ptr(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, void** dptr,
+                 int64_t* nbytes);
+int rs_store_bytes(rs_engine* e, int32_t which, int64_t* total);
+int rs_store_read(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, int64_t offset,
+                  int64_t nbytes, void* host);
+int rs_store_write(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index,
+                   int64_t offset, int64_t nbytes, const void* host);
+int rs_store_free(rs_engine* e, int32_t which);
+
+int rs_fill_pattern(rs_engine* e, int32_t which, uint64_t seed);
+int rs_verify_pattern(rs_engine* e, int32_t which, uint64_t seed, int64_t* mismatches,
+                      int64_t* first_bad_entry);
+
+/* --------------------------------------------------------------- execution */
+int rs_prepare(rs_engine* e, const rs_plan* plan);  /* compile + upload work lists */
+int rs_run(rs_engine* e, rs_exec_report* report);   /* launch + wait */
+int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
+
+/* Host-resident stores: host_src[k] / host_dst[k] follow the (tensor, ascending
+ * rank) entry order of the src / dst layout.  Each layer's source shards are
+ * copied H2D, resharded on the device, and the destination shards copied D2H,
+ * pipelined across layers on separate streams; device memory is bounded by a
+ * window of layers.  Requires a prepared plan and laid-out (not allocated)
+ * stores. */
+int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
+                    void* const* host_dst, int32_t window_layers, rs_exec_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RS_RESHARD_H */

@@ -1,0 +1,335 @@
+// extern "C" boundary of libreshard_b200.so (include/rs_reshard.h).
+// Exceptions never cross it: std::invalid_argument / DomainError -> RS_EDOMAIN,
+// IntegrityError / plan parse errors -> RS_EINTEGRITY, SystemError (CUDA) ->
+// RS_ESYSTEM; the message is kept per thread for rs_last_error().
+#include <cstring>
+#include <memory>
+#include <set>
+#include <sstream>
+#include <string>
+
+#include "engine/engine.hpp"
+#include "reshard_b200/reshard.hpp"
+#include "rs_reshard.h"
+
+struct rs_plan {
+  reshard::ModelSpec model;
+  reshard::TransferPlan plan;
+  std::int64_t pairs_checked = 0;
+};
+
+struct rs_engine {
+  explicit rs_engine(const rs_engine_options& o) : impl(o) {}
+  rsb::Engine impl;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_error.clear();
+    return RS_OK;
+  } catch (const rsb::SystemError& e) {
+    g_error = e.what();
+    return RS_ESYSTEM;
+  } catch (const rsb::IntegrityError& e) {
+    g_error = e.what();
+    return RS_EINTEGRITY;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return RS_EDOMAIN;
+  } catch (const std::out_of_range& e) {
+    g_error = e.what();
+    return RS_EDOMAIN;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return RS_ESYSTEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return RS_EINTEGRITY;
+  }
+}
+
+reshard::ParallelConfig to_config(const rs_config* c, int num_layers) {
+  if (!c) throw std::invalid_argument("null config");
+  if (c->num_ranks < 0 || (c->num_ranks > 0 && !c->ranks)) throw std::invalid_argument("config: bad rank list");
+  std::vector<int> ranks(c->ranks, c->ranks + c->num_ranks);
+  std::vector<int> stages = c->layer_stage ? std::vector<int>(c->layer_stage, c->layer_stage + num_layers)
+                                           : reshard::ParallelConfig::default_layer_assignment(num_layers, c->pp);
+  return reshard::ParallelConfig(c->generation_id, c->tp, c->pp, c->dp, std::move(ranks), std::move(stages));
+}
+
+// Copies s into buf (truncating); *needed is the full size incl. the NUL.
+void put_text(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_error.c_str(); }
+const char* rs_version(void) { return "reshard_b200 0.1 (sm_100a)"; }
+
+int rs_validate_config(const char* model_spec, const rs_config* cfg, char* buf, size_t cap, size_t* needed,
+                       int32_t* num_violations) {
+  return guarded([&] {
+    auto m = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    auto v = reshard::validate_config(to_config(cfg, m.num_layers), m);
+    std::string s;
+    for (auto& x : v) s += x + "\n";
+    if (num_violations) *num_violations = static_cast<int32_t>(v.size());
+    put_text(s, buf, cap, needed);
+  });
+}
+
+int rs_view(const char* model_spec, const rs_config* cfg, int32_t tensor_index, int32_t rank, int64_t* lo,
+            int64_t* hi, int32_t* present) {
+  return guarded([&] {
+    auto m = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    if (tensor_index < 0 || tensor_index >= static_cast<int32_t>(m.tensors.size()))
+      throw std::invalid_argument("tensor index out of range");
+    auto v = reshard::view(m.tensors[static_cast<std::size_t>(tensor_index)], to_config(cfg, m.num_layers), rank);
+    *present = v.has_value();
+    if (v)
+      for (std::size_t i = 0; i < v->ndims(); ++i) {
+        lo[i] = v->dim(i).lo;
+        hi[i] = v->dim(i).hi;
+      }
+  });
+}
+
+int rs_plan_compute(const char* model_spec, const rs_config* c_old, const rs_config* c_new,
+                    const rs_plan_options* opts, rs_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<rs_plan>();
+    p->model = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    if (auto v = p->model.validate(); !v.empty()) throw std::invalid_argument("model: " + v.front());
+    reshard::PlanOptions o;
+    o.balance_sources = opts && opts->balance_sources;
+    reshard::PlannerStats st;
+    p->plan = reshard::compute_transfer_plan(to_config(c_old, p->model.num_layers),
+                                             to_config(c_new, p->model.num_layers), p->model, o, &st);
+    p->pairs_checked = st.pairs_checked;
+    *out = p.release();
+  });
+}
+
+int rs_plan_read(const char* model_spec, const char* plan_text, rs_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<rs_plan>();
+    p->model = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    std::istringstream is(plan_text ? plan_text : "");
+    reshard::TransferPlan parsed = reshard::read_plan(is);
+    // read_plan interns ids in appearance order; re-index by name against the
+    // model so store lookups use model tensor indices (SURVEY.md §8c caveat)
+    std::vector<std::uint32_t> remap(parsed.tensor_ids.size(), 0);
+    for (std::size_t pi = 0; pi < parsed.tensor_ids.size(); ++pi) {
+      bool found = false;
+      for (std::size_t mi = 0; mi < p->model.tensors.size(); ++mi)
+        if (p->model.tensors[mi].tensor_id == parsed.tensor_ids[pi]) {
+          remap[pi] = static_cast<std::uint32_t>(mi);
+          found = true;
+        }
+      if (!found) throw std::invalid_argument("plan references unknown tensor " + parsed.tensor_ids[pi]);
+    }
+    p->plan = parsed;
+    p->plan.tensor_ids.clear();
+    for (const auto& t : p->model.tensors) p->plan.tensor_ids.push_back(t.tensor_id);
+    for (auto& kv : p->plan.tasks_by_layer)
+      for (auto& t : kv.second) t.tensor_index = remap[t.tensor_index];
+    for (auto& kv : p->plan.carryover_by_layer)
+      for (auto& k : kv.second) k.tensor_index = remap[k.tensor_index];
+    *out = p.release();
+  });
+}
+
+int rs_plan_write(const rs_plan* plan, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (!plan) throw std::invalid_argument("null plan");
+    std::ostringstream os;
+    reshard::write_plan(os, plan->plan);
+    put_text(os.str(), buf, cap, needed);
+  });
+}
+
+int rs_plan_summary(const rs_plan* plan, rs_plan_summary_t* out) {
+  return guarded([&] {
+    if (!plan || !out) throw std::invalid_argument("null argument");
+    const auto s = reshard::plan_cost_summary(plan->plan);
+    *out = rs_plan_summary_t{};
+    out->total_bytes = s.total_bytes;
+    out->max_link_bytes = s.max_link_bytes;
+    out->task_count = s.task_count;
+    out->pairs_checked = plan->pairs_checked;
+    out->num_tensors = static_cast<int32_t>(plan->plan.tensor_ids.size());
+    std::set<int> layers;
+    for (const auto& kv : plan->plan.tasks_by_layer) {
+      layers.insert(kv.first);
+      for (const auto& t : kv.second) (t.is_local() ? out->local_bytes : out->remote_bytes) += t.byte_size;
+    }
+    for (const auto& kv : plan->plan.carryover_by_layer) {
+      layers.insert(kv.first);
+      for (const auto& k : kv.second) {
+        out->carryover_bytes += k.byte_size;
+        out->carryover_count++;
+      }
+    }
+    out->num_layers_with_work = static_cast<int32_t>(layers.size());
+  });
+}
+
+int rs_plan_verify(const rs_plan* plan, const rs_config* c_old, const rs_config* c_new, char* buf, size_t cap,
+                   size_t* needed, int32_t* num_violations) {
+  return guarded([&] {
+    if (!plan) throw std::invalid_argument("null plan");
+    const int L = plan->model.num_layers;
+    auto v = reshard::verify_plan(plan->plan, to_config(c_old, L), to_config(c_new, L), plan->model);
+    std::string s;
+    for (auto& x : v) s += x + "\n";
+    if (num_violations) *num_violations = static_cast<int32_t>(v.size());
+    put_text(s, buf, cap, needed);
+  });
+}
+
+void rs_plan_destroy(rs_plan* plan) { delete plan; }
+
+int rs_chunk_bounds(int32_t ndims, const int64_t* lo, const int64_t* hi, int64_t max_bytes, int64_t bpe,
+                    int64_t* out_lo, int64_t* out_hi, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    std::vector<reshard::Interval> b;
+    for (int32_t i = 0; i < ndims; ++i) b.push_back({lo[i], hi[i]});
+    auto pieces = reshard::chunk_bounds(reshard::ShardView(b), max_bytes, bpe);
+    *count = static_cast<int64_t>(pieces.size());
+    for (std::size_t p = 0; p < pieces.size() && static_cast<int64_t>(p) < cap; ++p)
+      for (int32_t i = 0; i < ndims; ++i) {
+        out_lo[p * static_cast<std::size_t>(ndims) + static_cast<std::size_t>(i)] = pieces[p].dim(static_cast<std::size_t>(i)).lo;
+        out_hi[p * static_cast<std::size_t>(ndims) + static_cast<std::size_t>(i)] = pieces[p].dim(static_cast<std::size_t>(i)).hi;
+      }
+  });
+}
+
+int rs_engine_create(const rs_engine_options* opts, rs_engine** out) {
+  return guarded([&] {
+    if (!opts || !out) throw std::invalid_argument("null argument");
+    *out = new rs_engine(*opts);
+  });
+}
+
+void rs_engine_destroy(rs_engine* e) { delete e; }
+
+int rs_store_layout(rs_engine* e, int32_t which, const char* model_spec, const rs_config* cfg,
+                    const int32_t* rank_device) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    auto m = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    auto c = to_config(cfg, m.num_layers);
+    std::vector<int> rd(static_cast<std::size_t>(c.world_size()), 0);
+    if (rank_device)
+      for (std::size_t i = 0; i < rd.size(); ++i) rd[i] = rank_device[i];
+    e->impl.layout(which, m, c, rd);
+  });
+}
+
+int rs_store_alloc(rs_engine* e, int32_t which) {
+  return guarded([&] { e->impl.alloc(which); });
+}
+
+int rs_store_free(rs_engine* e, int32_t which) {
+  return guarded([&] { e->impl.free_store(which); });
+}
+
+int rs_store_bind(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, void* dptr, int64_t nbytes) {
+  return guarded([&] { e->impl.bind(which, rank, static_cast<std::uint32_t>(tensor_index), dptr, nbytes); });
+}
+
+int rs_store_ptr(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, void** dptr, int64_t* nbytes) {
+  return guarded([&] {
+    const rsb::Entry* en = e->impl.store(which).find(rank, static_cast<std::uint32_t>(tensor_index));
+    if (!en) throw std::invalid_argument("shard store: no buffer for rank " + std::to_string(rank) + " tensor " +
+                                         std::to_string(tensor_index));
+    *dptr = en->ptr;
+    *nbytes = en->nbytes;
+  });
+}
+
+int rs_store_bytes(rs_engine* e, int32_t which, int64_t* total) {
+  return guarded([&] { *total = e->impl.store(which).total_bytes(); });
+}
+
+int rs_store_read(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, int64_t offset, int64_t nbytes,
+                  void* host) {
+  return guarded([&] {
+    const rsb::Entry* en = e->impl.store(which).find(rank, static_cast<std::uint32_t>(tensor_index));
+    if (!en || !en->ptr) throw std::invalid_argument("store read: no such entry");
+    if (offset < 0 || nbytes < 0 || offset + nbytes > en->nbytes) throw std::invalid_argument("store read: out of range");
+    rsb::cuda_check(cudaMemcpy(host, en->ptr + offset, static_cast<std::size_t>(nbytes), cudaMemcpyDeviceToHost),
+                    "store read");
+  });
+}
+
+int rs_store_write(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, int64_t offset, int64_t nbytes,
+                   const void* host) {
+  return guarded([&] {
+    const rsb::Entry* en = e->impl.store(which).find(rank, static_cast<std::uint32_t>(tensor_index));
+    if (!en || !en->ptr) throw std::invalid_argument("store write: no such entry");
+    if (offset < 0 || nbytes < 0 || offset + nbytes > en->nbytes) throw std::invalid_argument("store write: out of range");
+    rsb::cuda_check(cudaMemcpy(en->ptr + offset, host, static_cast<std::size_t>(nbytes), cudaMemcpyHostToDevice),
+                    "store write");
+  });
+}
+
+int rs_fill_pattern(rs_engine* e, int32_t which, uint64_t seed) {
+  return guarded([&] { e->impl.fill_pattern(which, seed); });
+}
+
+int rs_verify_pattern(rs_engine* e, int32_t which, uint64_t seed, int64_t* mismatches, int64_t* first_bad_entry) {
+  return guarded([&] {
+    std::int64_t first = -1;
+    *mismatches = e->impl.verify_pattern(which, seed, &first);
+    if (first_bad_entry) *first_bad_entry = first;
+  });
+}
+
+int rs_prepare(rs_engine* e, const rs_plan* plan) {
+  return guarded([&] {
+    if (!e || !plan) throw std::invalid_argument("null argument");
+    e->impl.prepare(plan->plan);
+  });
+}
+
+int rs_run(rs_engine* e, rs_exec_report* report) {
+  return guarded([&] {
+    *report = e->impl.run();
+    if (!report->ok) throw rsb::IntegrityError(report->error);
+  });
+}
+
+int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report) {
+  return guarded([&] {
+    e->impl.prepare(plan->plan);
+    *report = e->impl.run();
+    if (!report->ok) throw rsb::IntegrityError(report->error);
+  });
+}
+
+int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src, void* const* host_dst,
+                    int32_t window_layers, rs_exec_report* report) {
+  return guarded([&] {
+    if (!e || !plan || !host_src || !host_dst) throw std::invalid_argument("null argument");
+    e->impl.prepare(plan->plan);
+    *report = e->impl.run_host(host_src, host_dst, window_layers);
+    if (!report->ok) throw rsb::IntegrityError(report->error);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Device work descriptors shared by the host descriptor compiler
+// (compile.cpp) and the sm_100a kernels (kernels.cu).  Plain C layout.
+//
+// A CopyDesc is one strided->strided byte copy of a sub-box between two
+// row-major shard buffers, after dimension coalescing: `rows` contiguous runs
+// of `row_bytes`, the run start of row r given by decomposing r over up to
+// RS_MAX_OUTER outer extents (innermost first) with independent source and
+// destination byte strides.  This one shape covers the reference's
+// slice_local (strided -> packed), scatter_local (packed -> strided), the local
+// task / carryover copy (strided -> strided) and ring pack/unpack
+// (proj/src/executor.cpp:23-93).
+#pragma once
+#include <stdint.h>
+
+#define RS_MAX_OUTER 4
+
+typedef struct {
+  uint64_t src;           // byte address of row 0 (local or peer-mapped)
+  uint64_t dst;
+  uint64_t row_bytes;     // contiguous run length
+  uint64_t rows;          // product of ext[0..nouter)
+  uint64_t item0;         // global index of this descriptor's first work item
+  uint64_t ext[RS_MAX_OUTER];
+  int64_t sstr[RS_MAX_OUTER];
+  int64_t dstr[RS_MAX_OUTER];
+  uint32_t rows_per_item;
+  uint32_t nouter;
+  uint32_t vec_log2;      // access width: 1 << vec_log2 bytes (0..4)
+  uint32_t tag;           // layer (diagnostics)
+} rs_copy_desc;
+
+// Synthetic-state descriptor: one shard buffer (row-major over its view),
+// filled with / checked against the reference pattern
+// byte b of global element g of tensor ti =
+//   byte (b % 8) of splitmix64(seed ^ 0x1000003*ti ^ g)   (shard_store.cpp:51-56)
+typedef struct {
+  uint64_t ptr;           // buffer base
+  uint64_t row_elems;     // elements per (coalesced) row
+  uint64_t rows;
+  uint64_t item0;
+  int64_t g0;             // global element index of the view origin
+  uint64_t ext[RS_MAX_OUTER];   // outer extents, innermost first
+  int64_t gstr[RS_MAX_OUTER];   // global element strides of the outer dims
+  uint32_t rows_per_item;
+  uint32_t nouter;
+  uint32_t elem_bytes;
+  uint32_t tensor_index;
+  uint32_t entry;         // store entry id (mismatch reporting)
+  uint32_t pad;
+} rs_pattern_desc;
+
+// Ring-staged transfer (STAGED mode): a batch is the set of frames packed
+// into one ring slot; frames are CopyDescs whose destination (pack) or source
+// (unpack) is the slot.  One lane = one single-producer / single-consumer ring
+// between a sender CTA and a receiver CTA.
+typedef struct {
+  uint64_t slot_base;       // lane's slot 0 address (receiver memory, as mapped for the sender)
+  uint64_t slot_base_rx;    // same slots as addressed by the receiver
+  uint64_t slot_bytes;
+  uint64_t ready_flags;     // uint64[slots] in receiver memory (sender addressing)
+  uint64_t ready_flags_rx;  // receiver addressing
+  uint64_t credit_flags;    // uint64[slots] in sender memory (receiver addressing)
+  uint64_t credit_flags_tx; // sender addressing
+  uint32_t slots;
+  uint32_t nbatches;
+  uint32_t batch0;          // index of the lane's first batch in the batch table
+  uint32_t pad;
+} rs_lane_desc;
+
+typedef struct {
+  uint32_t pack0, npack;     // frame descriptors packing into the slot (sender side)
+  uint32_t unpack0, nunpack; // frame descriptors unpacking out of the slot (receiver side)
+  uint64_t bytes;            // payload bytes in this batch
+} rs_batch_desc;

@@ -1,0 +1,140 @@
+// Device reshard engine: shard stores on one or more GPUs driven by this
+// process, plan compilation into per-device work lists, and execution.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "desc.h"
+#include "reshard_b200/reshard.hpp"
+#include "rs_reshard.h"
+
+namespace rsb {
+
+struct DomainError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct IntegrityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct SystemError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+// Device allocation owned by the engine.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(int device, std::size_t bytes);
+  ~DeviceBuffer();
+  DeviceBuffer(DeviceBuffer&& o) noexcept { *this = std::move(o); }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  char* data() const { return ptr_; }
+  std::size_t size() const { return bytes_; }
+  void upload(const void* host, std::size_t bytes, cudaStream_t s);
+
+ private:
+  int device_ = -1;
+  char* ptr_ = nullptr;
+  std::size_t bytes_ = 0;
+};
+
+struct Entry {
+  std::uint32_t ti = 0;
+  int rank = 0;
+  int dev = 0;  // engine device slot
+  reshard::ShardView view;
+  std::int64_t nbytes = 0;
+  char* ptr = nullptr;
+};
+
+struct Store {
+  bool laid_out = false;
+  reshard::ModelSpec model;
+  reshard::ParallelConfig config;
+  std::vector<Entry> entries;  // (tensor, ascending rank)
+  std::unordered_map<std::uint64_t, std::uint32_t> index;
+  std::vector<DeviceBuffer> arenas;  // engine-owned memory (rs_store_alloc)
+  const Entry* find(int rank, std::uint32_t ti) const;
+  Entry* find(int rank, std::uint32_t ti);
+  std::int64_t total_bytes() const;
+};
+
+struct LayerRange {
+  int layer;
+  std::uint64_t item_begin, item_end;  // copy items of this layer (per device)
+};
+
+// Per-device compiled work.
+struct DeviceProgram {
+  std::vector<rs_copy_desc> local;  // DIRECT copies executed here
+  std::vector<std::uint64_t> local_item0;
+  std::uint64_t local_items = 0;
+  std::vector<LayerRange> layers;
+  // STAGED
+  std::vector<rs_lane_desc> lanes;
+  std::vector<rs_batch_desc> batches;
+  std::vector<rs_copy_desc> frames;
+  DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error;
+  std::uint64_t local_bytes = 0;  // bytes this device moves in local descriptors
+};
+
+struct Device {
+  int ordinal = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+};
+
+class Engine {
+ public:
+  explicit Engine(const rs_engine_options& opts);
+  ~Engine();
+
+  void layout(int which, const reshard::ModelSpec& model, const reshard::ParallelConfig& cfg,
+              const std::vector<int>& rank_device);
+  void alloc(int which);
+  void free_store(int which);
+  void bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t nbytes);
+  const Store& store(int which) const { return stores_[which]; }
+  Store& store(int which) { return stores_[which]; }
+
+  void fill_pattern(int which, std::uint64_t seed);
+  std::int64_t verify_pattern(int which, std::uint64_t seed, std::int64_t* first_bad);
+
+  void prepare(const reshard::TransferPlan& plan);
+  rs_exec_report run();
+  rs_exec_report run_host(void* const* host_src, void* const* host_dst, int window_layers);
+
+  int num_devices() const { return static_cast<int>(devices_.size()); }
+
+ private:
+  void compile_direct(const reshard::TransferPlan& plan);
+  void compile_staged(const reshard::TransferPlan& plan);
+  void upload_programs();
+  int grid_for(int dev, int which_kernel) const;
+  void check_stores_ready() const;
+
+  rs_engine_options opts_{};
+  std::vector<Device> devices_;
+  Store stores_[2];
+  std::vector<DeviceProgram> programs_;
+  std::vector<DeviceBuffer> rings_;  // staging memory per device
+  std::vector<int> staged_tx_, staged_rx_;  // ring lanes sent / received per device
+  bool prepared_ = false;
+  std::uint64_t epoch_ = 0;
+  // compile-time report fields (reference semantics, see prepare())
+  rs_exec_report planned_{};
+  std::vector<int> plan_layers_;
+};
+
+}  // namespace rsb

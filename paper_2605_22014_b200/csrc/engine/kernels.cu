@@ -1,0 +1,479 @@
+// sm_100a kernels of the reshard engine.
+//
+//   rs_copy_kernel     batched strided->strided byte copy over rs_copy_desc
+//                      work lists (pack / unpack / relayout / carryover;
+//                      proj/src/executor.cpp:23-93 + :142-166 on the device).
+//                      Warp-granular persistent loop, 16 B vector accesses,
+//                      U independent loads in flight per lane.
+//   rs_pattern_kernel  synthetic state fill / verify against the reference
+//                      pattern (proj/src/shard_store.cpp:12-85), one hash per
+//                      element, 16 B stores / compares.
+//   rs_exchange_kernel ring-staged transfer: sender warps pack frames into the
+//                      receiver's staging slots (peer stores over NVLink when
+//                      the receiver is another GPU), publish with a .sys
+//                      release flag; receiver warps acquire, unpack, return a
+//                      credit (bounded staging, proj/src/executor.cpp:183-206).
+//
+// Everything is integer/byte movement: no floating point touches the data.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "desc.h"
+#include "kernels.h"
+
+namespace {
+
+constexpr int kUnroll = 4;
+
+// ---------------------------------------------------------------- accesses
+
+// Read-only path (L1 no-allocate): for shard buffers that nothing writes
+// during the launch.
+template <typename T, bool kReadOnly>
+__device__ __forceinline__ T load(const T* p);
+
+template <>
+__device__ __forceinline__ uint4 load<uint4, true>(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// Coherent-at-L2 path: staging slots written by another SM / GPU.
+template <>
+__device__ __forceinline__ uint4 load<uint4, false>(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 load<uint2, true>(const uint2* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint2 load<uint2, false>(const uint2* p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ uint32_t load<uint32_t, true>(const uint32_t* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint32_t load<uint32_t, false>(const uint32_t* p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ uint16_t load<uint16_t, true>(const uint16_t* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint16_t load<uint16_t, false>(const uint16_t* p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ uint8_t load<uint8_t, true>(const uint8_t* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint8_t load<uint8_t, false>(const uint8_t* p) { return __ldcg(p); }
+
+template <typename T>
+__device__ __forceinline__ void store(T* p, const T& v) { *p = v; }
+template <>
+__device__ __forceinline__ void store<uint4>(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// One warp copies one contiguous run: lanes stride T-sized vectors, kUnroll
+// loads issued before their stores.
+template <typename T, bool kReadOnly>
+__device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64_t nbytes,
+                                              int lane) {
+  const T* s = reinterpret_cast<const T*>(src);
+  T* d = reinterpret_cast<T*>(dst);
+  const uint64_t n = nbytes / sizeof(T);
+  uint64_t i = static_cast<uint64_t>(lane);
+  for (; i + 32 * (kUnroll - 1) < n; i += 32 * kUnroll) {
+    T v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = load<T, kReadOnly>(s + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) store<T>(d + i + 32 * u, v[u]);
+  }
+  for (; i < n; i += 32) store<T>(d + i, load<T, kReadOnly>(s + i));
+}
+
+template <bool kReadOnly>
+__device__ __forceinline__ void warp_copy_any(const char* src, char* dst, uint64_t nbytes,
+                                              uint32_t vec_log2, int lane) {
+  switch (vec_log2) {
+    case 4: warp_copy_run<uint4, kReadOnly>(src, dst, nbytes, lane); break;
+    case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane); break;
+    case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane); break;
+    case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane); break;
+    default: warp_copy_run<uint8_t, kReadOnly>(src, dst, nbytes, lane); break;
+  }
+}
+
+// Largest i with item0[i] <= item (item0 ascending, item0[0] == 0).
+__device__ __forceinline__ uint32_t find_desc(const uint64_t* __restrict__ item0, uint32_t n,
+                                              uint64_t item) {
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(item0 + mid) <= item) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Byte offsets of row r: decompose r over the outer extents (32-bit: the
+// compiler guarantees every extent and row count fits, see compile.cpp).
+__device__ __forceinline__ void row_offsets(const rs_copy_desc& D, uint32_t r, int64_t& so,
+                                            int64_t& dof) {
+  so = 0;
+  dof = 0;
+  for (uint32_t k = 0; k < D.nouter; ++k) {
+    const uint32_t e = static_cast<uint32_t>(D.ext[k]);
+    const uint32_t q = r / e;
+    const uint32_t i = r - q * e;
+    so += static_cast<int64_t>(i) * D.sstr[k];
+    dof += static_cast<int64_t>(i) * D.dstr[k];
+    r = q;
+  }
+}
+
+template <bool kReadOnly>
+__device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t local_item,
+                                               int lane) {
+  const uint64_t r0 = local_item * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  const char* src = reinterpret_cast<const char*>(D.src);
+  char* dst = reinterpret_cast<char*>(D.dst);
+  for (uint64_t r = r0; r < r1; ++r) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    warp_copy_any<kReadOnly>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+  }
+}
+
+__global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __restrict__ descs,
+                                                      const uint64_t* __restrict__ item0,
+                                                      uint32_t ndesc, uint64_t item_begin,
+                                                      uint64_t item_end) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = item_begin + warp; item < item_end; item += nwarps) {
+    const uint32_t di = find_desc(item0, ndesc, item);
+    warp_copy_item<true>(descs[di], item - descs[di].item0, lane);
+  }
+}
+
+// ------------------------------------------------------------- pattern
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// 16 bytes of pattern starting at element g (elements of EB bytes, EB | 16).
+template <int EB>
+__device__ __forceinline__ uint4 pattern16(uint64_t base, int64_t g) {
+  uint32_t w[4];
+  if constexpr (EB == 8) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint64_t h = splitmix64(base ^ static_cast<uint64_t>(g + k));
+      w[2 * k] = static_cast<uint32_t>(h);
+      w[2 * k + 1] = static_cast<uint32_t>(h >> 32);
+    }
+  } else if constexpr (EB == 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = static_cast<uint32_t>(splitmix64(base ^ static_cast<uint64_t>(g + k)));
+  } else if constexpr (EB == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a = static_cast<uint32_t>(splitmix64(base ^ static_cast<uint64_t>(g + 2 * k))) & 0xffffu;
+      const uint32_t b = static_cast<uint32_t>(splitmix64(base ^ static_cast<uint64_t>(g + 2 * k + 1))) & 0xffffu;
+      w[k] = a | (b << 16);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v |= (static_cast<uint32_t>(splitmix64(base ^ static_cast<uint64_t>(g + 4 * k + j))) & 0xffu) << (8 * j);
+      w[k] = v;
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+
+template <int EB>
+__device__ __forceinline__ uint32_t mismatch_count16(const uint4& have, const uint4& want) {
+  const uint32_t hv[4] = {have.x, have.y, have.z, have.w};
+  const uint32_t wv[4] = {want.x, want.y, want.z, want.w};
+  uint32_t bad = 0;
+  if constexpr (EB == 8) {
+    bad += (hv[0] != wv[0]) | (hv[1] != wv[1]);
+    bad += (hv[2] != wv[2]) | (hv[3] != wv[3]);
+  } else if constexpr (EB == 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bad += hv[k] != wv[k];
+  } else if constexpr (EB == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = hv[k] ^ wv[k];
+      bad += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = hv[k] ^ wv[k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bad += ((x >> (8 * j)) & 0xffu) != 0;
+    }
+  }
+  return bad;
+}
+
+// One row of a pattern descriptor: g = global element index of the row start.
+template <int EB, bool kVerify>
+__device__ __forceinline__ uint32_t pattern_row_vec(char* row, uint64_t n_elems, uint64_t base,
+                                                    int64_t g, int lane) {
+  constexpr int kPer = 16 / EB;
+  const uint64_t nvec = n_elems / kPer;
+  uint4* p = reinterpret_cast<uint4*>(row);
+  uint32_t bad = 0;
+  for (uint64_t i = lane; i < nvec; i += 32) {
+    const uint4 want = pattern16<EB>(base, g + static_cast<int64_t>(i) * kPer);
+    if constexpr (kVerify) bad += mismatch_count16<EB>(__ldcg(p + i), want);
+    else p[i] = want;
+  }
+  // tail elements
+  for (uint64_t e = nvec * kPer + lane; e < n_elems; e += 32) {
+    const uint64_t h = splitmix64(base ^ static_cast<uint64_t>(g + static_cast<int64_t>(e)));
+    uint8_t* q = reinterpret_cast<uint8_t*>(row) + e * EB;
+    bool ok = true;
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      const uint8_t v = static_cast<uint8_t>(h >> ((b % 8) * 8));
+      if constexpr (kVerify) ok &= q[b] == v;
+      else q[b] = v;
+    }
+    if constexpr (kVerify) bad += !ok;
+  }
+  return bad;
+}
+
+template <bool kVerify>
+__device__ __forceinline__ uint32_t pattern_row_any(char* row, uint64_t n_elems, uint32_t eb,
+                                                    bool aligned, uint64_t base, int64_t g,
+                                                    int lane) {
+  if (aligned) {
+    switch (eb) {
+      case 1: return pattern_row_vec<1, kVerify>(row, n_elems, base, g, lane);
+      case 2: return pattern_row_vec<2, kVerify>(row, n_elems, base, g, lane);
+      case 4: return pattern_row_vec<4, kVerify>(row, n_elems, base, g, lane);
+      case 8: return pattern_row_vec<8, kVerify>(row, n_elems, base, g, lane);
+      default: break;
+    }
+  }
+  uint32_t bad = 0;
+  for (uint64_t e = lane; e < n_elems; e += 32) {
+    const uint64_t h = splitmix64(base ^ static_cast<uint64_t>(g + static_cast<int64_t>(e)));
+    uint8_t* q = reinterpret_cast<uint8_t*>(row) + e * eb;
+    bool ok = true;
+    for (uint32_t b = 0; b < eb; ++b) {
+      const uint8_t v = static_cast<uint8_t>(h >> ((b % 8) * 8));
+      if constexpr (kVerify) ok &= q[b] == v;
+      else q[b] = v;
+    }
+    if constexpr (kVerify) bad += !ok;
+  }
+  return bad;
+}
+
+template <bool kVerify>
+__global__ void __launch_bounds__(256) rs_pattern_kernel(const rs_pattern_desc* __restrict__ descs,
+                                                         const uint64_t* __restrict__ item0,
+                                                         uint32_t ndesc, uint64_t nitems,
+                                                         uint64_t seed,
+                                                         unsigned long long* mismatches,
+                                                         unsigned long long* first_bad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = warp; item < nitems; item += nwarps) {
+    const uint32_t di = find_desc(item0, ndesc, item);
+    const rs_pattern_desc& D = descs[di];
+    const uint64_t base = seed ^ (0x1000003ULL * D.tensor_index);
+    const uint64_t r0 = (item - D.item0) * D.rows_per_item;
+    const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+    const uint64_t row_bytes = D.row_elems * D.elem_bytes;
+    uint32_t bad = 0;
+    for (uint64_t r = r0; r < r1; ++r) {
+      int64_t g = D.g0;
+      uint32_t rr = static_cast<uint32_t>(r);
+      for (uint32_t k = 0; k < D.nouter; ++k) {
+        const uint32_t e = static_cast<uint32_t>(D.ext[k]);
+        const uint32_t q = rr / e;
+        g += static_cast<int64_t>(rr - q * e) * D.gstr[k];
+        rr = q;
+      }
+      char* row = reinterpret_cast<char*>(D.ptr) + r * row_bytes;
+      const bool aligned = ((D.ptr | row_bytes) & 15u) == 0;
+      bad += pattern_row_any<kVerify>(row, D.row_elems, D.elem_bytes, aligned, base, g, lane);
+    }
+    if constexpr (kVerify) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      if (lane == 0 && bad) {
+        atomicAdd(mismatches, static_cast<unsigned long long>(bad));
+        atomicMin(first_bad, static_cast<unsigned long long>(D.entry));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- exchange
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Spin with a bounded budget; on expiry raise the error flag (no hangs on a
+// protocol bug: the host reports failed_layer instead).
+__device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
+                                         unsigned int* error_flag, uint64_t spin_limit) {
+  uint64_t spins = 0;
+  while (ld_acquire_sys(flag) < want) {
+    if (*reinterpret_cast<volatile unsigned int*>(error_flag)) return false;
+    if (++spins > spin_limit) {
+      atomicExch(error_flag, 1u);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// Block roles: blocks [0, ntx) send lanes_tx[b], [ntx, ntx + nrx) receive
+// lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
+// never exceeds the co-resident CTA capacity, so every waiting role has its
+// counterpart running (same device) or launched on its own device (peers).
+__global__ void __launch_bounds__(256) rs_exchange_kernel(
+    const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
+    uint32_t nrx, const rs_batch_desc* __restrict__ batches,
+    const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
+    const uint64_t* __restrict__ local_item0, uint32_t nlocal, uint64_t local_items, uint64_t epoch,
+    unsigned int* error_flag, uint64_t spin_limit) {
+  const int lane_id = threadIdx.x & 31;
+  const int warp_in_block = threadIdx.x >> 5;
+  const int warps_per_block = blockDim.x >> 5;
+  __shared__ int ok_shared;
+
+  if (blockIdx.x < ntx + nrx) {
+    const bool sender = blockIdx.x < ntx;
+    const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
+    for (uint32_t b = 0; b < L.nbatches; ++b) {
+      const rs_batch_desc B = batches[L.batch0 + b];
+      const uint32_t slot = b % L.slots;
+      const uint64_t seq = epoch + b + 1;           // value published for batch b
+      if (threadIdx.x == 0) {
+        bool ok;
+        if (sender) {
+          // slot reuse: the receiver must have drained batch b - slots
+          ok = b < L.slots ||
+               wait_geq(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + slot,
+                        epoch + b - L.slots + 1, error_flag, spin_limit);
+        } else {
+          ok = wait_geq(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + slot, seq, error_flag,
+                        spin_limit);
+        }
+        ok_shared = ok;
+      }
+      __syncthreads();
+      if (!ok_shared) return;
+      if (sender) {
+        // pack: frame f copies its source box into the slot (remote stores)
+        for (uint32_t f = 0; f < B.npack; ++f) {
+          const rs_copy_desc& D = frames[B.pack0 + f];
+          const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
+          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<true>(D, it, lane_id);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence_system();
+          st_release_sys(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq);
+        }
+      } else {
+        for (uint32_t f = 0; f < B.nunpack; ++f) {
+          const rs_copy_desc& D = frames[B.unpack0 + f];
+          const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
+          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<false>(D, it, lane_id);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence_system();
+          st_release_sys(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, seq);
+        }
+      }
+    }
+    return;
+  }
+
+  // local copy role
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x - ntx - nrx) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x - ntx - nrx) * blockDim.x) >> 5;
+  for (uint64_t item = warp; item < local_items; item += nwarps) {
+    const uint32_t di = find_desc(local_item0, nlocal, item);
+    warp_copy_item<true>(local_descs[di], item - local_descs[di].item0, lane_id);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc,
+                           uint64_t item_begin, uint64_t item_end, int grid, cudaStream_t stream) {
+  if (item_end <= item_begin || ndesc == 0) return cudaSuccess;
+  rs_copy_kernel<<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+  return cudaGetLastError();
+}
+
+cudaError_t rs_launch_pattern(const rs_pattern_desc* descs, const uint64_t* item0, uint32_t ndesc,
+                              uint64_t nitems, uint64_t seed, int verify,
+                              unsigned long long* mismatches, unsigned long long* first_bad,
+                              int grid, cudaStream_t stream) {
+  if (nitems == 0 || ndesc == 0) return cudaSuccess;
+  if (verify)
+    rs_pattern_kernel<true><<<grid, 256, 0, stream>>>(descs, item0, ndesc, nitems, seed, mismatches, first_bad);
+  else
+    rs_pattern_kernel<false><<<grid, 256, 0, stream>>>(descs, item0, ndesc, nitems, seed, mismatches, first_bad);
+  return cudaGetLastError();
+}
+
+cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const rs_lane_desc* lanes_rx,
+                               uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
+                               const rs_copy_desc* local_descs, const uint64_t* local_item0,
+                               uint32_t nlocal, uint64_t local_items, uint64_t epoch,
+                               unsigned int* error_flag, uint64_t spin_limit, int local_blocks,
+                               cudaStream_t stream) {
+  const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
+  if (grid == 0) return cudaSuccess;
+  rs_exchange_kernel<<<grid, 256, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,
+                                               local_item0, nlocal, local_items, epoch, error_flag, spin_limit);
+  return cudaGetLastError();
+}
+
+int rs_kernel_max_blocks_per_sm(int which) {
+  int n = 0;
+  if (which == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel, 256, 0);
+  else if (which == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_pattern_kernel<false>, 256, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel, 256, 0);
+  return n;
+}
+
+}  // extern "C"

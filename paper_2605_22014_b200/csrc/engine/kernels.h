@@ -1,0 +1,32 @@
+// Host-callable launchers for kernels.cu (C linkage, no templates exposed).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "desc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc,
+                           uint64_t item_begin, uint64_t item_end, int grid, cudaStream_t stream);
+
+cudaError_t rs_launch_pattern(const rs_pattern_desc* descs, const uint64_t* item0, uint32_t ndesc,
+                              uint64_t nitems, uint64_t seed, int verify,
+                              unsigned long long* mismatches, unsigned long long* first_bad,
+                              int grid, cudaStream_t stream);
+
+cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
+                               const rs_lane_desc* lanes_rx, uint32_t nrx,
+                               const rs_batch_desc* batches, const rs_copy_desc* frames,
+                               const rs_copy_desc* local_descs, const uint64_t* local_item0,
+                               uint32_t nlocal, uint64_t local_items, uint64_t epoch,
+                               unsigned int* error_flag, uint64_t spin_limit, int local_blocks,
+                               cudaStream_t stream);
+
+int rs_kernel_max_blocks_per_sm(int which);
+
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,323 @@
+// Metadata-only transfer planner and its exact completeness check.
+//
+// compute_transfer_plan follows proj/src/planner.cpp:57-192 decision for
+// decision (tile each destination view by the old TP block partition;
+// self-held regions become carryovers when the local linear layout is
+// unchanged (planner.cpp:31-42) or local tasks otherwise; other regions are
+// sourced from the dp-index-0 replica, lowest rank id for replicated tensors,
+// optional round-robin balance_sources), so write_plan output is
+// byte-identical to the reference's.
+//
+// verify_plan reports the same violations with the same messages as the
+// reference's brute-force oracle (planner.cpp:194-303), but counts coverage on
+// a coordinate-compressed grid of cells instead of per element.
+#include <algorithm>
+#include <stdexcept>
+
+#include "reshard_b200/reshard.hpp"
+
+namespace reshard {
+
+namespace {
+
+// Row-major linear offset of `p` (the region origin) inside `owner`, and
+// whether every non-degenerate axis of `region` has the same stride in both
+// owners -- the "layout unchanged" test of planner.cpp:31-42.
+bool same_local_layout(const ShardView& owner_old, const ShardView& owner_new,
+                       const ShardView& region) {
+  const std::size_t nd = region.ndims();
+  std::int64_t stride_old = 1, stride_new = 1, off_old = 0, off_new = 0;
+  bool strides_match = true;
+  for (std::size_t k = nd; k-- > 0;) {
+    off_old += (region.dim(k).lo - owner_old.dim(k).lo) * stride_old;
+    off_new += (region.dim(k).lo - owner_new.dim(k).lo) * stride_new;
+    if (region.dim(k).length() > 1 && stride_old != stride_new) strides_match = false;
+    stride_old *= owner_old.dim(k).length();
+    stride_new *= owner_new.dim(k).length();
+  }
+  return off_old == off_new && strides_match;
+}
+
+}  // namespace
+
+TransferPlan compute_transfer_plan(const ParallelConfig& c_old, const ParallelConfig& c_new,
+                                   const ModelSpec& model, const PlanOptions& options,
+                                   PlannerStats* stats) {
+  if (c_old.generation_id() == c_new.generation_id())
+    throw std::invalid_argument("compute_transfer_plan: identical generation ids");
+  if (auto v = validate_config(c_old, model); !v.empty())
+    throw std::invalid_argument("compute_transfer_plan: invalid source config: " + v.front());
+  if (auto v = validate_config(c_new, model); !v.empty())
+    throw std::invalid_argument("compute_transfer_plan: invalid destination config: " + v.front());
+
+  TransferPlan plan;
+  plan.src_config_gen = c_old.generation_id();
+  plan.dst_config_gen = c_new.generation_id();
+  plan.tensor_ids.reserve(model.tensors.size());
+
+  const int tp_old = c_old.tp(), dp_old = c_old.dp(), tp_new = c_new.tp(), dp_new = c_new.dp();
+  std::int64_t pairs = 0, round_robin = 0;
+
+  struct OldBlock {
+    int tp_index;
+    Interval iv;
+  };
+  std::vector<OldBlock> old_blocks;
+
+  for (std::uint32_t ti = 0; ti < model.tensors.size(); ++ti) {
+    const TensorSpec& t = model.tensors[ti];
+    plan.tensor_ids.push_back(t.tensor_id);
+    const std::int64_t ebytes = model.element_bytes(t);
+    const int s_old = c_old.stage_of_layer(t.layer);
+    const int s_new = c_new.stage_of_layer(t.layer);
+    const bool sharded = t.tp_shard_axis.has_value();
+    const std::size_t axis = sharded ? static_cast<std::size_t>(*t.tp_shard_axis) : 0;
+    const std::int64_t axis_len = sharded ? t.shape[axis] : 0;
+
+    // position -> rank within one stage; positions are tp + tp*(dp + dp*stage)
+    auto old_rank = [&](int tp_i, int dp_i) {
+      return c_old.ranks()[static_cast<std::size_t>(tp_i + tp_old * (dp_i + dp_old * s_old))];
+    };
+    auto new_rank = [&](int tp_i, int dp_i) {
+      return c_new.ranks()[static_cast<std::size_t>(tp_i + tp_new * (dp_i + dp_new * s_new))];
+    };
+
+    old_blocks.clear();
+    if (sharded) {
+      for (int i = 0; i < tp_old; ++i)
+        if (auto b = tp_block(axis_len, tp_old, i)) old_blocks.push_back({i, *b});
+    } else {
+      old_blocks.push_back({-1, {0, 1}});
+    }
+
+    const ShardView full = ShardView::full(t.shape);
+    for (int dtp = 0; dtp < tp_new; ++dtp) {
+      ShardView v_dst = full;
+      if (sharded) {
+        auto b = tp_block(axis_len, tp_new, dtp);
+        if (!b) continue;
+        v_dst.raw(axis) = *b;
+      }
+      for (int ddp = 0; ddp < dp_new; ++ddp) {
+        const int dst = new_rank(dtp, ddp);
+
+        // The destination's own old view of this tensor, if it had one.
+        bool held_before = false;  // dst sat on the tensor's old stage
+        int held_tp = -1;
+        std::optional<ShardView> v_held;
+        if (c_old.contains(dst)) {
+          const RankCoord oc = c_old.coord_of(dst);
+          if (oc.pp == s_old) {
+            held_before = true;
+            held_tp = oc.tp;
+            ShardView vh = full;
+            bool present = true;
+            if (sharded) {
+              if (auto b = tp_block(axis_len, tp_old, oc.tp)) vh.raw(axis) = *b;
+              else present = false;
+            }
+            if (present) v_held = vh;
+          }
+        }
+
+        for (const OldBlock& ob : old_blocks) {
+          ++pairs;
+          ShardView region = v_dst;
+          if (sharded) {
+            Interval& iv = region.raw(axis);
+            iv.lo = std::max(v_dst.dim(axis).lo, ob.iv.lo);
+            iv.hi = std::min(v_dst.dim(axis).hi, ob.iv.hi);
+            if (iv.lo >= iv.hi) continue;
+          }
+          const std::int64_t bytes = region.element_count() * ebytes;
+
+          if (held_before && (!sharded || held_tp == ob.tp_index)) {
+            if (same_local_layout(*v_held, v_dst, region))
+              plan.carryover_by_layer[t.layer].push_back({ti, t.layer, dst, region, bytes});
+            else
+              plan.tasks_by_layer[t.layer].push_back({ti, t.layer, dst, dst, region, bytes});
+            continue;
+          }
+
+          const int src_dp = options.balance_sources ? static_cast<int>(round_robin++ % dp_old) : 0;
+          int src;
+          if (sharded) {
+            src = old_rank(ob.tp_index, src_dp);
+          } else {
+            src = old_rank(0, src_dp);
+            for (int k = 1; k < tp_old; ++k) src = std::min(src, old_rank(k, src_dp));
+          }
+          plan.tasks_by_layer[t.layer].push_back({ti, t.layer, src, dst, region, bytes});
+        }
+      }
+    }
+  }
+  if (stats) stats->pairs_checked = pairs;
+  return plan;
+}
+
+namespace {
+
+// Exact cover counting over the cells of a compressed grid: every axis is cut
+// at every box bound, so each cell is either fully inside or fully outside
+// each box.  Returns {elements with cover 0, elements with cover > 1}.
+std::pair<std::int64_t, std::int64_t> cover_counts(const ShardView& domain,
+                                                   const std::vector<ShardView>& boxes) {
+  const std::size_t nd = domain.ndims();
+  std::vector<std::vector<std::int64_t>> cuts(nd);
+  for (std::size_t k = 0; k < nd; ++k) {
+    auto& c = cuts[k];
+    c.push_back(domain.dim(k).lo);
+    c.push_back(domain.dim(k).hi);
+    for (const auto& b : boxes) {
+      c.push_back(b.dim(k).lo);
+      c.push_back(b.dim(k).hi);
+    }
+    std::sort(c.begin(), c.end());
+    c.erase(std::unique(c.begin(), c.end()), c.end());
+  }
+  std::vector<std::size_t> seg(nd);
+  std::size_t cells = 1;
+  for (std::size_t k = 0; k < nd; ++k) {
+    seg[k] = cuts[k].size() - 1;
+    cells *= seg[k];
+  }
+  std::vector<std::uint16_t> cover(cells, 0);
+  // Mark each box's cell range.
+  std::vector<std::size_t> lo(nd), hi(nd), idx(nd);
+  for (const auto& b : boxes) {
+    for (std::size_t k = 0; k < nd; ++k) {
+      lo[k] = static_cast<std::size_t>(std::lower_bound(cuts[k].begin(), cuts[k].end(), b.dim(k).lo) - cuts[k].begin());
+      hi[k] = static_cast<std::size_t>(std::lower_bound(cuts[k].begin(), cuts[k].end(), b.dim(k).hi) - cuts[k].begin());
+      idx[k] = lo[k];
+    }
+    while (true) {
+      std::size_t flat = 0;
+      for (std::size_t k = 0; k < nd; ++k) flat = flat * seg[k] + idx[k];
+      if (cover[flat] < 0xffff) ++cover[flat];
+      std::size_t k = nd;
+      while (k-- > 0) {
+        if (++idx[k] < hi[k]) break;
+        idx[k] = lo[k];
+      }
+      if (k == static_cast<std::size_t>(-1)) break;
+    }
+  }
+  std::int64_t gaps = 0, overlaps = 0;
+  std::fill(idx.begin(), idx.end(), 0);
+  for (std::size_t flat = 0; flat < cells; ++flat) {
+    std::size_t rem = flat;
+    std::int64_t vol = 1;
+    for (std::size_t k = nd; k-- > 0;) {
+      const std::size_t i = rem % seg[k];
+      rem /= seg[k];
+      vol *= cuts[k][i + 1] - cuts[k][i];
+    }
+    if (cover[flat] == 0) gaps += vol;
+    else if (cover[flat] > 1) overlaps += vol;
+  }
+  return {gaps, overlaps};
+}
+
+}  // namespace
+
+std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelConfig& c_old,
+                                     const ParallelConfig& c_new, const ModelSpec& model) {
+  std::vector<std::string> out;
+  auto complain = [&](std::string msg) {
+    if (out.size() < 64) out.push_back(std::move(msg));
+  };
+
+  std::vector<int> to_model(plan.tensor_ids.size(), -1);
+  for (std::size_t pi = 0; pi < plan.tensor_ids.size(); ++pi) {
+    for (std::size_t mi = 0; mi < model.tensors.size(); ++mi)
+      if (model.tensors[mi].tensor_id == plan.tensor_ids[pi]) to_model[pi] = static_cast<int>(mi);
+    if (to_model[pi] < 0) complain("plan references unknown tensor " + plan.tensor_ids[pi]);
+  }
+
+  std::vector<ShardView> marked;
+  for (std::size_t mi = 0; mi < model.tensors.size(); ++mi) {
+    const TensorSpec& t = model.tensors[mi];
+    const auto dst_views = owners(t, c_new);
+    const auto src_views = owners(t, c_old);
+    const auto tasks = plan.tasks_by_layer.find(t.layer);
+    const auto keeps = plan.carryover_by_layer.find(t.layer);
+
+    for (const auto& [dst, v_dst] : dst_views) {
+      marked.clear();
+      auto mark = [&](const ShardView& region, const char* what) {
+        if (!v_dst.contains(region)) {
+          complain(std::string(what) + " for tensor " + t.tensor_id + " rank " +
+                   std::to_string(dst) + " escapes destination view");
+          return;
+        }
+        marked.push_back(region);
+      };
+      if (tasks != plan.tasks_by_layer.end()) {
+        for (const auto& task : tasks->second) {
+          if (task.dst_rank != dst || to_model.at(task.tensor_index) != static_cast<int>(mi)) continue;
+          if (task.bounds.element_count() <= 0 || task.byte_size <= 0) {
+            complain("empty task for tensor " + t.tensor_id);
+            continue;
+          }
+          auto s = src_views.find(task.src_rank);
+          if (s == src_views.end())
+            complain("task source rank " + std::to_string(task.src_rank) + " owns nothing of tensor " +
+                     t.tensor_id);
+          else if (!s->second.contains(task.bounds))
+            complain("task bounds escape source view for tensor " + t.tensor_id + " src " +
+                     std::to_string(task.src_rank));
+          mark(task.bounds, "task");
+        }
+      }
+      if (keeps != plan.carryover_by_layer.end()) {
+        for (const auto& k : keeps->second) {
+          if (k.rank != dst || to_model.at(k.tensor_index) != static_cast<int>(mi)) continue;
+          auto s = src_views.find(k.rank);
+          if (s == src_views.end() || !s->second.contains(k.bounds))
+            complain("carryover not resident in old view for tensor " + t.tensor_id + " rank " +
+                     std::to_string(k.rank));
+          mark(k.bounds, "carryover");
+        }
+      }
+      const auto [gaps, overlaps] = cover_counts(v_dst, marked);
+      if (gaps)
+        complain("coverage gap: tensor " + t.tensor_id + " rank " + std::to_string(dst) + " missing " +
+                 std::to_string(gaps) + " elements");
+      if (overlaps)
+        complain("coverage overlap: tensor " + t.tensor_id + " rank " + std::to_string(dst) + " has " +
+                 std::to_string(overlaps) + " doubly-covered elements");
+    }
+  }
+  return out;
+}
+
+std::vector<ShardView> chunk_bounds(const ShardView& bounds, std::int64_t max_bytes,
+                                    std::int64_t bytes_per_element) {
+  std::vector<ShardView> out;
+  const std::int64_t total = bounds.element_count() * bytes_per_element;
+  if (total <= max_bytes) {
+    out.push_back(bounds);
+    return out;
+  }
+  if (bytes_per_element > max_bytes)
+    throw std::invalid_argument("chunk_bounds: one element exceeds the staging budget");
+  std::size_t d = 0;
+  while (d < bounds.ndims() && bounds.dim(d).length() <= 1) ++d;
+  if (d == bounds.ndims()) throw std::logic_error("chunk_bounds: single-element region over budget");
+  const std::int64_t unit = total / bounds.dim(d).length();
+  const std::int64_t step = std::max<std::int64_t>(1, max_bytes / std::max<std::int64_t>(unit, 1));
+  for (std::int64_t lo = bounds.dim(d).lo; lo < bounds.dim(d).hi; lo += step) {
+    ShardView piece = bounds;
+    piece.raw(d) = {lo, std::min(lo + step, bounds.dim(d).hi)};
+    if (piece.element_count() * bytes_per_element <= max_bytes) {
+      out.push_back(piece);
+    } else {
+      auto sub = chunk_bounds(piece, max_bytes, bytes_per_element);
+      out.insert(out.end(), sub.begin(), sub.end());
+    }
+  }
+  return out;
+}
+
+}  // namespace reshard

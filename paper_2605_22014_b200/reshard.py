@@ -1,0 +1,264 @@
+"""Python mirror of the reference reshard API, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(``proj/include/reshard/{planner,transfer_plan,topology,parallel_config,executor}.hpp``):
+
+* ``compute_transfer_plan(c_old, c_new, model, options, stats)`` raises
+  ``ValueError`` (``DomainError``) where the reference throws
+  ``std::invalid_argument`` (planner.cpp:60-71);
+* ``verify_plan`` returns the violation list (planner.cpp:194-303);
+* ``write_plan`` / ``read_plan`` use the reference text format;
+* ``execute_plan(plan, engine)`` replaces ``execute_plan(plan, src, dst,
+  transport, staging_bytes, bpe)`` (executor.hpp:50-53): the engine holds the
+  device shard stores, the transport (DIRECT peer stores or STAGED rings) and
+  the staging budget; it returns an ExecutionReport dict with the reference's
+  fields (ok, error, failed_layer, peak_staging_bytes, bytes_moved,
+  local_copy_bytes, layers_processed) plus timing.
+
+Every call goes to libreshard_b200.so; nothing here computes a plan or moves a
+byte in Python.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, List, Optional, Sequence
+
+from . import native as N
+from .native import DomainError, IntegrityError, ReshardError  # noqa: F401
+from .specs import ModelSpec, ParallelConfig
+
+
+def _text(fn) -> str:
+    need = C.c_size_t(0)
+    fn(None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    fn(buf, need.value, C.byref(need))
+    return buf.value.decode()
+
+
+class PlanOptions:
+    def __init__(self, balance_sources: bool = False):
+        self.balance_sources = balance_sources
+
+
+class PlannerStats:
+    pairs_checked: int = 0
+
+
+class TransferPlan:
+    """Owning handle of a native plan."""
+
+    def __init__(self, handle: int, model: ModelSpec):
+        self._h = C.c_void_p(handle)
+        self.model = model
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            try:
+                N.lib().rs_plan_destroy(self._h)
+            except Exception:
+                pass
+            self._h = C.c_void_p(0)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def text(self) -> str:
+        L = N.lib()
+        out = {}
+
+        def call(buf, cap, need):
+            N.check(L.rs_plan_write(self._h, buf, cap, need))
+        return _text(call)
+
+    def summary(self) -> dict:
+        s = N.PlanSummary()
+        N.check(N.lib().rs_plan_summary(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in N.PlanSummary._fields_}
+
+    def total_bytes(self) -> int:
+        return self.summary()["total_bytes"]
+
+
+def compute_transfer_plan(c_old: ParallelConfig, c_new: ParallelConfig, model: ModelSpec,
+                          options: Optional[PlanOptions] = None,
+                          stats: Optional[PlannerStats] = None) -> TransferPlan:
+    opts = N.PlanOptions(int(bool(options and options.balance_sources)))
+    h = C.c_void_p()
+    N.check(N.lib().rs_plan_compute(model.to_text().encode(),
+                                    N.config_struct(c_old, model.num_layers),
+                                    N.config_struct(c_new, model.num_layers), C.byref(opts),
+                                    C.byref(h)))
+    plan = TransferPlan(h.value, model)
+    if stats is not None:
+        stats.pairs_checked = plan.summary()["pairs_checked"]
+    return plan
+
+
+def write_plan(plan: TransferPlan) -> str:
+    return plan.text()
+
+
+def read_plan(text: str, model: ModelSpec) -> TransferPlan:
+    h = C.c_void_p()
+    N.check(N.lib().rs_plan_read(model.to_text().encode(), text.encode(), C.byref(h)))
+    return TransferPlan(h.value, model)
+
+
+def verify_plan(plan: TransferPlan, c_old: ParallelConfig, c_new: ParallelConfig) -> List[str]:
+    L = N.lib()
+    n = C.c_int32(0)
+    co = N.config_struct(c_old, plan.model.num_layers)
+    cn = N.config_struct(c_new, plan.model.num_layers)
+
+    def call(buf, cap, need):
+        N.check(L.rs_plan_verify(plan.handle, co, cn, buf, cap, need, C.byref(n)))
+    return [l for l in _text(call).split("\n") if l]
+
+
+def plan_cost_summary(plan: TransferPlan) -> dict:
+    s = plan.summary()
+    return {"total_bytes": s["total_bytes"], "max_link_bytes": s["max_link_bytes"],
+            "task_count": s["task_count"]}
+
+
+def validate_config(config: ParallelConfig, model: ModelSpec) -> List[str]:
+    L = N.lib()
+    n = C.c_int32(0)
+    cs = N.config_struct(config, model.num_layers)
+
+    def call(buf, cap, need):
+        N.check(L.rs_validate_config(model.to_text().encode(), cs, buf, cap, need, C.byref(n)))
+    return [l for l in _text(call).split("\n") if l]
+
+
+def view(model: ModelSpec, tensor_index: int, config: ParallelConfig, rank: int):
+    nd = len(model.tensors[tensor_index].shape)
+    lo = (C.c_int64 * nd)(); hi = (C.c_int64 * nd)(); present = C.c_int32(0)
+    N.check(N.lib().rs_view(model.to_text().encode(), N.config_struct(config, model.num_layers),
+                            tensor_index, rank, lo, hi, C.byref(present)))
+    return [(lo[i], hi[i]) for i in range(nd)] if present.value else None
+
+
+def chunk_bounds(lo: Sequence[int], hi: Sequence[int], max_bytes: int, bpe: int):
+    nd = len(lo)
+    cap = 1 << 16
+    olo = (C.c_int64 * (cap * nd))(); ohi = (C.c_int64 * (cap * nd))(); cnt = C.c_int64()
+    N.check(N.lib().rs_chunk_bounds(nd, (C.c_int64 * nd)(*lo), (C.c_int64 * nd)(*hi), max_bytes,
+                                    bpe, olo, ohi, cap, C.byref(cnt)))
+    return [([olo[i * nd + k] for k in range(nd)], [ohi[i * nd + k] for k in range(nd)])
+            for i in range(min(cnt.value, cap))]
+
+
+class Engine:
+    """Device engine: stores for C_old (RS_SRC) and C_new (RS_DST) + execution."""
+
+    def __init__(self, devices: Iterable[int] = (0,), staging_bytes: int = 1 << 30,
+                 mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 4,
+                 strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0):
+        devs = list(devices)
+        self._devs = (C.c_int32 * len(devs))(*devs)
+        o = N.EngineOptions(len(devs), self._devs, staging_bytes,
+                            N.RS_MODE_DIRECT if mode == "direct" else N.RS_MODE_STAGED,
+                            slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
+                            blocks_per_sm, 0)
+        h = C.c_void_p()
+        N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
+        self._h = h
+        self.models = {}
+        self.configs = {}
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            N.lib().rs_engine_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def layout(self, which: int, model: ModelSpec, config: ParallelConfig,
+               rank_device: Optional[Sequence[int]] = None):
+        rd = list(rank_device) if rank_device is not None else [0] * config.world
+        arr = (C.c_int32 * max(1, len(rd)))(*rd)
+        N.check(N.lib().rs_store_layout(self._h, which, model.to_text().encode(),
+                                        N.config_struct(config, model.num_layers), arr))
+        self.models[which] = model
+        self.configs[which] = config
+
+    def alloc(self, which: int):
+        N.check(N.lib().rs_store_alloc(self._h, which))
+
+    def free(self, which: int):
+        N.check(N.lib().rs_store_free(self._h, which))
+
+    def bind(self, which: int, rank: int, tensor_index: int, dptr: int, nbytes: int):
+        N.check(N.lib().rs_store_bind(self._h, which, rank, tensor_index, C.c_void_p(dptr), nbytes))
+
+    def ptr(self, which: int, rank: int, tensor_index: int):
+        p = C.c_void_p(); n = C.c_int64()
+        N.check(N.lib().rs_store_ptr(self._h, which, rank, tensor_index, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def store_bytes(self, which: int) -> int:
+        n = C.c_int64()
+        N.check(N.lib().rs_store_bytes(self._h, which, C.byref(n)))
+        return n.value
+
+    def read(self, which: int, rank: int, tensor_index: int, offset: int = 0,
+             nbytes: Optional[int] = None):
+        import numpy as np
+        if nbytes is None:
+            nbytes = self.ptr(which, rank, tensor_index)[1] - offset
+        out = np.empty(nbytes, np.uint8)
+        N.check(N.lib().rs_store_read(self._h, which, rank, tensor_index, offset, nbytes,
+                                      out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def write(self, which: int, rank: int, tensor_index: int, offset: int, data) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(data, dtype=np.uint8)
+        N.check(N.lib().rs_store_write(self._h, which, rank, tensor_index, offset, a.size,
+                                       a.ctypes.data_as(C.c_void_p)))
+
+    def fill_pattern(self, which: int, seed: int):
+        N.check(N.lib().rs_fill_pattern(self._h, which, seed))
+
+    def verify_pattern(self, which: int, seed: int):
+        bad = C.c_int64(); first = C.c_int64()
+        N.check(N.lib().rs_verify_pattern(self._h, which, seed, C.byref(bad), C.byref(first)))
+        return bad.value, first.value
+
+    def prepare(self, plan: TransferPlan):
+        N.check(N.lib().rs_prepare(self._h, plan.handle))
+
+    def run(self, raise_on_failure: bool = False) -> dict:
+        rep = N.ExecReport()
+        rc = N.lib().rs_run(self._h, C.byref(rep))
+        if rc not in (N.RS_OK, N.RS_EINTEGRITY) or (rc and raise_on_failure):
+            N.check(rc)
+        return rep.as_dict()
+
+    def execute_host(self, plan: TransferPlan, host_src: Sequence[int], host_dst: Sequence[int],
+                     window_layers: int = 2) -> dict:
+        rep = N.ExecReport()
+        s = (C.c_void_p * len(host_src))(*host_src)
+        d = (C.c_void_p * len(host_dst))(*host_dst)
+        rc = N.lib().rs_execute_host(self._h, plan.handle, s, d, window_layers, C.byref(rep))
+        if rc not in (N.RS_OK, N.RS_EINTEGRITY):
+            N.check(rc)
+        return rep.as_dict()
+
+
+def execute_plan(plan: TransferPlan, engine: Engine) -> dict:
+    """Reference ``execute_plan`` on device stores: prepare + run, report dict.
+
+    Integrity failures come back as ``ok=False`` with ``error`` and
+    ``failed_layer`` (executor.cpp:210-215); CUDA / argument errors raise.
+    """
+    engine.prepare(plan)
+    return engine.run()
