@@ -1,0 +1,349 @@
+#!/usr/bin/env python3
+"""Reshard benchmark (BASELINE.json metric: reshard GB/s + handoff ms for a
+7B TP/PP/DP resize, and % of the NVLink/HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one live handoff: the full transfer plan of the workload executed
+over device-resident shard stores (plan computed and compiled beforehand, as
+in the paper's Prepare phase).
+
+N=1 workload (BASELINE config 2 at full size, the metric's own config):
+Llama-2-7B, bf16 params + fp32 master + Adam m/v, TP4.PP2.DP1 (8 ranks) ->
+TP2.PP2.DP1 (4 ranks) with every logical rank on cuda:0 (intra-device
+relayout): 91.06 GB of plan bytes + 3.28 GB of carryover; src + dst state is
+188.7 GB resident in HBM.  Inputs are ~700x the 126 MB L2, so no L2 flush is
+needed between steps.
+
+--impl reference times the reference's own execute_plan (oracle/_ref, built
+from /root/reference/proj/src) on the host cores, on a bounded sample of the
+same workload.
+
+Every number is printed as ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reshard GB/s (Llama-2-7B TP4PP2->TP2PP2 handoff)"
+UNIT = "GB/s"
+HIGH_IS_GOOD = True
+SEED = 42
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(n_gpus: int, layers: int = 0):
+    from paper_2605_22014_b200 import specs
+    if layers:  # profiling-only slice (never a bench value)
+        sp, co, cn = specs.sliced_case("c2", layers)
+        return sp, co, cn, f"c2 PROFILING SLICE ({layers} layers)"
+    sp, co, cn = specs.baseline_case("c2")
+    desc = ("c2: Llama-2-7B bf16 params + fp32 master/m/v, TP4.PP2.DP1 (8 ranks) -> "
+            "TP2.PP2.DP1 (4 ranks), all logical ranks on one B200 (intra-device relayout)")
+    return sp, co, cn, desc
+
+
+def cpu_sample(layers: int):
+    """Bounded sample of the same workload for the reference CPU path: the
+    C2 resize on a `layers`-deep slice of Llama-2-7B (embedding + blocks +
+    head), one single-dtype spec per group (the reference holds one element
+    size per ModelSpec, model_spec.hpp:45)."""
+    from paper_2605_22014_b200 import specs
+    sp, co, cn = specs.sliced_case("c2", layers)
+    return [(specs.group_spec(sp, b), co, cn) for b in (2, 4)]
+
+
+def run_reference_cpu(threads: int, layers: int, steps: int, warmup: int, staging: int):
+    """Time the reference execute_plan (oracle/_ref) on host cores."""
+    from oracle.pyoracle import Oracle, available
+    if not available("ref"):
+        return None
+    ref = Oracle("ref")
+    nproc = os.cpu_count() or 1
+    benches = [ref.bench(g, co, cn, SEED, fill_threads=nproc) for g, co, cn in cpu_sample(layers)]
+    for _ in range(warmup):
+        for b in benches:
+            b.step(staging, threads)
+    secs, nbytes, ok = [], 0, True
+    for _ in range(steps):
+        t = 0.0
+        for b in benches:
+            r = b.step(staging, threads)
+            ok &= r["ok"]
+            t += r["seconds"]
+        secs.append(t)
+    nbytes = sum(b.plan_bytes for b in benches)
+    bad = sum(b.mismatches(nproc) for b in benches)
+    for b in benches:
+        b.close()
+    mean = statistics.mean(secs)
+    return {"value": nbytes / mean / 1e9, "seconds_per_step": mean, "plan_bytes": nbytes,
+            "ok": ok and bad == 0, "mismatches": bad}
+
+
+def reference_arm(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    layers = int(os.environ.get("RS_BENCH_CPU_LAYERS", "8"))
+    threads = min(os.cpu_count() or 1, layers)  # execute_plan is per-layer; one thread per layer
+    res = run_reference_cpu(threads, layers, max(1, args.steps), args.warmup, args.staging_bytes)
+    _, _, _, desc = workload(args.gpus)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref not built (reference sources absent at build time)"}))
+        return
+    sample = ("reference execute_plan (oracle/_ref, unmodified /root/reference/proj/src) on the "
+              f"C2 resize of a {layers}-layer Llama-2-7B slice (bf16 group + fp32 master/m/v group), "
+              f"{res['plan_bytes'] / 1e9:.2f} GB plan bytes per step, layers dealt to "
+              f"{threads} threads, LoopbackTransport, B={args.staging_bytes}")
+    line = {"metric": METRIC, "value": round(res["value"], 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds_per_step"] * 1e3,
+            "higher_is_better": HIGH_IS_GOOD, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (reference pattern, shard_store.cpp:51-85)",
+            "impl": "reference",
+            "config": {"workload": desc + f" -- CPU sample: {layers}-layer slice", "staging_bytes": args.staging_bytes},
+            "cpu_baseline": {"value": round(res["value"], 4), "unit": UNIT, "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(res["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "correct": res["ok"]}
+    print(json.dumps(line), flush=True)
+
+
+def ours(args) -> None:
+    import torch
+    from paper_2605_22014_b200 import reshard as R
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    sp, co, cn, desc = workload(args.gpus, args.profile_layers)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    summ = plan.summary()
+    total = summ["total_bytes"]
+    algo_bytes = 2 * (total + summ["carryover_bytes"])  # read + write of every moved byte
+
+    eng = R.Engine([local], staging_bytes=args.staging_bytes, mode=args.mode,
+                   lanes_per_link=args.lanes, strict_layers=args.strict)
+    eng.layout(RS_SRC, sp, co)
+    eng.layout(RS_DST, sp, cn)
+    eng.alloc(RS_SRC)
+    eng.alloc(RS_DST)
+    eng.fill_pattern(RS_SRC, SEED)
+    eng.prepare(plan)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        rep = eng.run()
+        assert rep["ok"], rep
+    bad_src = eng.verify_pattern(RS_DST, SEED)[0]
+
+    barrier()
+    launches = 0
+    dev_ms = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep = eng.run()
+            dev_ms.append(rep["device_ms"])
+            launches += rep["kernel_launches"]
+        barrier()
+        wall = time.perf_counter() - t0
+    step_ms = sum(dev_ms) / len(dev_ms)
+    if world > 1:
+        t = torch.tensor([step_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms = float(t.item())
+    mismatches = eng.verify_pattern(RS_DST, SEED)[0]
+
+    pk = peaks()
+    achieved = algo_bytes / (step_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("rs_copy_kernel_dram_bytes_per_launch")
+
+    line = {"metric": METRIC, "value": round(world * total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(step_ms, 4), "handoff_ms": round(step_ms, 4),
+            "higher_is_better": HIGH_IS_GOOD, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: reference pattern state (shard_store.cpp:51-85), random-init-equivalent bytes",
+            "config": {"workload": desc, "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
+                       "tasks": summ["task_count"], "mode": args.mode, "staging_bytes": args.staging_bytes,
+                       "strict_layers": bool(args.strict),
+                       "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+                         "kernel": "rs_copy_kernel",
+                         "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"]},
+            "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
+            "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_src)}}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = run_reference_cpu(1, 2, 1, 0, args.staging_bytes)
+        if res is not None:
+            line["cpu_baseline"] = {
+                "value": round(res["value"], 4), "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": (f"reference execute_plan (oracle/_ref) on the C2 resize of a 2-layer Llama-2-7B "
+                           f"slice, both dtype groups, {res['plan_bytes'] / 1e9:.2f} GB, 1 thread "
+                           f"(the reference is single-threaded) of {os.cpu_count()} host cores")}
+    if not args.no_e2e:
+        line["e2e"] = e2e(eng, plan, total, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e(eng, plan, total, args) -> dict:
+    """Same handoff through rs_execute_host with HOST shard stores: every step
+    copies all source shards H2D from pinned memory and all destination shards
+    D2H.  Host RAM cannot hold a second 94 GB store next to the pinned source
+    (196 GB box), so destination shards land in a 4 GiB pinned window that
+    successive shards overwrite; every byte still crosses PCIe."""
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+
+    src = eng.entries(RS_SRC)
+    dst = eng.entries(RS_DST)
+    h2d = sum(n for _, _, n in src)
+    d2h = sum(n for _, _, n in dst)
+    from paper_2605_22014_b200.reshard import PinnedBuffer
+    host_src = PinnedBuffer(h2d)
+    window = PinnedBuffer(4 << 30)
+    # the host source store holds the device source state, so the e2e output
+    # is checkable against the analytic pattern afterwards
+    off, src_ptrs = 0, []
+    for ti, r, n in src:
+        src_ptrs.append(host_src.ptr + off)
+        eng.read_to(RS_SRC, r, ti, host_src.ptr + off, n)
+        off += n
+    dst_ptrs, woff = [], 0
+    for _, _, n in dst:
+        if woff + n > window.nbytes:
+            woff = 0
+        dst_ptrs.append(window.ptr + woff)
+        woff += (n + 255) // 256 * 256
+    eng.fill_pattern(RS_DST, SEED ^ 0xDEAD)  # poison: the e2e run must rewrite every byte
+    times, ok = [], True
+    steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rep = eng.execute_host(plan, src_ptrs, dst_ptrs)
+        times.append(time.perf_counter() - t0)
+        ok &= rep["ok"]
+    bad = eng.verify_pattern(RS_DST, SEED)[0]
+    host_src.free()
+    window.free()
+    mean = statistics.mean(times)
+    return {"value": round(total / mean / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(mean, 4),
+            "path": "rs_execute_host (C ABI, host shard stores)", "ok": bool(ok and bad == 0)}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="direct", choices=["direct", "staged"])
+    ap.add_argument("--staging-bytes", type=int, default=1 << 30)
+    ap.add_argument("--lanes", type=int, default=4)
+    ap.add_argument("--strict", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-layers", type=int, default=0, help="profiling slice (not a bench value)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

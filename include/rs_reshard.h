@@ -131,6 +131,9 @@ int rs_store_bind(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_inde
 int rs_store_ptr(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, void** dptr,
                  int64_t* nbytes);
 int rs_store_bytes(rs_engine* e, int32_t which, int64_t* total);
+/* Entries in store order (tensor, ascending rank): up to cap triples. */
+int rs_store_entries(rs_engine* e, int32_t which, int32_t* tensor_index, int32_t* rank,
+                     int64_t* nbytes, int64_t cap, int64_t* count);
 int rs_store_read(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, int64_t offset,
                   int64_t nbytes, void* host);
 int rs_store_write(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index,
@@ -154,6 +157,10 @@ int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
  * stores. */
 int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
                     void* const* host_dst, int32_t window_layers, rs_exec_report* report);
+
+/* Page-locked host memory for host shard stores (full-bandwidth H2D/D2H). */
+int rs_host_alloc(size_t bytes, void** out);
+int rs_host_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -117,12 +117,7 @@ class Oracle:
         f("free").argtypes = [C.c_void_p]
         f("pattern_byte").restype = C.c_uint8
         f("pattern_byte").argtypes = [C.c_uint32, C.c_int64, C.c_int64, C.c_uint64]
-        if kind == "ref":
-            lib.ref_time_execute.argtypes = [C.c_char_p, C.POINTER(_Config), C.POINTER(_Config),
-                                             C.c_uint64, C.c_int64, C.c_int, C.c_int,
-                                             C.POINTER(Report), C.POINTER(C.c_int64),
-                                             C.POINTER(C.c_int64)]
-        else:
+        if kind == "c":
             lib.orc_chunk_bounds.argtypes = [C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                              C.c_int64, C.c_int64, C.POINTER(C.c_int64),
                                              C.POINTER(C.c_int64), C.c_int64,
@@ -208,17 +203,43 @@ class Oracle:
         return out[:n]
 
     # -- reference-only: the timed CPU arm -------------------------------------
-    def time_execute(self, spec, c_old, c_new, seed: int, staging: int, threads: int,
-                     check: bool = True) -> dict:
-        rep = Report(); nbytes = C.c_int64(); bad = C.c_int64()
-        rc = self.lib.ref_time_execute(spec.to_text().encode(),
-                                       config_struct(c_old, spec.num_layers),
-                                       config_struct(c_new, spec.num_layers), seed, staging,
-                                       threads, int(check), C.byref(rep), C.byref(nbytes),
-                                       C.byref(bad))
-        if rc:
+    def bench(self, spec, c_old, c_new, seed: int, fill_threads: int = 1) -> "RefBench":
+        return RefBench(self, spec, c_old, c_new, seed, fill_threads)
+
+
+class RefBench:
+    """The reference's own execute_plan, planned and filled once, timed per step."""
+
+    def __init__(self, orc: Oracle, spec, c_old, c_new, seed: int, fill_threads: int):
+        lib = orc.lib
+        lib.ref_bench_setup.restype = C.c_void_p
+        lib.ref_bench_setup.argtypes = [C.c_char_p, C.POINTER(_Config), C.POINTER(_Config),
+                                        C.c_uint64, C.c_int, C.POINTER(C.c_int64), C.POINTER(Report)]
+        lib.ref_bench_step.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.POINTER(Report)]
+        lib.ref_bench_check.restype = C.c_int64
+        lib.ref_bench_check.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
+        lib.ref_bench_free.argtypes = [C.c_void_p]
+        self.lib, self.seed = lib, seed
+        rep = Report(); nb = C.c_int64()
+        self.h = lib.ref_bench_setup(spec.to_text().encode(), config_struct(c_old, spec.num_layers),
+                                     config_struct(c_new, spec.num_layers), seed, fill_threads,
+                                     C.byref(nb), C.byref(rep))
+        if not self.h:
             raise OracleError(rep.error.decode())
-        d = rep.as_dict()
-        d["plan_bytes"] = nbytes.value
-        d["mismatches"] = bad.value
-        return d
+        self.plan_bytes = nb.value
+
+    def step(self, staging: int, threads: int) -> dict:
+        rep = Report()
+        self.lib.ref_bench_step(self.h, staging, threads, C.byref(rep))
+        return rep.as_dict()
+
+    def mismatches(self, threads: int) -> int:
+        return int(self.lib.ref_bench_check(self.h, self.seed, threads))
+
+    def close(self):
+        if self.h:
+            self.lib.ref_bench_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

@@ -354,73 +354,90 @@ uint8_t ref_pattern_byte(uint32_t ti, int64_t element, int64_t b, uint64_t seed)
   return ShardStore::pattern_byte(ti, element, b, seed);
 }
 
-// The CPU arm: plan, fill, then time the reference's execute_plan.  With
-// nthreads > 1 the plan's layers are dealt round-robin to threads, each
-// running the reference execute_plan on its layer subset with its own
-// LoopbackTransport (layers touch disjoint buffers; ShardStore lookups are
-// read-only map finds).  Returns the destination mismatch count vs the
-// analytic pattern in *mismatches (-1 if not checked).
-int ref_time_execute(const char* spec, const ref_config* o, const ref_config* n, uint64_t seed,
-                     int64_t staging, int nthreads, int check, ref_report* rep,
-                     int64_t* plan_bytes, int64_t* mismatches) {
+// The CPU arm.  ref_bench_setup plans and fills once; every ref_bench_step
+// times the reference's execute_plan over the same stores.  With nthreads > 1
+// the plan's layers are dealt round-robin to threads, each running the
+// reference execute_plan on its layer subset with its own LoopbackTransport
+// (layers touch disjoint buffers; ShardStore lookups are read-only map finds).
+struct Bench {
+  Handle src, dst;
+  TransferPlan plan;
+  int64_t plan_bytes = 0;
+};
+
+void* ref_bench_setup(const char* spec, const ref_config* o, const ref_config* n, uint64_t seed,
+                      int nthreads, int64_t* plan_bytes, ref_report* rep) {
   std::memset(rep, 0, sizeof(*rep));
   rep->failed_layer = -1;
   try {
-    Handle src, dst;
-    src.model = parse_spec(spec);
-    dst.model = src.model;
-    ParallelConfig co = make_config(o, src.model.num_layers);
-    ParallelConfig cn = make_config(n, src.model.num_layers);
-    TransferPlan plan = compute_transfer_plan(co, cn, src.model);
-    *plan_bytes = plan.total_bytes();
-    src.store = ShardStore::allocate(src.model, co);
-    index_store(src, co);
-    fast_fill(src, seed, nthreads > 0 ? nthreads : 1);
-    dst.store = ShardStore::allocate(dst.model, cn);
-    index_store(dst, cn);
-    if (nthreads < 1) nthreads = 1;
-    std::vector<TransferPlan> parts(nthreads);
-    int k = 0;
-    std::vector<int> layers;
-    for (auto& [l, t] : plan.tasks_by_layer) layers.push_back(l);
-    for (auto& [l, c] : plan.carryover_by_layer)
-      if (!plan.tasks_by_layer.count(l)) layers.push_back(l);
-    for (int l : layers) {
-      auto& p = parts[k++ % nthreads];
-      p.tensor_ids = plan.tensor_ids;
-      if (plan.tasks_by_layer.count(l)) p.tasks_by_layer[l] = plan.tasks_by_layer.at(l);
-      if (plan.carryover_by_layer.count(l)) p.carryover_by_layer[l] = plan.carryover_by_layer.at(l);
-    }
-    std::vector<ExecutionReport> reps(nthreads);
-    auto t0 = std::chrono::steady_clock::now();
-    {
-      std::vector<std::thread> ts;
-      for (int i = 0; i < nthreads; ++i)
-        ts.emplace_back([&, i] {
-          LoopbackTransport lb;
-          reps[i] = execute_plan(parts[i], src.store, dst.store, lb, staging,
-                                 src.model.bytes_per_element);
-        });
-      for (auto& t : ts) t.join();
-    }
-    auto t1 = std::chrono::steady_clock::now();
-    ExecutionReport all;
-    all.ok = true;
-    for (auto& r : reps) {
-      all.ok = all.ok && r.ok;
-      if (!r.ok && all.error.empty()) { all.error = r.error; all.failed_layer = r.failed_layer; }
-      all.peak_staging_bytes = std::max(all.peak_staging_bytes, r.peak_staging_bytes);
-      all.bytes_moved += r.bytes_moved;
-      all.local_copy_bytes += r.local_copy_bytes;
-      all.layers_processed += r.layers_processed;
-    }
-    fill_report(rep, all, std::chrono::duration<double>(t1 - t0).count());
-    *mismatches = check ? pattern_mismatches(dst, seed, nthreads) : -1;
-    return 0;
+    auto* b = new Bench;
+    b->src.model = parse_spec(spec);
+    b->dst.model = b->src.model;
+    ParallelConfig co = make_config(o, b->src.model.num_layers);
+    ParallelConfig cn = make_config(n, b->src.model.num_layers);
+    b->plan = compute_transfer_plan(co, cn, b->src.model);
+    b->plan_bytes = b->plan.total_bytes();
+    *plan_bytes = b->plan_bytes;
+    b->src.store = ShardStore::allocate(b->src.model, co);
+    index_store(b->src, co);
+    fast_fill(b->src, seed, nthreads > 0 ? nthreads : 1);
+    b->dst.store = ShardStore::allocate(b->dst.model, cn);
+    index_store(b->dst, cn);
+    return b;
   } catch (const std::exception& e) {
     std::snprintf(rep->error, sizeof rep->error, "%s", e.what());
-    return 1;
+    return nullptr;
   }
 }
+
+int ref_bench_step(void* h, int64_t staging, int nthreads, ref_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  rep->failed_layer = -1;
+  auto* b = static_cast<Bench*>(h);
+  if (nthreads < 1) nthreads = 1;
+  std::vector<TransferPlan> parts(nthreads);
+  std::vector<int> layers;
+  for (auto& [l, t] : b->plan.tasks_by_layer) layers.push_back(l);
+  for (auto& [l, c] : b->plan.carryover_by_layer)
+    if (!b->plan.tasks_by_layer.count(l)) layers.push_back(l);
+  int k = 0;
+  for (int l : layers) {
+    auto& p = parts[k++ % nthreads];
+    p.tensor_ids = b->plan.tensor_ids;
+    if (b->plan.tasks_by_layer.count(l)) p.tasks_by_layer[l] = b->plan.tasks_by_layer.at(l);
+    if (b->plan.carryover_by_layer.count(l)) p.carryover_by_layer[l] = b->plan.carryover_by_layer.at(l);
+  }
+  std::vector<ExecutionReport> reps(nthreads);
+  auto t0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::thread> ts;
+    for (int i = 0; i < nthreads; ++i)
+      ts.emplace_back([&, i] {
+        LoopbackTransport lb;
+        reps[i] = execute_plan(parts[i], b->src.store, b->dst.store, lb, staging,
+                               b->src.model.bytes_per_element);
+      });
+    for (auto& t : ts) t.join();
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  ExecutionReport all;
+  all.ok = true;
+  for (auto& r : reps) {
+    all.ok = all.ok && r.ok;
+    if (!r.ok && all.error.empty()) { all.error = r.error; all.failed_layer = r.failed_layer; }
+    all.peak_staging_bytes = std::max(all.peak_staging_bytes, r.peak_staging_bytes);
+    all.bytes_moved += r.bytes_moved;
+    all.local_copy_bytes += r.local_copy_bytes;
+    all.layers_processed += r.layers_processed;
+  }
+  fill_report(rep, all, std::chrono::duration<double>(t1 - t0).count());
+  return all.ok ? 0 : 1;
+}
+
+int64_t ref_bench_check(void* h, uint64_t seed, int nthreads) {
+  return pattern_mismatches(static_cast<Bench*>(h)->dst, seed, nthreads > 0 ? nthreads : 1);
+}
+
+void ref_bench_free(void* h) { delete static_cast<Bench*>(h); }
 
 }  // extern "C"

@@ -266,6 +266,19 @@ int rs_store_bytes(rs_engine* e, int32_t which, int64_t* total) {
   return guarded([&] { *total = e->impl.store(which).total_bytes(); });
 }
 
+int rs_store_entries(rs_engine* e, int32_t which, int32_t* tensor_index, int32_t* rank, int64_t* nbytes,
+                     int64_t cap, int64_t* count) {
+  return guarded([&] {
+    const auto& entries = e->impl.store(which).entries;
+    *count = static_cast<int64_t>(entries.size());
+    for (std::size_t k = 0; k < entries.size() && static_cast<int64_t>(k) < cap; ++k) {
+      tensor_index[k] = static_cast<int32_t>(entries[k].ti);
+      rank[k] = entries[k].rank;
+      nbytes[k] = entries[k].nbytes;
+    }
+  });
+}
+
 int rs_store_read(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index, int64_t offset, int64_t nbytes,
                   void* host) {
   return guarded([&] {
@@ -330,6 +343,21 @@ int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src, vo
     *report = e->impl.run_host(host_src, host_dst, window_layers);
     if (!report->ok) throw rsb::IntegrityError(report->error);
   });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rs_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    rsb::cuda_check(cudaHostAlloc(out, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+  });
+}
+
+int rs_host_free(void* p) {
+  return guarded([&] { rsb::cuda_check(cudaFreeHost(p), "cudaFreeHost"); });
 }
 
 }  // extern "C"

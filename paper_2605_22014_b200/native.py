@@ -21,9 +21,10 @@ EXPORTS = [
     "rs_last_error", "rs_version", "rs_validate_config", "rs_view", "rs_plan_compute",
     "rs_plan_read", "rs_plan_write", "rs_plan_summary", "rs_plan_verify", "rs_plan_destroy",
     "rs_chunk_bounds", "rs_engine_create", "rs_engine_destroy", "rs_store_layout",
-    "rs_store_alloc", "rs_store_bind", "rs_store_ptr", "rs_store_bytes", "rs_store_read",
+    "rs_store_alloc", "rs_store_bind", "rs_store_ptr", "rs_store_bytes", "rs_store_entries",
+    "rs_store_read",
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
-    "rs_run", "rs_execute", "rs_execute_host",
+    "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free",
 ]
 
 
@@ -126,6 +127,7 @@ def lib() -> C.CDLL:
         L.rs_store_bind.argtypes = [VP, I32, I32, I32, VP, I64]
         L.rs_store_ptr.argtypes = [VP, I32, I32, I32, P(VP), P(I64)]
         L.rs_store_bytes.argtypes = [VP, I32, P(I64)]
+        L.rs_store_entries.argtypes = [VP, I32, P(I32), P(I32), P(I64), I64, P(I64)]
         L.rs_store_read.argtypes = [VP, I32, I32, I32, I64, I64, VP]
         L.rs_store_write.argtypes = [VP, I32, I32, I32, I64, I64, VP]
         L.rs_fill_pattern.argtypes = [VP, I32, U64]
@@ -134,6 +136,8 @@ def lib() -> C.CDLL:
         L.rs_run.argtypes = [VP, P(ExecReport)]
         L.rs_execute.argtypes = [VP, VP, P(ExecReport)]
         L.rs_execute_host.argtypes = [VP, VP, P(VP), P(VP), I32, P(ExecReport)]
+        L.rs_host_alloc.argtypes = [SZ, P(VP)]
+        L.rs_host_free.argtypes = [VP]
         _lib = L
     return _lib
 

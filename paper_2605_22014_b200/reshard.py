@@ -209,6 +209,21 @@ class Engine:
         N.check(N.lib().rs_store_bytes(self._h, which, C.byref(n)))
         return n.value
 
+    def entries(self, which: int):
+        """[(tensor_index, rank, nbytes)] in store order (tensor, ascending rank)."""
+        L = N.lib()
+        cnt = C.c_int64()
+        N.check(L.rs_store_entries(self._h, which, None, None, None, 0, C.byref(cnt)))
+        n = cnt.value
+        ti = (C.c_int32 * max(1, n))(); rk = (C.c_int32 * max(1, n))(); nb = (C.c_int64 * max(1, n))()
+        N.check(L.rs_store_entries(self._h, which, ti, rk, nb, n, C.byref(cnt)))
+        return [(ti[i], rk[i], nb[i]) for i in range(n)]
+
+    def read_to(self, which: int, rank: int, tensor_index: int, host_ptr: int, nbytes: int,
+                offset: int = 0) -> None:
+        N.check(N.lib().rs_store_read(self._h, which, rank, tensor_index, offset, nbytes,
+                                      C.c_void_p(host_ptr)))
+
     def read(self, which: int, rank: int, tensor_index: int, offset: int = 0,
              nbytes: Optional[int] = None):
         import numpy as np
@@ -262,3 +277,23 @@ def execute_plan(plan: TransferPlan, engine: Engine) -> dict:
     """
     engine.prepare(plan)
     return engine.run()
+
+
+class PinnedBuffer:
+    """Page-locked host memory from rs_host_alloc (exact size, no rounding)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        N.check(N.lib().rs_host_alloc(nbytes, C.byref(p)))
+        self.ptr, self.nbytes = p.value, nbytes
+
+    def free(self):
+        if self.ptr:
+            N.check(N.lib().rs_host_free(C.c_void_p(self.ptr)))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -191,6 +191,8 @@ LLAMA = {
     "llama2-7b": (4096, 32, 32, 32, 128, 11008, 32000),
     "llama3-8b": (4096, 32, 32, 8, 128, 14336, 128256),
     "llama2-13b": (5120, 40, 40, 40, 128, 13824, 32000),
+    # test scale: same tensor structure (GQA fused QKV, SwiGLU fc1), tiny dims
+    "llama-mini": (256, 4, 16, 8, 16, 688, 1000),
 }
 
 # bf16 model weights + fp32 master weights + fp32 Adam m / v

@@ -79,7 +79,6 @@ def test_c1_gpt2_bitexact(mode, golden, oracle_c):
 
 
 def mini_llama(layers=2):
-    specs.LLAMA.setdefault("llama-mini", (256, 4, 8, 2, 32, 688, 1000))
     return specs.llama("llama-mini", layers)
 
 
