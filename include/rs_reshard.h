@@ -81,8 +81,13 @@ typedef struct {
   int32_t strict_layers;    /* 1: one launch per layer (layer barrier), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
   int32_t blocks_per_sm;    /* 0: occupancy maximum */
-  int32_t reserved;
+  int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
 } rs_engine_options;
+
+#define RS_COPY_AUTO 0     /* engine default */
+#define RS_COPY_LDG4 1     /* warp-per-row 16 B vectors, 4 loads in flight per lane */
+#define RS_COPY_LDG8 2     /* same, 8 loads in flight per lane */
+#define RS_COPY_BULK 3     /* cp.async.bulk global->smem->global ring, one issuer per CTA */
 
 typedef struct {
   int32_t ok;

@@ -123,6 +123,8 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
     DeviceGuard g(d.ordinal);
     cuda_check(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, d.ordinal), "sm count");
     cuda_check(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&d.h2d, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&d.d2h, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&d.ev_begin), "event");
     cuda_check(cudaEventCreate(&d.ev_end), "event");
     devices_.push_back(d);
@@ -147,6 +149,8 @@ Engine::~Engine() {
   for (auto& d : devices_) {
     cudaSetDevice(d.ordinal);
     if (d.stream) cudaStreamDestroy(d.stream);
+    if (d.h2d) cudaStreamDestroy(d.h2d);
+    if (d.d2h) cudaStreamDestroy(d.d2h);
     if (d.ev_begin) cudaEventDestroy(d.ev_begin);
     if (d.ev_end) cudaEventDestroy(d.ev_end);
   }
@@ -233,6 +237,22 @@ int Engine::grid_for(int dev, int which_kernel) const {
   if (per_sm < 1) per_sm = 1;
   if (opts_.blocks_per_sm > 0) per_sm = std::min(per_sm, opts_.blocks_per_sm);
   return devices_[static_cast<std::size_t>(dev)].sms * per_sm;
+}
+
+int Engine::copy_variant(int dev) const {
+  switch (opts_.copy_kernel) {
+    case RS_COPY_LDG8: return 2;
+    case RS_COPY_BULK: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 3 : 1;
+    default: return 1;
+  }
+}
+
+int Engine::copy_grid(int dev) const {
+  switch (copy_variant(dev)) {
+    case 2: return grid_for(dev, 3);
+    case 3: return devices_[static_cast<std::size_t>(dev)].sms;  // one bulk issuer CTA per SM
+    default: return grid_for(dev, 0);
+  }
 }
 
 // ---------------------------------------------------------------- patterns
@@ -641,12 +661,19 @@ void Engine::upload_programs() {
     DeviceProgram& p = programs_[d];
     const Device& dv = devices_[d];
     std::uint64_t bytes = 0;
-    for (const auto& c : p.local) bytes += bytes_of(c);
+    p.all_aligned = true;
+    for (const auto& c : p.local) {
+      bytes += bytes_of(c);
+      p.all_aligned = p.all_aligned && c.vec_log2 == 4;
+    }
     p.local_bytes = bytes;
     std::uint64_t item_bytes = static_cast<std::uint64_t>(opts_.item_bytes);
     if (item_bytes == 0) {
-      const std::uint64_t warps = static_cast<std::uint64_t>(grid_for(static_cast<int>(d), 0)) * 8;
-      item_bytes = std::clamp<std::uint64_t>(bytes / (warps * 8 + 1), 32768, 1 << 20);
+      // ~8 items per worker (warp, or bulk-issuer CTA) for load balance
+      const int variant = copy_variant(static_cast<int>(d));
+      const std::uint64_t workers = variant == 3 ? static_cast<std::uint64_t>(dv.sms)
+                                                 : static_cast<std::uint64_t>(copy_grid(static_cast<int>(d))) * 8;
+      item_bytes = std::clamp<std::uint64_t>(bytes / (workers * 8 + 1), 32768, variant == 3 ? 8u << 20 : 1u << 20);
     }
     // item ranges per layer
     std::uint64_t item = 0;
@@ -702,7 +729,7 @@ rs_exec_report Engine::run() {
         cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                   reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                                   static_cast<std::uint32_t>(p.local.size()), 0, p.local_items,
-                                  grid_for(static_cast<int>(d), 0), devices_[d].stream),
+                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
                    "copy kernel launch");
         ++launches;
       }
@@ -717,7 +744,7 @@ rs_exec_report Engine::run() {
           cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                     reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                                     static_cast<std::uint32_t>(p.local.size()), lr.item_begin, lr.item_end,
-                                    grid_for(static_cast<int>(d), 0), devices_[d].stream),
+                                    copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
                      "copy kernel launch");
           ++launches;
         }
@@ -789,27 +816,120 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
   (void)window_layers;
   if (!prepared_) throw DomainError("engine: prepare a plan first");
   const auto t0 = std::chrono::steady_clock::now();
-  // H2D every source shard, reshard, D2H every destination shard (copy
-  // engines overlap across devices; per-layer pipelining is future work)
-  for (std::size_t k = 0; k < stores_[RS_SRC].entries.size(); ++k) {
-    const Entry& e = stores_[RS_SRC].entries[k];
-    const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
-    DeviceGuard g(dv.ordinal);
-    cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice, dv.stream),
-               "H2D");
+  if (opts_.mode != RS_MODE_DIRECT) {
+    // staged transfers run as one launch: stage everything in, run, stage out
+    for (std::size_t k = 0; k < stores_[RS_SRC].entries.size(); ++k) {
+      const Entry& e = stores_[RS_SRC].entries[k];
+      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+      DeviceGuard g(dv.ordinal);
+      cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
+                                 dv.stream), "H2D");
+    }
+    rs_exec_report rep = run();
+    for (std::size_t k = 0; k < stores_[RS_DST].entries.size(); ++k) {
+      const Entry& e = stores_[RS_DST].entries[k];
+      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+      DeviceGuard g(dv.ordinal);
+      cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
+                                 dv.stream), "D2H");
+    }
+    for (auto& dv : devices_) {
+      DeviceGuard g(dv.ordinal);
+      cuda_check(cudaStreamSynchronize(dv.stream), "D2H");
+    }
+    rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return rep;
   }
-  rs_exec_report rep = run();
-  for (std::size_t k = 0; k < stores_[RS_DST].entries.size(); ++k) {
-    const Entry& e = stores_[RS_DST].entries[k];
-    const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
-    DeviceGuard g(dv.ordinal);
-    cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost, dv.stream),
-               "D2H");
+
+  // DIRECT: layer pipeline over three streams per device.  Layer l's source
+  // shards go H2D (h2d stream), its copy kernel waits for them (compute
+  // stream), its destination shards go D2H once every device finished layer l
+  // (d2h stream) -- so H2D of l+1, the kernel of l and D2H of l-1 overlap and
+  // PCIe runs full duplex.  The layers are the plan's (executor.cpp:134-138).
+  rs_exec_report rep = planned_;
+  const std::size_t nlayers = programs_.empty() ? 0 : programs_[0].layers.size();
+  std::map<int, std::size_t> layer_slot;
+  for (std::size_t li = 0; li < nlayers; ++li) layer_slot[programs_[0].layers[li].layer] = li;
+  const std::size_t ndev = devices_.size();
+  std::vector<cudaEvent_t> ev_in(nlayers * ndev), ev_done(nlayers * ndev);
+  auto mk = [](cudaEvent_t& e) { cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"); };
+  for (std::size_t d = 0; d < ndev; ++d) {
+    DeviceGuard g(devices_[d].ordinal);
+    for (std::size_t li = 0; li < nlayers; ++li) {
+      mk(ev_in[li * ndev + d]);
+      mk(ev_done[li * ndev + d]);
+    }
+    cuda_check(cudaEventRecord(devices_[d].ev_begin, devices_[d].h2d), "event");
   }
+  auto layer_of = [&](const Store& s, const Entry& e) { return s.model.tensors[e.ti].layer; };
+  // H2D per layer, in layer order
+  for (std::size_t li = 0; li < nlayers; ++li) {
+    const int layer = programs_[0].layers[li].layer;
+    for (std::size_t k = 0; k < stores_[RS_SRC].entries.size(); ++k) {
+      const Entry& e = stores_[RS_SRC].entries[k];
+      if (layer_of(stores_[RS_SRC], e) != layer) continue;
+      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+      DeviceGuard g(dv.ordinal);
+      cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
+                                 dv.h2d), "H2D");
+    }
+    for (std::size_t d = 0; d < ndev; ++d) {
+      DeviceGuard g(devices_[d].ordinal);
+      cuda_check(cudaEventRecord(ev_in[li * ndev + d], devices_[d].h2d), "event");
+    }
+  }
+  // kernels per layer; a layer's copies may read any device's sources
+  int launches = 0;
+  for (std::size_t li = 0; li < nlayers; ++li) {
+    for (std::size_t d = 0; d < ndev; ++d) {
+      DeviceProgram& p = programs_[d];
+      const LayerRange& lr = p.layers[li];
+      DeviceGuard g(devices_[d].ordinal);
+      for (std::size_t o = 0; o < ndev; ++o)
+        cuda_check(cudaStreamWaitEvent(devices_[d].stream, ev_in[li * ndev + o], 0), "wait");
+      if (lr.item_end > lr.item_begin) {
+        cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
+                                  reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
+                                  static_cast<std::uint32_t>(p.local.size()), lr.item_begin, lr.item_end,
+                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
+                   "copy kernel launch");
+        ++launches;
+      }
+      cuda_check(cudaEventRecord(ev_done[li * ndev + d], devices_[d].stream), "event");
+    }
+  }
+  // D2H per layer after every device finished that layer
+  for (std::size_t li = 0; li < nlayers; ++li) {
+    const int layer = programs_[0].layers[li].layer;
+    for (std::size_t d = 0; d < ndev; ++d) {
+      DeviceGuard g(devices_[d].ordinal);
+      for (std::size_t o = 0; o < ndev; ++o)
+        cuda_check(cudaStreamWaitEvent(devices_[d].d2h, ev_done[li * ndev + o], 0), "wait");
+    }
+    for (std::size_t k = 0; k < stores_[RS_DST].entries.size(); ++k) {
+      const Entry& e = stores_[RS_DST].entries[k];
+      if (layer_of(stores_[RS_DST], e) != layer) continue;
+      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+      DeviceGuard g(dv.ordinal);
+      cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
+                                 dv.d2h), "D2H");
+    }
+  }
+  double worst = 0;
   for (auto& dv : devices_) {
     DeviceGuard g(dv.ordinal);
-    cuda_check(cudaStreamSynchronize(dv.stream), "D2H");
+    cuda_check(cudaEventRecord(dv.ev_end, dv.d2h), "event");
+    cuda_check(cudaEventSynchronize(dv.ev_end), "host-store reshard");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, dv.ev_begin, dv.ev_end), "elapsed");
+    worst = std::max(worst, static_cast<double>(ms));
   }
+  for (std::size_t i = 0; i < ev_in.size(); ++i) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_done[i]);
+  }
+  rep.device_ms = worst;
+  rep.kernel_launches = launches;
   rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return rep;
 }

@@ -86,12 +86,14 @@ struct DeviceProgram {
   std::vector<rs_copy_desc> frames;
   DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error;
   std::uint64_t local_bytes = 0;  // bytes this device moves in local descriptors
+  bool all_aligned = true;        // every local descriptor is 16 B aligned (bulk-copy eligible)
 };
 
 struct Device {
   int ordinal = 0;
   int sms = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;              // reshard kernels
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // host-store copies (rs_execute_host)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 
@@ -122,6 +124,8 @@ class Engine {
   void compile_staged(const reshard::TransferPlan& plan);
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
+  int copy_variant(int dev) const;  // rs_launch_copy variant for this device's program
+  int copy_grid(int dev) const;
   void check_stores_ready() const;
 
   rs_engine_options opts_{};

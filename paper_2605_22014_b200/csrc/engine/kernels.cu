@@ -73,30 +73,30 @@ __device__ __forceinline__ void store<uint4>(uint4* p, const uint4& v) {
                : "memory");
 }
 
-// One warp copies one contiguous run: lanes stride T-sized vectors, kUnroll
-// loads issued before their stores.
-template <typename T, bool kReadOnly>
+// One warp copies one contiguous run: lanes stride T-sized vectors, U loads
+// issued before their stores.
+template <typename T, bool kReadOnly, int U = kUnroll>
 __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64_t nbytes,
                                               int lane) {
   const T* s = reinterpret_cast<const T*>(src);
   T* d = reinterpret_cast<T*>(dst);
   const uint64_t n = nbytes / sizeof(T);
   uint64_t i = static_cast<uint64_t>(lane);
-  for (; i + 32 * (kUnroll - 1) < n; i += 32 * kUnroll) {
-    T v[kUnroll];
+  for (; i + 32 * (U - 1) < n; i += 32 * U) {
+    T v[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = load<T, kReadOnly>(s + i + 32 * u);
+    for (int u = 0; u < U; ++u) v[u] = load<T, kReadOnly>(s + i + 32 * u);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) store<T>(d + i + 32 * u, v[u]);
+    for (int u = 0; u < U; ++u) store<T>(d + i + 32 * u, v[u]);
   }
   for (; i < n; i += 32) store<T>(d + i, load<T, kReadOnly>(s + i));
 }
 
-template <bool kReadOnly>
+template <bool kReadOnly, int U = kUnroll>
 __device__ __forceinline__ void warp_copy_any(const char* src, char* dst, uint64_t nbytes,
                                               uint32_t vec_log2, int lane) {
   switch (vec_log2) {
-    case 4: warp_copy_run<uint4, kReadOnly>(src, dst, nbytes, lane); break;
+    case 4: warp_copy_run<uint4, kReadOnly, U>(src, dst, nbytes, lane); break;
     case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane); break;
     case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane); break;
     case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane); break;
@@ -132,7 +132,7 @@ __device__ __forceinline__ void row_offsets(const rs_copy_desc& D, uint32_t r, i
   }
 }
 
-template <bool kReadOnly>
+template <bool kReadOnly, int U = kUnroll>
 __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t local_item,
                                                int lane) {
   const uint64_t r0 = local_item * D.rows_per_item;
@@ -142,10 +142,11 @@ __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t l
   for (uint64_t r = r0; r < r1; ++r) {
     int64_t so, dof;
     row_offsets(D, static_cast<uint32_t>(r), so, dof);
-    warp_copy_any<kReadOnly>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+    warp_copy_any<kReadOnly, U>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
   }
 }
 
+template <int U>
 __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __restrict__ descs,
                                                       const uint64_t* __restrict__ item0,
                                                       uint32_t ndesc, uint64_t item_begin,
@@ -155,8 +156,148 @@ __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __rest
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t item = item_begin + warp; item < item_end; item += nwarps) {
     const uint32_t di = find_desc(item0, ndesc, item);
-    warp_copy_item<true>(descs[di], item - descs[di].item0, lane);
+    warp_copy_item<true, U>(descs[di], item - descs[di].item0, lane);
   }
+}
+
+// ------------------------------------------------------ TMA bulk-copy ring
+//
+// One elected thread per CTA streams rows through a ring of kStages shared
+// memory stages with the Blackwell bulk-copy engine (cp.async.bulk, SASS
+// UBLKCP): global -> smem completes on a per-stage mbarrier (complete_tx),
+// smem -> global is a bulk_group store.  Loads run kLag stages ahead of
+// stores; a stage is refilled only after `cp.async.bulk.wait_group.read`
+// proves its previous store has read it.  Requires 16 B aligned rows
+// (descriptors with vec_log2 < 4 go to the LDG kernel).
+
+constexpr int kBulkStages = 8;
+constexpr int kBulkLag = 5;
+constexpr uint32_t kBulkStageBytes = 24576;
+constexpr int kBulkMaxPieces = 32;
+
+struct BulkPiece {
+  uint64_t src, dst;
+  uint32_t off, bytes;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32, 1) rs_copy_bulk_kernel(const rs_copy_desc* __restrict__ descs,
+                                                             const uint64_t* __restrict__ item0,
+                                                             uint32_t ndesc, uint64_t item_begin,
+                                                             uint64_t item_end) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
+  __shared__ BulkPiece pieces[kBulkStages][kBulkMaxPieces];
+  __shared__ int npieces[kBulkStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  uint64_t chunk = 0;   // stages filled so far
+  uint64_t drained = 0; // stages whose stores were issued
+  int s = 0, n = 0;
+  uint32_t fill = 0;
+
+  auto drain_one = [&]() {
+    const int ds = static_cast<int>(drained % kBulkStages);
+    mbar_wait(&bars[ds], static_cast<uint32_t>((drained / kBulkStages) & 1));
+    for (int k = 0; k < npieces[ds]; ++k) {
+      const BulkPiece& p = pieces[ds][k];
+      bulk_store(reinterpret_cast<void*>(p.dst), ring + ds * kBulkStageBytes + p.off, p.bytes);
+    }
+    bulk_commit();
+    ++drained;
+  };
+  auto issue = [&]() {  // launch the loads of the stage being filled
+    npieces[s] = n;
+    mbar_expect_tx(&bars[s], fill);
+    for (int k = 0; k < n; ++k) {
+      const BulkPiece& p = pieces[s][k];
+      bulk_load(ring + s * kBulkStageBytes + p.off, reinterpret_cast<const void*>(p.src), p.bytes, &bars[s]);
+    }
+    ++chunk;
+    if (chunk > static_cast<uint64_t>(kBulkLag)) drain_one();
+    s = static_cast<int>(chunk % kBulkStages);
+    n = 0;
+    fill = 0;
+    // the next stage to fill was last stored by chunk - kStages: make sure that
+    // store finished reading smem (groups committed after it: stages-lag-1)
+    if (chunk >= static_cast<uint64_t>(kBulkStages)) bulk_wait_read<kBulkStages - kBulkLag - 1>();
+  };
+
+  const uint64_t per = gridDim.x;
+  for (uint64_t item = item_begin + blockIdx.x; item < item_end; item += per) {
+    const uint32_t di = find_desc(item0, ndesc, item);
+    const rs_copy_desc& D = descs[di];
+    const uint64_t r0 = (item - D.item0) * D.rows_per_item;
+    const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+    for (uint64_t r = r0; r < r1; ++r) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      uint64_t src = D.src + so, dst = D.dst + dof, left = D.row_bytes;
+      while (left) {
+        uint32_t room = kBulkStageBytes - fill;
+        if (room == 0 || n == kBulkMaxPieces) {
+          issue();
+          room = kBulkStageBytes;
+        }
+        const uint32_t b = static_cast<uint32_t>(left < room ? left : static_cast<uint64_t>(room));
+        pieces[s][n++] = BulkPiece{src, dst, fill, b};
+        fill += b;
+        src += b;
+        dst += b;
+        left -= b;
+      }
+    }
+  }
+  if (n) issue();
+  while (drained < chunk) drain_one();
+  bulk_wait_all();
 }
 
 // ------------------------------------------------------------- pattern
@@ -437,9 +578,27 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
 extern "C" {
 
 cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc,
-                           uint64_t item_begin, uint64_t item_end, int grid, cudaStream_t stream) {
+                           uint64_t item_begin, uint64_t item_end, int grid, int variant,
+                           cudaStream_t stream) {
   if (item_end <= item_begin || ndesc == 0) return cudaSuccess;
-  rs_copy_kernel<<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+  switch (variant) {
+    case 2:
+      rs_copy_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 3: {
+      static bool configured = false;
+      const int smem = kBulkStages * static_cast<int>(kBulkStageBytes);
+      if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+      }
+      rs_copy_bulk_kernel<<<grid, 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    }
+    default:
+      rs_copy_kernel<4><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+  }
   return cudaGetLastError();
 }
 
@@ -470,7 +629,9 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
 
 int rs_kernel_max_blocks_per_sm(int which) {
   int n = 0;
-  if (which == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel, 256, 0);
+  if (which == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel<4>, 256, 0);
+  else if (which == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel<8>, 256, 0);
+  else if (which == 4) n = 1;  // bulk ring: one CTA (one issuer, ~200 KB smem) per SM
   else if (which == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_pattern_kernel<false>, 256, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel, 256, 0);
   return n;

@@ -9,8 +9,10 @@
 extern "C" {
 #endif
 
+// variant: 1 LDG x4 (default), 2 LDG x8, 3 TMA bulk ring (16 B aligned descriptors only)
 cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc,
-                           uint64_t item_begin, uint64_t item_end, int grid, cudaStream_t stream);
+                           uint64_t item_begin, uint64_t item_end, int grid, int variant,
+                           cudaStream_t stream);
 
 cudaError_t rs_launch_pattern(const rs_pattern_desc* descs, const uint64_t* item0, uint32_t ndesc,
                               uint64_t nitems, uint64_t seed, int verify,

@@ -72,7 +72,7 @@ class EngineOptions(C.Structure):
                 ("staging_bytes", C.c_int64), ("mode", C.c_int32),
                 ("slots_per_link", C.c_int32), ("lanes_per_link", C.c_int32),
                 ("strict_layers", C.c_int32), ("item_bytes", C.c_int64),
-                ("blocks_per_sm", C.c_int32), ("reserved", C.c_int32)]
+                ("blocks_per_sm", C.c_int32), ("copy_kernel", C.c_int32)]
 
 
 class ExecReport(C.Structure):

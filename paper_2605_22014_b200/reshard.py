@@ -157,13 +157,14 @@ class Engine:
 
     def __init__(self, devices: Iterable[int] = (0,), staging_bytes: int = 1 << 30,
                  mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 4,
-                 strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0):
+                 strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
+                 copy_kernel: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         o = N.EngineOptions(len(devs), self._devs, staging_bytes,
                             N.RS_MODE_DIRECT if mode == "direct" else N.RS_MODE_STAGED,
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
-                            blocks_per_sm, 0)
+                            blocks_per_sm, copy_kernel)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h

@@ -61,10 +61,11 @@ def test_random_pairs_bitexact(mode, golden, oracle_c):
         eng.close()
 
 
-@pytest.mark.parametrize("mode", ["direct", "staged"])
-def test_c1_gpt2_bitexact(mode, golden, oracle_c):
+@pytest.mark.parametrize("mode,copy_kernel", [("direct", 1), ("direct", 2), ("direct", 3), ("staged", 0)])
+def test_c1_gpt2_bitexact(mode, copy_kernel, golden, oracle_c):
     sp, co, cn = specs.baseline_case("c1")
-    eng = make_engine(sp, co, cn, mode, 1 << 30 if mode == "direct" else 256 << 20, lanes_per_link=2)
+    eng = make_engine(sp, co, cn, mode, 1 << 30 if mode == "direct" else 256 << 20, lanes_per_link=2,
+                      copy_kernel=copy_kernel)
     plan = R.compute_transfer_plan(co, cn, sp)
     rep = R.execute_plan(plan, eng)
     want = golden["c1_exec"]["1073741824"]
@@ -82,7 +83,7 @@ def mini_llama(layers=2):
     return specs.llama("llama-mini", layers)
 
 
-@pytest.mark.parametrize("mode", ["direct", "staged"])
+@pytest.mark.parametrize("mode", ["direct", "staged", "bulk"])
 @pytest.mark.parametrize("pair", [((4, 2, 1), (2, 2, 1)), ((2, 2, 1), (4, 2, 1)), ((8, 1, 1), (4, 1, 2)),
                                   ((2, 4, 1), (4, 1, 2)), ((1, 1, 2), (2, 2, 2))])
 def test_mixed_dtype_gqa_glu_against_oracle(mode, pair, oracle_c):
@@ -90,7 +91,10 @@ def test_mixed_dtype_gqa_glu_against_oracle(mode, pair, oracle_c):
     sp = mini_llama(4)
     (t0, p0, d0), (t1, p1, d1) = pair
     co, cn = specs.iota_config(1, t0, p0, d0), specs.iota_config(2, t1, p1, d1)
-    eng = make_engine(sp, co, cn, mode, 1 << 20, lanes_per_link=2)
+    if mode == "bulk":
+        eng = make_engine(sp, co, cn, "direct", 1 << 20, copy_kernel=3)
+    else:
+        eng = make_engine(sp, co, cn, mode, 1 << 20, lanes_per_link=2)
     plan = R.compute_transfer_plan(co, cn, sp)
     text = plan.text()
     assert text == oracle_c.plan_text(sp, co, cn)[0]
