@@ -88,6 +88,8 @@ typedef struct {
 #define RS_COPY_LDG4 1     /* warp-per-row 16 B vectors, 4 loads in flight per lane */
 #define RS_COPY_LDG8 2     /* same, 8 loads in flight per lane */
 #define RS_COPY_BULK 3     /* cp.async.bulk global->smem->global ring, one issuer per CTA */
+#define RS_COPY_LDG4_CS 4  /* LDG4 with evict-first (st.global.cs) stores */
+#define RS_COPY_LDG8_CS 5  /* LDG8 with evict-first (st.global.cs) stores */
 
 typedef struct {
   int32_t ok;

@@ -243,13 +243,16 @@ int Engine::copy_variant(int dev) const {
   switch (opts_.copy_kernel) {
     case RS_COPY_LDG8: return 2;
     case RS_COPY_BULK: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 3 : 1;
+    case RS_COPY_LDG4_CS: return 4;
+    case RS_COPY_LDG8_CS: return 5;
     default: return 1;
   }
 }
 
 int Engine::copy_grid(int dev) const {
   switch (copy_variant(dev)) {
-    case 2: return grid_for(dev, 3);
+    case 2:
+    case 5: return grid_for(dev, 3);
     case 3: return devices_[static_cast<std::size_t>(dev)].sms;  // one bulk issuer CTA per SM
     default: return grid_for(dev, 0);
   }

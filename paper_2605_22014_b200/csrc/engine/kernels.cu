@@ -73,9 +73,16 @@ __device__ __forceinline__ void store<uint4>(uint4* p, const uint4& v) {
                : "memory");
 }
 
+// Streaming store (evict-first in L2): the destination is not re-read.
+__device__ __forceinline__ void store_cs(uint4* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 // One warp copies one contiguous run: lanes stride T-sized vectors, U loads
 // issued before their stores.
-template <typename T, bool kReadOnly, int U = kUnroll>
+template <typename T, bool kReadOnly, int U = kUnroll, bool kStream = false>
 __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64_t nbytes,
                                               int lane) {
   const T* s = reinterpret_cast<const T*>(src);
@@ -87,16 +94,19 @@ __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = load<T, kReadOnly>(s + i + 32 * u);
 #pragma unroll
-    for (int u = 0; u < U; ++u) store<T>(d + i + 32 * u, v[u]);
+    for (int u = 0; u < U; ++u) {
+      if constexpr (kStream && sizeof(T) == 16) store_cs(reinterpret_cast<uint4*>(d + i + 32 * u), v[u]);
+      else store<T>(d + i + 32 * u, v[u]);
+    }
   }
   for (; i < n; i += 32) store<T>(d + i, load<T, kReadOnly>(s + i));
 }
 
-template <bool kReadOnly, int U = kUnroll>
+template <bool kReadOnly, int U = kUnroll, bool kStream = false>
 __device__ __forceinline__ void warp_copy_any(const char* src, char* dst, uint64_t nbytes,
                                               uint32_t vec_log2, int lane) {
   switch (vec_log2) {
-    case 4: warp_copy_run<uint4, kReadOnly, U>(src, dst, nbytes, lane); break;
+    case 4: warp_copy_run<uint4, kReadOnly, U, kStream>(src, dst, nbytes, lane); break;
     case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane); break;
     case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane); break;
     case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane); break;
@@ -132,7 +142,7 @@ __device__ __forceinline__ void row_offsets(const rs_copy_desc& D, uint32_t r, i
   }
 }
 
-template <bool kReadOnly, int U = kUnroll>
+template <bool kReadOnly, int U = kUnroll, bool kStream = false>
 __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t local_item,
                                                int lane) {
   const uint64_t r0 = local_item * D.rows_per_item;
@@ -142,11 +152,11 @@ __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t l
   for (uint64_t r = r0; r < r1; ++r) {
     int64_t so, dof;
     row_offsets(D, static_cast<uint32_t>(r), so, dof);
-    warp_copy_any<kReadOnly, U>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+    warp_copy_any<kReadOnly, U, kStream>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
   }
 }
 
-template <int U>
+template <int U, bool kStream = false>
 __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __restrict__ descs,
                                                       const uint64_t* __restrict__ item0,
                                                       uint32_t ndesc, uint64_t item_begin,
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __rest
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t item = item_begin + warp; item < item_end; item += nwarps) {
     const uint32_t di = find_desc(item0, ndesc, item);
-    warp_copy_item<true, U>(descs[di], item - descs[di].item0, lane);
+    warp_copy_item<true, U, kStream>(descs[di], item - descs[di].item0, lane);
   }
 }
 
@@ -584,6 +594,12 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
   switch (variant) {
     case 2:
       rs_copy_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 4:
+      rs_copy_kernel<4, true><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 5:
+      rs_copy_kernel<8, true><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
     case 3: {
       static bool configured = false;

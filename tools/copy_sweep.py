@@ -15,15 +15,12 @@ from paper_2605_22014_b200 import reshard as R  # noqa: E402
 from paper_2605_22014_b200 import specs  # noqa: E402
 from paper_2605_22014_b200.native import RS_DST, RS_SRC  # noqa: E402
 
-VARIANTS = [
-    dict(name="ldg4_auto", copy_kernel=1),
-    dict(name="ldg4_item128k", copy_kernel=1, item_bytes=128 << 10),
-    dict(name="ldg4_item4m", copy_kernel=1, item_bytes=4 << 20),
-    dict(name="ldg4_bps4", copy_kernel=1, blocks_per_sm=4),
-    dict(name="ldg8_auto", copy_kernel=2),
-    dict(name="bulk_auto", copy_kernel=3),
-    dict(name="bulk_item1m", copy_kernel=3, item_bytes=1 << 20),
-]
+VARIANTS = [dict(name="ldg4_auto", copy_kernel=1)]
+for ck, cname in ((1, "ldg4"), (2, "ldg8"), (4, "ldg4cs"), (5, "ldg8cs")):
+    for bps in (2, 3, 4):
+        for item in (0, 256 << 10):
+            VARIANTS.append(dict(name=f"{cname}_bps{bps}_item{item >> 10}k", copy_kernel=ck,
+                                 blocks_per_sm=bps, item_bytes=item))
 
 
 def main():
