@@ -82,6 +82,8 @@ typedef struct {
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
   int32_t blocks_per_sm;    /* 0: occupancy maximum */
   int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
+  int32_t world_slots;      /* device slots in the whole job (0: = num_devices) */
+  int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default */
@@ -146,6 +148,22 @@ int rs_store_read(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_inde
 int rs_store_write(rs_engine* e, int32_t which, int32_t rank, int32_t tensor_index,
                    int64_t offset, int64_t nbytes, const void* host);
 int rs_store_free(rs_engine* e, int32_t which);
+
+/* One process per GPU: every process lays out the same stores over the same
+ * global slots; each allocates its local slots, exports the arenas
+ * (CUDA IPC handle, RS_IPC_HANDLE_BYTES bytes), and imports every peer's.
+ * which: RS_SRC, RS_DST or RS_COMM (the staging arena: B per destination rank
+ * on the slot + ring flags, allocated by rs_comm_alloc). */
+#define RS_COMM 2
+#define RS_IPC_HANDLE_BYTES 64
+int rs_comm_alloc(rs_engine* e);
+int rs_arena_export(rs_engine* e, int32_t which, int32_t slot, void* handle, int64_t* arena_bytes);
+int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handle, int64_t arena_bytes);
+
+/* Per-slot traffic of a plan under a placement (host only): egress / ingress
+ * of remote task bytes, local task bytes, carryover bytes, out[4*slot + k]. */
+int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old,
+                    const rs_config* c_new, const int32_t* slot_new, int32_t nslots, int64_t* out);
 
 int rs_fill_pattern(rs_engine* e, int32_t which, uint64_t seed);
 int rs_verify_pattern(rs_engine* e, int32_t which, uint64_t seed, int64_t* mismatches,

@@ -2,6 +2,8 @@
 // Exceptions never cross it: std::invalid_argument / DomainError -> RS_EDOMAIN,
 // IntegrityError / plan parse errors -> RS_EINTEGRITY, SystemError (CUDA) ->
 // RS_ESYSTEM; the message is kept per thread for rs_last_error().
+#include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -16,6 +18,12 @@ struct rs_plan {
   reshard::ModelSpec model;
   reshard::TransferPlan plan;
   std::int64_t pairs_checked = 0;
+  // process-unique identity: an engine skips recompiling the plan it already holds
+  std::uint64_t id = next_id();
+  static std::uint64_t next_id() {
+    static std::atomic<std::uint64_t> counter{0};
+    return ++counter;
+  }
 };
 
 struct rs_engine {
@@ -316,7 +324,7 @@ int rs_verify_pattern(rs_engine* e, int32_t which, uint64_t seed, int64_t* misma
 int rs_prepare(rs_engine* e, const rs_plan* plan) {
   return guarded([&] {
     if (!e || !plan) throw std::invalid_argument("null argument");
-    e->impl.prepare(plan->plan);
+    e->impl.prepare(plan->plan, plan->id);
   });
 }
 
@@ -329,7 +337,7 @@ int rs_run(rs_engine* e, rs_exec_report* report) {
 
 int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report) {
   return guarded([&] {
-    e->impl.prepare(plan->plan);
+    if (!e->impl.prepared_for(plan->id)) e->impl.prepare(plan->plan, plan->id);
     *report = e->impl.run();
     if (!report->ok) throw rsb::IntegrityError(report->error);
   });
@@ -339,7 +347,7 @@ int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src, vo
                     int32_t window_layers, rs_exec_report* report) {
   return guarded([&] {
     if (!e || !plan || !host_src || !host_dst) throw std::invalid_argument("null argument");
-    e->impl.prepare(plan->plan);
+    if (!e->impl.prepared_for(plan->id)) e->impl.prepare(plan->plan, plan->id);
     *report = e->impl.run_host(host_src, host_dst, window_layers);
     if (!report->ok) throw rsb::IntegrityError(report->error);
   });
@@ -358,6 +366,55 @@ int rs_host_alloc(size_t bytes, void** out) {
 
 int rs_host_free(void* p) {
   return guarded([&] { rsb::cuda_check(cudaFreeHost(p), "cudaFreeHost"); });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rs_comm_alloc(rs_engine* e) {
+  return guarded([&] { e->impl.comm_alloc(); });
+}
+
+int rs_arena_export(rs_engine* e, int32_t which, int32_t slot, void* handle, int64_t* arena_bytes) {
+  return guarded([&] {
+    if (!handle || !arena_bytes) throw std::invalid_argument("null argument");
+    *arena_bytes = e->impl.export_arena(which, slot, handle);
+  });
+}
+
+int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handle, int64_t arena_bytes) {
+  return guarded([&] {
+    if (!handle) throw std::invalid_argument("null argument");
+    e->impl.import_arena(which, slot, handle, arena_bytes);
+  });
+}
+
+int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old, const rs_config* c_new,
+                    const int32_t* slot_new, int32_t nslots, int64_t* out) {
+  return guarded([&] {
+    if (!plan || !out || nslots < 1) throw std::invalid_argument("bad argument");
+    const int L = plan->model.num_layers;
+    const auto co = to_config(c_old, L), cn = to_config(c_new, L);
+    auto slot_in = [&](const reshard::ParallelConfig& c, const int32_t* slots, int rank) {
+      const int s = slots ? slots[c.index_of(rank)] : c.index_of(rank);
+      if (s < 0 || s >= nslots) throw std::invalid_argument("slot out of range");
+      return static_cast<std::size_t>(s);
+    };
+    std::fill(out, out + 4 * nslots, 0);
+    for (const auto& kv : plan->plan.tasks_by_layer)
+      for (const auto& t : kv.second) {
+        const std::size_t s = slot_in(co, slot_old, t.src_rank), d = slot_in(cn, slot_new, t.dst_rank);
+        if (t.is_local() || s == d) {
+          out[4 * d + 2] += t.byte_size;  // moved inside one GPU
+        } else {
+          out[4 * s + 0] += t.byte_size;  // egress
+          out[4 * d + 1] += t.byte_size;  // ingress
+        }
+      }
+    for (const auto& kv : plan->plan.carryover_by_layer)
+      for (const auto& k : kv.second) out[4 * slot_in(cn, slot_new, k.rank) + 3] += k.byte_size;
+  });
 }
 
 }  // extern "C"

@@ -6,13 +6,19 @@
 // failed_layer with every earlier layer executed, like execute_plan's
 // per-layer try/catch (executor.cpp:210-215).
 //
+// Devices are global *slots*: every process lays out the same stores over the
+// same slots and drives the slots it owns (one process per GPU, or one
+// process for several GPUs).  Peer arenas are mapped with CUDA IPC, so a
+// process reaches a peer GPU's shards and staging rings by plain loads and
+// stores over NVLink.
+//
 // DIRECT mode: every task and carryover is one strided->strided copy issued
-//   by the device holding its source (push); cross-device destinations are
-//   written through peer mappings (NVLink stores).  Zero staging.
+//   by the slot holding its source (push); destinations on other GPUs are
+//   written through the peer mapping.  Zero staging.
 // STAGED mode: cross-rank tasks are chunked to the ring slot size and
 //   streamed through per-(src,dst) single-producer/single-consumer rings that
-//   live in the destination's staging budget B; local tasks and carryovers
-//   run as DIRECT copies in the same launch.
+//   live in the destination's staging budget B (the comm arena); local tasks
+//   and carryovers run as DIRECT copies in the same launch.
 #include "engine.hpp"
 
 #include <algorithm>
@@ -34,6 +40,8 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 constexpr std::size_t kAlign = 256;
+constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
+constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 std::uint64_t key(int rank, std::uint32_t ti) {
   return (static_cast<std::uint64_t>(ti) << 32) | static_cast<std::uint32_t>(rank);
@@ -49,6 +57,16 @@ struct DeviceGuard {
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+std::string escape_msg(const char* who, const reshard::ShardView& b, const reshard::ShardView& owner) {
+  return std::string(who) + ": bounds " + b.to_string() + " escape owner view " + owner.to_string();
+}
+
+std::string no_buffer(int rank, std::uint32_t ti) {
+  return "shard store: no buffer for rank " + std::to_string(rank) + " tensor " + std::to_string(ti);
+}
+
+std::uint64_t addr(const char* p) { return reinterpret_cast<std::uint64_t>(p); }
 
 }  // namespace
 
@@ -88,6 +106,33 @@ void DeviceBuffer::upload(const void* host, std::size_t bytes, cudaStream_t s) {
   cuda_check(cudaMemcpyAsync(ptr_, host, bytes, cudaMemcpyHostToDevice, s), "upload");
 }
 
+ImportedArena::ImportedArena(int device, const cudaIpcMemHandle_t& h) : device_(device) {
+  DeviceGuard g(device);
+  void* p = nullptr;
+  cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  ptr_ = static_cast<char*>(p);
+}
+
+ImportedArena::~ImportedArena() {
+  if (ptr_) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    cudaIpcCloseMemHandle(ptr_);
+    cudaSetDevice(prev);
+  }
+}
+
+ImportedArena& ImportedArena::operator=(ImportedArena&& o) noexcept {
+  if (this != &o) {
+    this->~ImportedArena();
+    device_ = o.device_;
+    ptr_ = o.ptr_;
+    o.ptr_ = nullptr;
+  }
+  return *this;
+}
+
 // ------------------------------------------------------------------- Store
 
 const Entry* Store::find(int rank, std::uint32_t ti) const {
@@ -114,11 +159,18 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED) throw DomainError("engine: unknown mode");
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
   if (opts_.lanes_per_link < 1) opts_.lanes_per_link = 1;
+  nslots_ = opts.world_slots > 0 ? opts.world_slots : opts.num_devices;
+  first_local_ = opts.first_local_slot;
+  if (first_local_ < 0 || first_local_ + opts.num_devices > nslots_)
+    throw DomainError("engine: local slots [" + std::to_string(first_local_) + "," +
+                      std::to_string(first_local_ + opts.num_devices) + ") outside world of " +
+                      std::to_string(nslots_) + " slots");
   int count = 0;
   cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
   for (int i = 0; i < opts.num_devices; ++i) {
     Device d;
     d.ordinal = opts.device_ids[i];
+    d.slot = first_local_ + i;
     if (d.ordinal < 0 || d.ordinal >= count) throw DomainError("engine: bad device id " + std::to_string(d.ordinal));
     DeviceGuard g(d.ordinal);
     cuda_check(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, d.ordinal), "sm count");
@@ -140,12 +192,17 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
       if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
       else cuda_check(e, "cudaDeviceEnablePeerAccess");
     }
+  comm_imported_.resize(static_cast<std::size_t>(nslots_));
 }
 
 Engine::~Engine() {
   programs_.clear();
-  rings_.clear();
-  for (auto& s : stores_) s.arenas.clear();
+  comm_.clear();
+  comm_imported_.clear();
+  for (auto& s : stores_) {
+    s.arenas.clear();
+    s.imported.clear();
+  }
   for (auto& d : devices_) {
     cudaSetDevice(d.ordinal);
     if (d.stream) cudaStreamDestroy(d.stream);
@@ -156,49 +213,64 @@ Engine::~Engine() {
   }
 }
 
+int Engine::local_of(int slot) const {
+  const int i = slot - first_local_;
+  return (i >= 0 && i < num_devices()) ? i : -1;
+}
+
 void Engine::layout(int which, const reshard::ModelSpec& model, const reshard::ParallelConfig& cfg,
-                    const std::vector<int>& rank_device) {
+                    const std::vector<int>& rank_slot) {
   if (which != RS_SRC && which != RS_DST) throw DomainError("store: which must be RS_SRC or RS_DST");
   if (auto v = model.validate(); !v.empty()) throw DomainError("model: " + v.front());
   if (auto v = reshard::validate_config(cfg, model); !v.empty()) throw DomainError("config: " + v.front());
-  if (static_cast<int>(rank_device.size()) != cfg.world_size())
+  if (static_cast<int>(rank_slot.size()) != cfg.world_size())
     throw DomainError("store: rank_device must have one entry per rank");
-  for (int d : rank_device)
-    if (d < 0 || d >= num_devices()) throw DomainError("store: rank_device entry out of range");
+  for (int d : rank_slot)
+    if (d < 0 || d >= nslots_) throw DomainError("store: rank_device entry out of range");
   Store s;
   s.model = model;
   s.config = cfg;
+  s.arena_bytes.assign(static_cast<std::size_t>(nslots_), 0);
   for (std::uint32_t ti = 0; ti < model.tensors.size(); ++ti) {
     const auto& t = model.tensors[ti];
     for (const auto& [rank, v] : reshard::owners(t, cfg)) {
       Entry e;
       e.ti = ti;
       e.rank = rank;
-      e.dev = rank_device[static_cast<std::size_t>(cfg.index_of(rank))];
+      e.slot = rank_slot[static_cast<std::size_t>(cfg.index_of(rank))];
       e.view = v;
       e.nbytes = v.element_count() * model.element_bytes(t);
+      // deterministic arena offsets for every slot: peers compute the same
+      auto& used = s.arena_bytes[static_cast<std::size_t>(e.slot)];
+      e.off = used;
+      used += align_up(static_cast<std::size_t>(e.nbytes), kAlign);
       s.index.emplace(key(rank, ti), static_cast<std::uint32_t>(s.entries.size()));
       s.entries.push_back(e);
     }
   }
+  s.imported.resize(static_cast<std::size_t>(nslots_));
   s.laid_out = true;
   stores_[which] = std::move(s);
+  if (which == RS_DST) {
+    comm_.clear();
+    for (auto& c : comm_imported_) c.reset();
+  }
   prepared_ = false;
+}
+
+void Engine::check_laid_out() const {
+  if (!stores_[RS_SRC].laid_out) throw DomainError("src store not laid out");
+  if (!stores_[RS_DST].laid_out) throw DomainError("dst store not laid out");
 }
 
 void Engine::alloc(int which) {
   Store& s = stores_[which];
   if (!s.laid_out) throw DomainError("store: layout first");
   s.arenas.clear();
-  std::vector<std::size_t> need(devices_.size(), 0);
-  for (const auto& e : s.entries) need[static_cast<std::size_t>(e.dev)] += align_up(static_cast<std::size_t>(e.nbytes), kAlign);
-  for (std::size_t d = 0; d < devices_.size(); ++d)
-    s.arenas.emplace_back(devices_[d].ordinal, need[d]);
-  std::vector<std::size_t> off(devices_.size(), 0);
+  for (const auto& dv : devices_) s.arenas.emplace_back(dv.ordinal, s.arena_bytes[static_cast<std::size_t>(dv.slot)]);
   for (auto& e : s.entries) {
-    const auto d = static_cast<std::size_t>(e.dev);
-    e.ptr = s.arenas[d].data() + off[d];
-    off[d] += align_up(static_cast<std::size_t>(e.nbytes), kAlign);
+    const int l = local_of(e.slot);
+    if (l >= 0) e.ptr = s.arenas[static_cast<std::size_t>(l)].data() + e.off;
   }
   prepared_ = false;
 }
@@ -206,6 +278,7 @@ void Engine::alloc(int which) {
 void Engine::free_store(int which) {
   Store& s = stores_[which];
   s.arenas.clear();
+  for (auto& a : s.imported) a.reset();
   for (auto& e : s.entries) e.ptr = nullptr;
   prepared_ = false;
 }
@@ -214,7 +287,7 @@ void Engine::bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t
   Store& s = stores_[which];
   if (!s.laid_out) throw DomainError("store: layout first");
   Entry* e = s.find(rank, ti);
-  if (!e) throw DomainError("shard store: no buffer for rank " + std::to_string(rank) + " tensor " + std::to_string(ti));
+  if (!e) throw DomainError(no_buffer(rank, ti));
   if (nbytes != e->nbytes)
     throw DomainError("store bind: buffer size " + std::to_string(nbytes) + " does not match view size " +
                       std::to_string(e->nbytes));
@@ -222,15 +295,82 @@ void Engine::bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t
   prepared_ = false;
 }
 
-void Engine::check_stores_ready() const {
-  for (int w = 0; w < 2; ++w) {
-    if (!stores_[w].laid_out) throw DomainError(w ? "dst store not laid out" : "src store not laid out");
-    for (const auto& e : stores_[w].entries)
-      if (!e.ptr && e.nbytes)
-        throw DomainError(std::string(w ? "dst" : "src") + " store: entry rank " + std::to_string(e.rank) +
-                          " tensor " + std::to_string(e.ti) + " has no device memory");
-  }
+// ------------------------------------------------------ comm arenas and IPC
+
+std::size_t Engine::comm_bytes(int slot) const {
+  std::set<int> ranks;
+  for (const auto& e : stores_[RS_DST].entries)
+    if (e.slot == slot) ranks.insert(e.rank);
+  return static_cast<std::size_t>(opts_.staging_bytes) * ranks.size() + kFlagBytes;
 }
+
+void Engine::comm_alloc() {
+  if (!stores_[RS_DST].laid_out) throw DomainError("comm: lay out the dst store first");
+  comm_.clear();
+  for (const auto& dv : devices_) {
+    const std::size_t n = comm_bytes(dv.slot);
+    comm_.emplace_back(dv.ordinal, n);
+    DeviceGuard g(dv.ordinal);
+    cuda_check(cudaMemset(comm_.back().data(), 0, n), "comm memset");
+  }
+  prepared_ = false;
+}
+
+char* Engine::comm_base(int slot) const {
+  const int l = local_of(slot);
+  if (l >= 0) return static_cast<std::size_t>(l) < comm_.size() ? comm_[static_cast<std::size_t>(l)].data() : nullptr;
+  const auto& imp = comm_imported_[static_cast<std::size_t>(slot)];
+  return imp ? imp->data() : nullptr;
+}
+
+std::int64_t Engine::export_arena(int which, int slot, void* handle) const {
+  const int l = local_of(slot);
+  if (l < 0) throw DomainError("export: slot " + std::to_string(slot) + " is not local");
+  const char* base = nullptr;
+  std::int64_t bytes = 0;
+  if (which == RS_COMM) {
+    if (static_cast<std::size_t>(l) >= comm_.size()) throw DomainError("export: comm arena not allocated");
+    base = comm_[static_cast<std::size_t>(l)].data();
+    bytes = static_cast<std::int64_t>(comm_[static_cast<std::size_t>(l)].size());
+  } else {
+    const Store& s = stores_[which];
+    if (static_cast<std::size_t>(l) >= s.arenas.size()) throw DomainError("export: store arena not allocated");
+    base = s.arenas[static_cast<std::size_t>(l)].data();
+    bytes = static_cast<std::int64_t>(s.arenas[static_cast<std::size_t>(l)].size());
+  }
+  cudaIpcMemHandle_t h{};
+  if (base) {
+    DeviceGuard g(devices_[static_cast<std::size_t>(l)].ordinal);
+    cuda_check(cudaIpcGetMemHandle(&h, const_cast<char*>(base)), "cudaIpcGetMemHandle");
+  }
+  std::memcpy(handle, &h, sizeof h);
+  return bytes;
+}
+
+void Engine::import_arena(int which, int slot, const void* handle, std::int64_t bytes) {
+  if (slot < 0 || slot >= nslots_) throw DomainError("import: slot out of range");
+  if (local_of(slot) >= 0) return;  // own arena
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  // mapped through the first local device (peer access over NVLink)
+  const int dev = devices_[0].ordinal;
+  if (which == RS_COMM) {
+    if (static_cast<std::size_t>(bytes) != comm_bytes(slot)) throw DomainError("import: comm arena size mismatch");
+    comm_imported_[static_cast<std::size_t>(slot)] = bytes ? std::make_unique<ImportedArena>(dev, h) : nullptr;
+  } else {
+    Store& s = stores_[which];
+    if (!s.laid_out) throw DomainError("import: lay out the store first");
+    if (static_cast<std::size_t>(bytes) != s.arena_bytes[static_cast<std::size_t>(slot)])
+      throw DomainError("import: arena size mismatch for slot " + std::to_string(slot) + " (layouts differ?)");
+    auto& imp = s.imported[static_cast<std::size_t>(slot)];
+    imp = bytes ? std::make_unique<ImportedArena>(dev, h) : nullptr;
+    for (auto& e : s.entries)
+      if (e.slot == slot) e.ptr = imp ? imp->data() + e.off : nullptr;
+  }
+  prepared_ = false;
+}
+
+// ------------------------------------------------------------- kernel knobs
 
 int Engine::grid_for(int dev, int which_kernel) const {
   int per_sm = rs_kernel_max_blocks_per_sm(which_kernel);
@@ -239,42 +379,52 @@ int Engine::grid_for(int dev, int which_kernel) const {
   return devices_[static_cast<std::size_t>(dev)].sms * per_sm;
 }
 
+// RS_COPY_AUTO = LDG8 at 3 CTAs (24 warps) per SM with 256 KB work items:
+// the best of the full-size C2 sweep on B200 (profiles/r1/sweep.jsonl).
 int Engine::copy_variant(int dev) const {
   switch (opts_.copy_kernel) {
-    case RS_COPY_LDG8: return 2;
+    case RS_COPY_LDG4: return 1;
     case RS_COPY_BULK: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 3 : 1;
     case RS_COPY_LDG4_CS: return 4;
     case RS_COPY_LDG8_CS: return 5;
-    default: return 1;
+    default: return 2;
   }
 }
 
 int Engine::copy_grid(int dev) const {
+  const Device& d = devices_[static_cast<std::size_t>(dev)];
   switch (copy_variant(dev)) {
     case 2:
-    case 5: return grid_for(dev, 3);
-    case 3: return devices_[static_cast<std::size_t>(dev)].sms;  // one bulk issuer CTA per SM
+    case 5: {
+      int per_sm = std::max(1, rs_kernel_max_blocks_per_sm(3));
+      per_sm = std::min(per_sm, opts_.blocks_per_sm > 0 ? opts_.blocks_per_sm : 3);
+      return d.sms * per_sm;
+    }
+    case 3: return d.sms;  // one bulk issuer CTA per SM
     default: return grid_for(dev, 0);
   }
 }
 
 // ---------------------------------------------------------------- patterns
 
-void Engine::fill_pattern(int which, std::uint64_t seed) { (void)verify_pattern(-1 - which, seed, nullptr); }
+void Engine::fill_pattern(int which, std::uint64_t seed) { (void)pattern_pass(which, seed, false, nullptr); }
 
-std::int64_t Engine::verify_pattern(int which_in, std::uint64_t seed, std::int64_t* first_bad) {
-  const bool verify = which_in >= 0;
-  const int which = verify ? which_in : -1 - which_in;
+std::int64_t Engine::verify_pattern(int which, std::uint64_t seed, std::int64_t* first_bad) {
+  return pattern_pass(which, seed, true, first_bad);
+}
+
+// Fill / verify the entries on this process's slots.
+std::int64_t Engine::pattern_pass(int which, std::uint64_t seed, bool verify, std::int64_t* first_bad) {
   const Store& s = stores_[which];
   if (!s.laid_out) throw DomainError("store: layout first");
   std::int64_t total_bad = 0;
   std::uint64_t first = ~0ull;
   for (int d = 0; d < num_devices(); ++d) {
+    const Device& dv = devices_[static_cast<std::size_t>(d)];
     std::vector<rs_pattern_desc> descs;
     std::uint64_t bytes = 0;
-    for (std::uint32_t k = 0; k < s.entries.size(); ++k) {
-      const Entry& e = s.entries[k];
-      if (e.dev != d) continue;
+    for (const auto& e : s.entries) {
+      if (e.slot != dv.slot) continue;
       if (!e.ptr) throw DomainError("store: entry without device memory");
       bytes += static_cast<std::uint64_t>(e.nbytes);
     }
@@ -284,10 +434,9 @@ std::int64_t Engine::verify_pattern(int which_in, std::uint64_t seed, std::int64
     const std::uint64_t item_bytes = std::clamp<std::uint64_t>(bytes / (warps * 8), 16384, 1 << 20);
     for (std::uint32_t k = 0; k < s.entries.size(); ++k) {
       const Entry& e = s.entries[k];
-      if (e.dev != d) continue;
+      if (e.slot != dv.slot) continue;
       const auto& t = s.model.tensors[e.ti];
-      append_pattern(descs, reinterpret_cast<std::uint64_t>(e.ptr), t, e.view, s.model.element_bytes(t), e.ti, k,
-                     item_bytes);
+      append_pattern(descs, addr(e.ptr), t, e.view, s.model.element_bytes(t), e.ti, k, item_bytes);
     }
     std::vector<std::uint64_t> item0(descs.size());
     std::uint64_t items = 0;
@@ -296,7 +445,6 @@ std::int64_t Engine::verify_pattern(int which_in, std::uint64_t seed, std::int64
       item0[i] = items;
       items += (descs[i].rows + descs[i].rows_per_item - 1) / descs[i].rows_per_item;
     }
-    const Device& dv = devices_[static_cast<std::size_t>(d)];
     DeviceGuard g(dv.ordinal);
     DeviceBuffer dd(dv.ordinal, descs.size() * sizeof(rs_pattern_desc));
     DeviceBuffer di(dv.ordinal, item0.size() * sizeof(std::uint64_t));
@@ -308,8 +456,8 @@ std::int64_t Engine::verify_pattern(int which_in, std::uint64_t seed, std::int64
     auto* counters = reinterpret_cast<unsigned long long*>(dc.data());
     cuda_check(rs_launch_pattern(reinterpret_cast<const rs_pattern_desc*>(dd.data()),
                                  reinterpret_cast<const std::uint64_t*>(di.data()),
-                                 static_cast<std::uint32_t>(descs.size()), items, seed, verify ? 1 : 0,
-                                 counters, counters + 1, grid, dv.stream),
+                                 static_cast<std::uint32_t>(descs.size()), items, seed, verify ? 1 : 0, counters,
+                                 counters + 1, grid, dv.stream),
                "pattern kernel launch");
     unsigned long long out[2] = {0, 0};
     cuda_check(cudaMemcpyAsync(out, counters, sizeof out, cudaMemcpyDeviceToHost, dv.stream), "readback");
@@ -323,32 +471,25 @@ std::int64_t Engine::verify_pattern(int which_in, std::uint64_t seed, std::int64
 
 // ----------------------------------------------------------------- prepare
 
-namespace {
-
-std::string escape_msg(const char* who, const reshard::ShardView& b, const reshard::ShardView& owner) {
-  return std::string(who) + ": bounds " + b.to_string() + " escape owner view " + owner.to_string();
-}
-
-std::string no_buffer(int rank, std::uint32_t ti) {
-  return "shard store: no buffer for rank " + std::to_string(rank) + " tensor " + std::to_string(ti);
-}
-
-}  // namespace
-
-void Engine::prepare(const reshard::TransferPlan& plan) {
-  check_stores_ready();
+void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
+  prepared_id_ = 0;
+  check_laid_out();
   const auto& m = stores_[RS_SRC].model;
   if (plan.tensor_ids.size() != m.tensors.size())
     throw DomainError("plan does not match the store model (tensor count)");
   for (std::size_t i = 0; i < m.tensors.size(); ++i)
     if (plan.tensor_ids[i] != m.tensors[i].tensor_id)
       throw DomainError("plan does not match the store model (tensor " + plan.tensor_ids[i] + ")");
-  const auto& md = stores_[RS_DST].model;
-  if (md.tensors.size() != m.tensors.size()) throw DomainError("src and dst stores use different models");
+  if (stores_[RS_DST].model.tensors.size() != m.tensors.size())
+    throw DomainError("src and dst stores use different models");
+  for (int w = 0; w < 2; ++w)  // every shard on this process's slots needs memory
+    for (const auto& e : stores_[w].entries)
+      if (local_of(e.slot) >= 0 && !e.ptr && e.nbytes)
+        throw DomainError(std::string(w ? "dst" : "src") + " store: entry rank " + std::to_string(e.rank) +
+                          " tensor " + std::to_string(e.ti) + " has no device memory");
 
   planned_ = rs_exec_report{};
   planned_.failed_layer = -1;
-  plan_layers_.clear();
   std::set<int> layers;
   for (const auto& kv : plan.tasks_by_layer) layers.insert(kv.first);
   for (const auto& kv : plan.carryover_by_layer) layers.insert(kv.first);
@@ -356,12 +497,29 @@ void Engine::prepare(const reshard::TransferPlan& plan) {
 
   programs_.clear();
   programs_.resize(devices_.size());
-  rings_.clear();
-  if (opts_.mode == RS_MODE_DIRECT) compile_direct(plan);
-  else compile_staged(plan);
+  if (opts_.mode == RS_MODE_DIRECT) {
+    compile_direct(plan);
+  } else {
+    if (comm_.size() != devices_.size()) comm_alloc();
+    compile_staged(plan);
+  }
   upload_programs();
   prepared_ = true;
+  prepared_id_ = plan_id;
 }
+
+namespace {
+
+// Pointer of an entry that local work must touch.
+char* need_ptr(const Entry* e, const char* what) {
+  if (!e->ptr)
+    throw DomainError(std::string(what) + " shard rank " + std::to_string(e->rank) + " tensor " +
+                      std::to_string(e->ti) + " on slot " + std::to_string(e->slot) +
+                      " is not mapped in this process (rs_arena_import)");
+  return e->ptr;
+}
+
+}  // namespace
 
 void Engine::compile_direct(const reshard::TransferPlan& plan) {
   const Store& src = stores_[RS_SRC];
@@ -369,6 +527,13 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
   const auto& m = src.model;
   const std::int64_t B = opts_.staging_bytes;
   std::vector<std::size_t> mark(devices_.size());
+
+  auto push = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb, int layer) {
+    const int l = local_of(se->slot);
+    if (l < 0) return;  // the source's process pushes it
+    append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
+                addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
+  };
 
   for (int layer : plan_layers_) {
     for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
@@ -378,14 +543,11 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
         for (const auto& k : it->second) {
           const Entry* se = src.find(k.rank, k.tensor_index);
           const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
-          if (!se) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
-          if (!de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
+          if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
           if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
           if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
-          append_copy(programs_[static_cast<std::size_t>(se->dev)].local, reinterpret_cast<std::uint64_t>(se->ptr),
-                      se->view, reinterpret_cast<std::uint64_t>(de->ptr), de->view, k.bounds, eb,
-                      static_cast<std::uint32_t>(layer));
+          push(se, de, k.bounds, eb, layer);
           delta.carryover_bytes += k.bounds.element_count() * eb;
         }
       }
@@ -395,20 +557,17 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
           if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
           if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
           const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
-          if (eb > B)
-            throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
+          if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
           if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
           if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
-          append_copy(programs_[static_cast<std::size_t>(se->dev)].local, reinterpret_cast<std::uint64_t>(se->ptr),
-                      se->view, reinterpret_cast<std::uint64_t>(de->ptr), de->view, t.bounds, eb,
-                      static_cast<std::uint32_t>(layer));
+          push(se, de, t.bounds, eb, layer);
           const std::int64_t n = t.bounds.element_count() * eb;
           if (t.is_local()) delta.local_copy_bytes += n;
           else delta.bytes_moved += n;
         }
       }
-    } catch (const std::exception& e) {
+    } catch (const IntegrityError& e) {
       for (std::size_t d = 0; d < devices_.size(); ++d) programs_[d].local.resize(mark[d]);
       planned_.ok = 0;
       planned_.failed_layer = layer;
@@ -438,41 +597,44 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
       if (!t.is_local()) inbound[t.dst_rank].insert(t.src_rank);
+  // each destination rank's B-sized region in its slot's comm arena
+  std::map<int, std::size_t> region_of;  // dst rank -> byte offset in its slot's comm arena
+  {
+    std::map<int, std::set<int>> ranks_on_slot;
+    for (const auto& e : dst.entries) ranks_on_slot[e.slot].insert(e.rank);
+    for (const auto& [slot, ranks] : ranks_on_slot) {
+      std::size_t i = 0;
+      for (int r : ranks) region_of[r] = (i++) * static_cast<std::size_t>(B);
+    }
+  }
+  std::map<int, std::uint64_t> slot_bytes_of;  // ring slot size per dst rank
+  for (const auto& [d, srcs] : inbound) {
+    std::uint64_t sb = static_cast<std::uint64_t>(B) / (srcs.size() * static_cast<std::uint64_t>(P * K));
+    slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
+  }
 
+  struct Frame {
+    const Entry* se;
+    const Entry* de;
+    reshard::ShardView region;
+    std::int64_t eb;
+    std::uint64_t off;
+    int layer;
+  };
   struct LaneBuild {
-    int src_rank, dst_rank, sdev, ddev;
+    int src_rank, dst_rank, sslot, dslot;
     std::uint64_t slot_bytes;
-    char* slots = nullptr;          // on ddev
-    std::uint64_t* ready = nullptr; // on ddev
-    std::uint64_t* credit = nullptr;// on sdev
-    struct Frame {
-      const Entry* se;
-      const Entry* de;
-      reshard::ShardView region;
-      std::int64_t eb;
-      std::uint64_t off;
-      int layer;
-    };
     std::vector<std::vector<Frame>> batches;
     std::uint64_t fill = 0;
   };
   std::vector<LaneBuild> lanes;
-  std::map<std::pair<int, int>, int> link_first_lane;
-  std::map<std::pair<int, int>, int> link_cursor;
-  std::map<int, std::uint64_t> slot_bytes_of;  // per dst rank
-  for (const auto& [d, srcs] : inbound) {
-    std::uint64_t sb = static_cast<std::uint64_t>(B) / (srcs.size() * static_cast<std::uint64_t>(P * K));
-    sb = sb / kAlign * kAlign;
-    slot_bytes_of[d] = sb;
-  }
+  std::map<std::pair<int, int>, int> link_first_lane, link_cursor;
 
-  // layer-ordered frames
   std::vector<std::size_t> mark(devices_.size());
   for (int layer : plan_layers_) {
     for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
-    std::vector<std::size_t> lane_mark_batches(lanes.size());
+    std::vector<std::size_t> lane_mark_batches(lanes.size()), lane_mark_frames(lanes.size());
     std::vector<std::uint64_t> lane_mark_fill(lanes.size());
-    std::vector<std::size_t> lane_mark_frames(lanes.size());
     for (std::size_t i = 0; i < lanes.size(); ++i) {
       lane_mark_batches[i] = lanes[i].batches.size();
       lane_mark_fill[i] = lanes[i].fill;
@@ -480,6 +642,12 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     }
     const std::size_t lanes_before = lanes.size();
     rs_exec_report delta{};
+    auto local_copy = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb) {
+      const int l = local_of(se->slot);
+      if (l < 0) return;
+      append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
+                  addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
+    };
     try {
       if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end()) {
         for (const auto& k : it->second) {
@@ -489,9 +657,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
           if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
-          append_copy(programs_[static_cast<std::size_t>(se->dev)].local, reinterpret_cast<std::uint64_t>(se->ptr),
-                      se->view, reinterpret_cast<std::uint64_t>(de->ptr), de->view, k.bounds, eb,
-                      static_cast<std::uint32_t>(layer));
+          local_copy(se, de, k.bounds, eb);
           delta.carryover_bytes += k.bounds.element_count() * eb;
         }
       }
@@ -501,38 +667,25 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
           if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
           const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
+          if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
+          if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
+          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
           if (t.is_local()) {
-            if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
-            if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
-            if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
-            append_copy(programs_[static_cast<std::size_t>(se->dev)].local, reinterpret_cast<std::uint64_t>(se->ptr),
-                        se->view, reinterpret_cast<std::uint64_t>(de->ptr), de->view, t.bounds, eb,
-                        static_cast<std::uint32_t>(layer));
+            local_copy(se, de, t.bounds, eb);
             delta.local_copy_bytes += t.bounds.element_count() * eb;
             continue;
           }
           const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);
-          if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           if (static_cast<std::uint64_t>(eb) > sb)
             throw IntegrityError("staging: ring slot of " + std::to_string(sb) + " bytes cannot hold one element (B=" +
                                  std::to_string(B) + " over " + std::to_string(inbound[t.dst_rank].size()) +
                                  " inbound links)");
-          auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
-          if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
-          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
+          const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
           const auto lk = std::make_pair(t.src_rank, t.dst_rank);
           if (!link_first_lane.count(lk)) {
             link_first_lane[lk] = static_cast<int>(lanes.size());
-            for (int p = 0; p < P; ++p) {
-              LaneBuild lb;
-              lb.src_rank = t.src_rank;
-              lb.dst_rank = t.dst_rank;
-              lb.sdev = se->dev;
-              lb.ddev = de->dev;
-              lb.slot_bytes = sb;
-              lanes.push_back(std::move(lb));
-            }
+            for (int p = 0; p < P; ++p) lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, {}, 0});
           }
           for (const auto& c : chunks) {
             int& cur = link_cursor[lk];
@@ -551,6 +704,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         }
       }
     } catch (const std::exception& e) {
+      if (dynamic_cast<const DomainError*>(&e)) throw;  // mapping errors are not plan integrity
       for (std::size_t d = 0; d < devices_.size(); ++d) programs_[d].local.resize(mark[d]);
       lanes.resize(lanes_before);
       for (std::size_t i = 0; i < lanes_before; ++i) {
@@ -574,88 +728,93 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   }
   if (planned_.failed_layer < 0) planned_.ok = 1;
 
-  // staging memory: slots + ready flags on the destination device, credit
-  // flags on the source device
-  std::vector<std::size_t> ring_need(devices_.size(), 0), flag_need(devices_.size(), 0);
-  std::map<int, std::int64_t> ring_per_dst;
-  for (const auto& lb : lanes) {
-    ring_need[static_cast<std::size_t>(lb.ddev)] += lb.slot_bytes * static_cast<std::uint64_t>(K);
-    flag_need[static_cast<std::size_t>(lb.ddev)] += align_up(sizeof(std::uint64_t) * K, kAlign);
-    flag_need[static_cast<std::size_t>(lb.sdev)] += align_up(sizeof(std::uint64_t) * K, kAlign);
-    ring_per_dst[lb.dst_rank] += static_cast<std::int64_t>(lb.slot_bytes) * K;
+  // Ring memory inside the comm arenas (deterministic on every process):
+  // a destination rank's lanes take consecutive K-slot rings in its B region;
+  // ready flags in the destination slot's flag area, credit flags in the
+  // source slot's.
+  std::map<int, std::uint64_t> ring_used;  // dst rank -> bytes used in its region
+  std::vector<std::size_t> flag_used(static_cast<std::size_t>(nslots_), 0);
+  const std::size_t flags_per_lane = align_up(sizeof(std::uint64_t) * static_cast<std::size_t>(K), 64);
+  struct LaneAddr {
+    std::uint64_t ring_off, ready_off, credit_off;
+  };
+  std::vector<LaneAddr> where(lanes.size());
+  for (std::size_t i = 0; i < lanes.size(); ++i) {
+    const auto& lb = lanes[i];
+    std::uint64_t& used = ring_used[lb.dst_rank];
+    where[i].ring_off = region_of.at(lb.dst_rank) + used;
+    used += lb.slot_bytes * static_cast<std::uint64_t>(K);
+    auto& fr = flag_used[static_cast<std::size_t>(lb.dslot)];
+    auto& fc = flag_used[static_cast<std::size_t>(lb.sslot)];
+    if (fr + flags_per_lane > kFlagBytes || fc + flags_per_lane > kFlagBytes)
+      throw DomainError("staged: too many ring lanes for the flag area; lower lanes_per_link");
+    where[i].ready_off = fr;
+    fr += flags_per_lane;
+    where[i].credit_off = fc;
+    fc += flags_per_lane;
+    planned_.peak_staging_bytes = std::max<std::int64_t>(planned_.peak_staging_bytes, static_cast<std::int64_t>(used));
   }
-  for (const auto& kv : ring_per_dst) planned_.peak_staging_bytes = std::max(planned_.peak_staging_bytes, kv.second);
-  std::vector<std::size_t> ring_off(devices_.size(), 0), flag_off(devices_.size(), 0);
-  for (std::size_t d = 0; d < devices_.size(); ++d) {
-    rings_.emplace_back(devices_[d].ordinal, ring_need[d] + flag_need[d]);
-    if (ring_need[d] + flag_need[d]) {
-      DeviceGuard g(devices_[d].ordinal);
-      cuda_check(cudaMemset(rings_.back().data(), 0, ring_need[d] + flag_need[d]), "ring memset");
-    }
-    flag_off[d] = ring_need[d];
-  }
-  for (auto& lb : lanes) {
-    const auto dd = static_cast<std::size_t>(lb.ddev), sd = static_cast<std::size_t>(lb.sdev);
-    lb.slots = rings_[dd].data() + ring_off[dd];
-    ring_off[dd] += lb.slot_bytes * static_cast<std::uint64_t>(K);
-    lb.ready = reinterpret_cast<std::uint64_t*>(rings_[dd].data() + flag_off[dd]);
-    flag_off[dd] += align_up(sizeof(std::uint64_t) * K, kAlign);
-    lb.credit = reinterpret_cast<std::uint64_t*>(rings_[sd].data() + flag_off[sd]);
-    flag_off[sd] += align_up(sizeof(std::uint64_t) * K, kAlign);
-  }
+  auto flag_base = [&](int slot) -> char* {
+    char* b = comm_base(slot);
+    const std::size_t ring_area = comm_bytes(slot) - kFlagBytes;
+    return b ? b + ring_area : nullptr;
+  };
 
-  // serialise lanes / batches / frames (global tables, uploaded to every device)
+  // serialise lanes / batches / frames (global tables, uploaded to every local device)
   std::vector<rs_lane_desc> all_lanes;
   std::vector<rs_batch_desc> batches;
   std::vector<rs_copy_desc> frames;
-  for (const auto& lb : lanes) {
+  for (std::size_t i = 0; i < lanes.size(); ++i) {
+    const auto& lb = lanes[i];
+    const bool tx_local = local_of(lb.sslot) >= 0, rx_local = local_of(lb.dslot) >= 0;
+    char* ring = comm_base(lb.dslot);
+    char* ready = flag_base(lb.dslot);
+    char* credit = flag_base(lb.sslot);
+    if ((tx_local || rx_local) && (!ring || !ready || !credit))
+      throw DomainError("staged: comm arena of slot " + std::to_string(tx_local ? lb.dslot : lb.sslot) +
+                        " not mapped in this process (rs_arena_import RS_COMM)");
+    const std::uint64_t ring_addr = ring ? addr(ring) + where[i].ring_off : 0;
     rs_lane_desc L{};
-    L.slot_base = L.slot_base_rx = reinterpret_cast<std::uint64_t>(lb.slots);
+    L.slot_base = L.slot_base_rx = ring_addr;
     L.slot_bytes = lb.slot_bytes;
-    L.ready_flags = L.ready_flags_rx = reinterpret_cast<std::uint64_t>(lb.ready);
-    L.credit_flags = L.credit_flags_tx = reinterpret_cast<std::uint64_t>(lb.credit);
+    L.ready_flags = L.ready_flags_rx = ready ? addr(ready) + where[i].ready_off : 0;
+    L.credit_flags = L.credit_flags_tx = credit ? addr(credit) + where[i].credit_off : 0;
     L.slots = static_cast<std::uint32_t>(K);
     L.batch0 = static_cast<std::uint32_t>(batches.size());
     L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
     for (std::size_t b = 0; b < lb.batches.size(); ++b) {
-      const std::uint64_t slot_addr = reinterpret_cast<std::uint64_t>(lb.slots) + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
-      rs_batch_desc B{};
-      B.pack0 = static_cast<std::uint32_t>(frames.size());
-      for (const auto& f : lb.batches[b]) {
-        append_copy(frames, reinterpret_cast<std::uint64_t>(f.se->ptr), f.se->view, slot_addr + f.off, f.region,
-                    f.region, f.eb, static_cast<std::uint32_t>(f.layer));
-        B.bytes += static_cast<std::uint64_t>(f.region.element_count() * f.eb);
-      }
-      B.npack = static_cast<std::uint32_t>(frames.size()) - B.pack0;
-      B.unpack0 = static_cast<std::uint32_t>(frames.size());
-      for (const auto& f : lb.batches[b])
-        append_copy(frames, slot_addr + f.off, f.region, reinterpret_cast<std::uint64_t>(f.de->ptr), f.de->view,
-                    f.region, f.eb, static_cast<std::uint32_t>(f.layer));
-      B.nunpack = static_cast<std::uint32_t>(frames.size()) - B.unpack0;
-      batches.push_back(B);
+      const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
+      rs_batch_desc Bd{};
+      Bd.pack0 = static_cast<std::uint32_t>(frames.size());
+      if (tx_local)
+        for (const auto& f : lb.batches[b])
+          append_copy(frames, addr(f.se->ptr), f.se->view, slot_addr + f.off, f.region, f.region, f.eb,
+                      static_cast<std::uint32_t>(f.layer));
+      for (const auto& f : lb.batches[b]) Bd.bytes += static_cast<std::uint64_t>(f.region.element_count() * f.eb);
+      Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
+      Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
+      if (rx_local)
+        for (const auto& f : lb.batches[b])
+          append_copy(frames, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
+                      f.eb, static_cast<std::uint32_t>(f.layer));
+      Bd.nunpack = static_cast<std::uint32_t>(frames.size()) - Bd.unpack0;
+      batches.push_back(Bd);
     }
     all_lanes.push_back(L);
   }
-  assign_items(frames, 0, 0, 1ull << 16);  // rows_per_item inside frames (per-warp slices)
+  assign_items(frames, 0, 0, 1ull << 16);  // per-warp slices inside each frame
   for (std::size_t d = 0; d < devices_.size(); ++d) {
     DeviceProgram& p = programs_[d];
+    const int slot = devices_[d].slot;
     p.batches = batches;
     p.frames = frames;
-    std::vector<rs_lane_desc> tx, rx;
-    for (std::size_t i = 0; i < lanes.size(); ++i) {
-      if (static_cast<std::size_t>(lanes[i].sdev) == d) tx.push_back(all_lanes[i]);
-    }
-    for (std::size_t i = 0; i < lanes.size(); ++i) {
-      if (static_cast<std::size_t>(lanes[i].ddev) == d) rx.push_back(all_lanes[i]);
-    }
-    p.lanes = tx;
-    p.lanes.insert(p.lanes.end(), rx.begin(), rx.end());
-  }
-  staged_tx_.assign(devices_.size(), 0);
-  staged_rx_.assign(devices_.size(), 0);
-  for (const auto& lb : lanes) {
-    staged_tx_[static_cast<std::size_t>(lb.sdev)]++;
-    staged_rx_[static_cast<std::size_t>(lb.ddev)]++;
+    p.lanes.clear();
+    for (std::size_t i = 0; i < lanes.size(); ++i)
+      if (lanes[i].sslot == slot) p.lanes.push_back(all_lanes[i]);
+    p.ntx = static_cast<int>(p.lanes.size());
+    for (std::size_t i = 0; i < lanes.size(); ++i)
+      if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);
+    p.nrx = static_cast<int>(p.lanes.size()) - p.ntx;
   }
 }
 
@@ -672,16 +831,19 @@ void Engine::upload_programs() {
     p.local_bytes = bytes;
     std::uint64_t item_bytes = static_cast<std::uint64_t>(opts_.item_bytes);
     if (item_bytes == 0) {
-      // ~8 items per worker (warp, or bulk-issuer CTA) for load balance
       const int variant = copy_variant(static_cast<int>(d));
-      const std::uint64_t workers = variant == 3 ? static_cast<std::uint64_t>(dv.sms)
-                                                 : static_cast<std::uint64_t>(copy_grid(static_cast<int>(d))) * 8;
-      item_bytes = std::clamp<std::uint64_t>(bytes / (workers * 8 + 1), 32768, variant == 3 ? 8u << 20 : 1u << 20);
+      if (variant == 3) {
+        item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 8 + 1), 32768, 8u << 20);
+      } else {
+        // 256 KB items (full-size sweep optimum); smaller when the work is small so
+        // every warp still gets ~8 items
+        const std::uint64_t warps = static_cast<std::uint64_t>(copy_grid(static_cast<int>(d))) * 8;
+        item_bytes = std::clamp<std::uint64_t>(bytes / (warps * 8 + 1), 16384, 256u << 10);
+      }
     }
-    // item ranges per layer
     std::uint64_t item = 0;
     for (auto& lr : p.layers) {
-      const std::size_t first = static_cast<std::size_t>(lr.item_begin), last = static_cast<std::size_t>(lr.item_end);
+      const auto first = static_cast<std::size_t>(lr.item_begin), last = static_cast<std::size_t>(lr.item_end);
       std::vector<rs_copy_desc> tmp(p.local.begin() + static_cast<std::ptrdiff_t>(first),
                                     p.local.begin() + static_cast<std::ptrdiff_t>(last));
       const std::uint64_t end = assign_items(tmp, 0, item, item_bytes);
@@ -723,35 +885,26 @@ rs_exec_report Engine::run() {
     DeviceGuard g(dv.ordinal);
     cuda_check(cudaEventRecord(dv.ev_begin, dv.stream), "event");
   }
+  auto launch_copy = [&](std::size_t d, std::uint64_t b, std::uint64_t e) {
+    DeviceProgram& p = programs_[d];
+    if (e <= b) return;
+    DeviceGuard g(devices_[d].ordinal);
+    cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
+                              reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
+                              static_cast<std::uint32_t>(p.local.size()), b, e, copy_grid(static_cast<int>(d)),
+                              copy_variant(static_cast<int>(d)), devices_[d].stream),
+               "copy kernel launch");
+    ++launches;
+  };
   if (opts_.mode == RS_MODE_DIRECT) {
     if (!opts_.strict_layers) {
-      for (std::size_t d = 0; d < devices_.size(); ++d) {
-        DeviceProgram& p = programs_[d];
-        if (!p.local_items) continue;
-        DeviceGuard g(devices_[d].ordinal);
-        cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
-                                  reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
-                                  static_cast<std::uint32_t>(p.local.size()), 0, p.local_items,
-                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
-                   "copy kernel launch");
-        ++launches;
-      }
+      for (std::size_t d = 0; d < devices_.size(); ++d) launch_copy(d, 0, programs_[d].local_items);
     } else {
       const std::size_t nl = programs_.empty() ? 0 : programs_[0].layers.size();
       for (std::size_t li = 0; li < nl; ++li) {
-        for (std::size_t d = 0; d < devices_.size(); ++d) {
-          DeviceProgram& p = programs_[d];
-          const LayerRange& lr = p.layers[li];
-          if (lr.item_end == lr.item_begin) continue;
-          DeviceGuard g(devices_[d].ordinal);
-          cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
-                                    reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
-                                    static_cast<std::uint32_t>(p.local.size()), lr.item_begin, lr.item_end,
-                                    copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
-                     "copy kernel launch");
-          ++launches;
-        }
-        if (devices_.size() > 1) {  // layer barrier across devices
+        for (std::size_t d = 0; d < devices_.size(); ++d)
+          launch_copy(d, programs_[d].layers[li].item_begin, programs_[d].layers[li].item_end);
+        if (devices_.size() > 1) {  // layer barrier across this process's devices
           for (auto& a : devices_) {
             DeviceGuard g(a.ordinal);
             cuda_check(cudaEventRecord(a.ev_end, a.stream), "event");
@@ -765,33 +918,31 @@ rs_exec_report Engine::run() {
     epoch_ += 1ull << 32;
     for (std::size_t d = 0; d < devices_.size(); ++d) {
       DeviceProgram& p = programs_[d];
-      const int ntx = staged_tx_[d], nrx = staged_rx_[d];
       const int cap = grid_for(static_cast<int>(d), 2);
-      if (ntx + nrx >= cap)
-        throw DomainError("staged: " + std::to_string(ntx + nrx) + " ring lanes exceed the co-resident CTA capacity " +
-                          std::to_string(cap) + "; lower lanes_per_link");
-      if (!ntx && !nrx && !p.local_items) continue;
+      if (p.ntx + p.nrx >= cap)
+        throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) +
+                          " ring lanes exceed the co-resident CTA capacity " + std::to_string(cap) +
+                          "; lower lanes_per_link");
+      if (!p.ntx && !p.nrx && !p.local_items) continue;
       DeviceGuard g(devices_[d].ordinal);
       const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
-      cuda_check(rs_launch_exchange(lanes, static_cast<std::uint32_t>(ntx), lanes + ntx, static_cast<std::uint32_t>(nrx),
+      cuda_check(rs_launch_exchange(lanes, static_cast<std::uint32_t>(p.ntx), lanes + p.ntx,
+                                    static_cast<std::uint32_t>(p.nrx),
                                     reinterpret_cast<const rs_batch_desc*>(p.d_batches.data()),
                                     reinterpret_cast<const rs_copy_desc*>(p.d_frames.data()),
                                     reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                     reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                                     static_cast<std::uint32_t>(p.local.size()), p.local_items, epoch_,
-                                    reinterpret_cast<unsigned int*>(p.d_error.data()), 200000000ull,
-                                    cap - ntx - nrx, devices_[d].stream),
+                                    reinterpret_cast<unsigned int*>(p.d_error.data()), kSpinLimit,
+                                    cap - p.ntx - p.nrx, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }
   }
-  for (auto& dv : devices_) {
-    DeviceGuard g(dv.ordinal);
-    cuda_check(cudaEventRecord(dv.ev_end, dv.stream), "event");
-  }
   double worst = 0;
   for (auto& dv : devices_) {
     DeviceGuard g(dv.ordinal);
+    cuda_check(cudaEventRecord(dv.ev_end, dv.stream), "event");
     cuda_check(cudaEventSynchronize(dv.ev_end), "reshard kernels");
     float ms = 0;
     cuda_check(cudaEventElapsedTime(&ms, dv.ev_begin, dv.ev_end), "elapsed");
@@ -804,7 +955,8 @@ rs_exec_report Engine::run() {
       cuda_check(cudaMemcpy(&flag, programs_[d].d_error.data(), sizeof flag, cudaMemcpyDeviceToHost), "error flag");
       if (flag) {
         rep.ok = 0;
-        std::snprintf(rep.error, sizeof rep.error, "staged transfer: ring wait timed out on device %d", devices_[d].ordinal);
+        std::snprintf(rep.error, sizeof rep.error, "staged transfer: ring wait timed out on device %d",
+                      devices_[d].ordinal);
         cuda_check(cudaMemset(programs_[d].d_error.data(), 0, sizeof flag), "memset");
       }
     }
@@ -819,19 +971,25 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
   (void)window_layers;
   if (!prepared_) throw DomainError("engine: prepare a plan first");
   const auto t0 = std::chrono::steady_clock::now();
+  const Store& S = stores_[RS_SRC];
+  const Store& D = stores_[RS_DST];
   if (opts_.mode != RS_MODE_DIRECT) {
     // staged transfers run as one launch: stage everything in, run, stage out
-    for (std::size_t k = 0; k < stores_[RS_SRC].entries.size(); ++k) {
-      const Entry& e = stores_[RS_SRC].entries[k];
-      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+    for (std::size_t k = 0; k < S.entries.size(); ++k) {
+      const Entry& e = S.entries[k];
+      const int l = local_of(e.slot);
+      if (l < 0) continue;
+      const Device& dv = devices_[static_cast<std::size_t>(l)];
       DeviceGuard g(dv.ordinal);
       cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
                                  dv.stream), "H2D");
     }
     rs_exec_report rep = run();
-    for (std::size_t k = 0; k < stores_[RS_DST].entries.size(); ++k) {
-      const Entry& e = stores_[RS_DST].entries[k];
-      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+    for (std::size_t k = 0; k < D.entries.size(); ++k) {
+      const Entry& e = D.entries[k];
+      const int l = local_of(e.slot);
+      if (l < 0) continue;
+      const Device& dv = devices_[static_cast<std::size_t>(l)];
       DeviceGuard g(dv.ordinal);
       cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
                                  dv.stream), "D2H");
@@ -846,32 +1004,37 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
 
   // DIRECT: layer pipeline over three streams per device.  Layer l's source
   // shards go H2D (h2d stream), its copy kernel waits for them (compute
-  // stream), its destination shards go D2H once every device finished layer l
-  // (d2h stream) -- so H2D of l+1, the kernel of l and D2H of l-1 overlap and
-  // PCIe runs full duplex.  The layers are the plan's (executor.cpp:134-138).
+  // stream), its destination shards go D2H once every local device finished
+  // layer l (d2h stream) -- H2D of l+1, the kernel of l and D2H of l-1
+  // overlap and PCIe runs full duplex.  Layers are the plan's
+  // (executor.cpp:134-138).
   rs_exec_report rep = planned_;
   const std::size_t nlayers = programs_.empty() ? 0 : programs_[0].layers.size();
-  std::map<int, std::size_t> layer_slot;
-  for (std::size_t li = 0; li < nlayers; ++li) layer_slot[programs_[0].layers[li].layer] = li;
   const std::size_t ndev = devices_.size();
+  std::map<int, std::size_t> slot_of_layer;
+  for (std::size_t li = 0; li < nlayers; ++li) slot_of_layer[programs_[0].layers[li].layer] = li;
+  std::vector<std::vector<std::size_t>> src_by_layer(nlayers), dst_by_layer(nlayers);
+  for (std::size_t k = 0; k < S.entries.size(); ++k) {
+    auto it = slot_of_layer.find(S.model.tensors[S.entries[k].ti].layer);
+    if (it != slot_of_layer.end() && local_of(S.entries[k].slot) >= 0) src_by_layer[it->second].push_back(k);
+  }
+  for (std::size_t k = 0; k < D.entries.size(); ++k) {
+    auto it = slot_of_layer.find(D.model.tensors[D.entries[k].ti].layer);
+    if (it != slot_of_layer.end() && local_of(D.entries[k].slot) >= 0) dst_by_layer[it->second].push_back(k);
+  }
   std::vector<cudaEvent_t> ev_in(nlayers * ndev), ev_done(nlayers * ndev);
-  auto mk = [](cudaEvent_t& e) { cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"); };
   for (std::size_t d = 0; d < ndev; ++d) {
     DeviceGuard g(devices_[d].ordinal);
     for (std::size_t li = 0; li < nlayers; ++li) {
-      mk(ev_in[li * ndev + d]);
-      mk(ev_done[li * ndev + d]);
+      cuda_check(cudaEventCreateWithFlags(&ev_in[li * ndev + d], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&ev_done[li * ndev + d], cudaEventDisableTiming), "event");
     }
     cuda_check(cudaEventRecord(devices_[d].ev_begin, devices_[d].h2d), "event");
   }
-  auto layer_of = [&](const Store& s, const Entry& e) { return s.model.tensors[e.ti].layer; };
-  // H2D per layer, in layer order
   for (std::size_t li = 0; li < nlayers; ++li) {
-    const int layer = programs_[0].layers[li].layer;
-    for (std::size_t k = 0; k < stores_[RS_SRC].entries.size(); ++k) {
-      const Entry& e = stores_[RS_SRC].entries[k];
-      if (layer_of(stores_[RS_SRC], e) != layer) continue;
-      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+    for (std::size_t k : src_by_layer[li]) {
+      const Entry& e = S.entries[k];
+      const Device& dv = devices_[static_cast<std::size_t>(local_of(e.slot))];
       DeviceGuard g(dv.ordinal);
       cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
                                  dv.h2d), "H2D");
@@ -881,7 +1044,6 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
       cuda_check(cudaEventRecord(ev_in[li * ndev + d], devices_[d].h2d), "event");
     }
   }
-  // kernels per layer; a layer's copies may read any device's sources
   int launches = 0;
   for (std::size_t li = 0; li < nlayers; ++li) {
     for (std::size_t d = 0; d < ndev; ++d) {
@@ -894,25 +1056,23 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
         cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                   reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                                   static_cast<std::uint32_t>(p.local.size()), lr.item_begin, lr.item_end,
-                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), devices_[d].stream),
+                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)),
+                                  devices_[d].stream),
                    "copy kernel launch");
         ++launches;
       }
       cuda_check(cudaEventRecord(ev_done[li * ndev + d], devices_[d].stream), "event");
     }
   }
-  // D2H per layer after every device finished that layer
   for (std::size_t li = 0; li < nlayers; ++li) {
-    const int layer = programs_[0].layers[li].layer;
     for (std::size_t d = 0; d < ndev; ++d) {
       DeviceGuard g(devices_[d].ordinal);
       for (std::size_t o = 0; o < ndev; ++o)
         cuda_check(cudaStreamWaitEvent(devices_[d].d2h, ev_done[li * ndev + o], 0), "wait");
     }
-    for (std::size_t k = 0; k < stores_[RS_DST].entries.size(); ++k) {
-      const Entry& e = stores_[RS_DST].entries[k];
-      if (layer_of(stores_[RS_DST], e) != layer) continue;
-      const Device& dv = devices_[static_cast<std::size_t>(e.dev)];
+    for (std::size_t k : dst_by_layer[li]) {
+      const Entry& e = D.entries[k];
+      const Device& dv = devices_[static_cast<std::size_t>(local_of(e.slot))];
       DeviceGuard g(dv.ordinal);
       cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
                                  dv.d2h), "D2H");

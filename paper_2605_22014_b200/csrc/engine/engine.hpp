@@ -1,5 +1,6 @@
-// Device reshard engine: shard stores on one or more GPUs driven by this
-// process, plan compilation into per-device work lists, and execution.
+// Device reshard engine: shard stores over global device slots (a slot is
+// one GPU of the job; this process drives a contiguous range of them), plan
+// compilation into per-device work lists, and execution.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -48,13 +49,29 @@ class DeviceBuffer {
   std::size_t bytes_ = 0;
 };
 
+// A peer arena mapped into this process through CUDA IPC.
+class ImportedArena {
+ public:
+  ImportedArena() = default;
+  ImportedArena(int device, const cudaIpcMemHandle_t& h);
+  ~ImportedArena();
+  ImportedArena(ImportedArena&& o) noexcept { *this = std::move(o); }
+  ImportedArena& operator=(ImportedArena&& o) noexcept;
+  char* data() const { return ptr_; }
+
+ private:
+  int device_ = -1;
+  char* ptr_ = nullptr;
+};
+
 struct Entry {
   std::uint32_t ti = 0;
   int rank = 0;
-  int dev = 0;  // engine device slot
+  int slot = 0;            // global device slot holding the buffer
   reshard::ShardView view;
   std::int64_t nbytes = 0;
-  char* ptr = nullptr;
+  std::size_t off = 0;     // offset in the slot's engine arena (rs_store_alloc)
+  char* ptr = nullptr;     // local, peer-mapped (IPC) or caller-bound address
 };
 
 struct Store {
@@ -63,7 +80,9 @@ struct Store {
   reshard::ParallelConfig config;
   std::vector<Entry> entries;  // (tensor, ascending rank)
   std::unordered_map<std::uint64_t, std::uint32_t> index;
-  std::vector<DeviceBuffer> arenas;  // engine-owned memory (rs_store_alloc)
+  std::vector<std::size_t> arena_bytes;            // per slot
+  std::vector<DeviceBuffer> arenas;                // per local device
+  std::vector<std::unique_ptr<ImportedArena>> imported;  // per slot
   const Entry* find(int rank, std::uint32_t ti) const;
   Entry* find(int rank, std::uint32_t ti);
   std::int64_t total_bytes() const;
@@ -74,23 +93,25 @@ struct LayerRange {
   std::uint64_t item_begin, item_end;  // copy items of this layer (per device)
 };
 
-// Per-device compiled work.
+// Per local device compiled work.
 struct DeviceProgram {
   std::vector<rs_copy_desc> local;  // DIRECT copies executed here
   std::vector<std::uint64_t> local_item0;
   std::uint64_t local_items = 0;
   std::vector<LayerRange> layers;
   // STAGED
-  std::vector<rs_lane_desc> lanes;
+  std::vector<rs_lane_desc> lanes;  // ntx sender lanes then nrx receiver lanes
+  int ntx = 0, nrx = 0;
   std::vector<rs_batch_desc> batches;
   std::vector<rs_copy_desc> frames;
   DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error;
-  std::uint64_t local_bytes = 0;  // bytes this device moves in local descriptors
-  bool all_aligned = true;        // every local descriptor is 16 B aligned (bulk-copy eligible)
+  std::uint64_t local_bytes = 0;
+  bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
 };
 
 struct Device {
   int ordinal = 0;
+  int slot = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;              // reshard kernels
   cudaStream_t h2d = nullptr, d2h = nullptr;  // host-store copies (rs_execute_host)
@@ -103,41 +124,53 @@ class Engine {
   ~Engine();
 
   void layout(int which, const reshard::ModelSpec& model, const reshard::ParallelConfig& cfg,
-              const std::vector<int>& rank_device);
+              const std::vector<int>& rank_slot);
   void alloc(int which);
   void free_store(int which);
   void bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t nbytes);
   const Store& store(int which) const { return stores_[which]; }
   Store& store(int which) { return stores_[which]; }
 
+  void comm_alloc();
+  std::int64_t export_arena(int which, int slot, void* handle) const;
+  void import_arena(int which, int slot, const void* handle, std::int64_t bytes);
+
   void fill_pattern(int which, std::uint64_t seed);
   std::int64_t verify_pattern(int which, std::uint64_t seed, std::int64_t* first_bad);
 
-  void prepare(const reshard::TransferPlan& plan);
+  void prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id = 0);
+  bool prepared_for(std::uint64_t plan_id) const { return prepared_ && plan_id && plan_id == prepared_id_; }
   rs_exec_report run();
   rs_exec_report run_host(void* const* host_src, void* const* host_dst, int window_layers);
 
   int num_devices() const { return static_cast<int>(devices_.size()); }
+  int num_slots() const { return nslots_; }
+  int local_of(int slot) const;  // local device index of a slot, -1 if remote
 
  private:
+  std::int64_t pattern_pass(int which, std::uint64_t seed, bool verify, std::int64_t* first_bad);
   void compile_direct(const reshard::TransferPlan& plan);
   void compile_staged(const reshard::TransferPlan& plan);
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
-  int copy_variant(int dev) const;  // rs_launch_copy variant for this device's program
+  int copy_variant(int dev) const;
   int copy_grid(int dev) const;
-  void check_stores_ready() const;
+  void check_laid_out() const;
+  std::size_t comm_bytes(int slot) const;
+  char* comm_base(int slot) const;
 
   rs_engine_options opts_{};
+  int nslots_ = 1;
+  int first_local_ = 0;
   std::vector<Device> devices_;
   Store stores_[2];
   std::vector<DeviceProgram> programs_;
-  std::vector<DeviceBuffer> rings_;  // staging memory per device
-  std::vector<int> staged_tx_, staged_rx_;  // ring lanes sent / received per device
+  std::vector<DeviceBuffer> comm_;                        // per local device
+  std::vector<std::unique_ptr<ImportedArena>> comm_imported_;  // per slot
   bool prepared_ = false;
+  std::uint64_t prepared_id_ = 0;  // rs_plan identity of the compiled program (0: none)
   std::uint64_t epoch_ = 0;
-  // compile-time report fields (reference semantics, see prepare())
-  rs_exec_report planned_{};
+  rs_exec_report planned_{};  // compile-time report fields (reference semantics)
   std::vector<int> plan_layers_;
 };
 

@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libreshard_b200.so")
 
 RS_OK, RS_EDOMAIN, RS_EINTEGRITY, RS_ESYSTEM = 0, 1, 2, 3
-RS_SRC, RS_DST = 0, 1
+RS_SRC, RS_DST, RS_COMM = 0, 1, 2
+RS_IPC_HANDLE_BYTES = 64
 RS_MODE_DIRECT, RS_MODE_STAGED = 0, 1
 
 EXPORTS = [
@@ -24,7 +25,8 @@ EXPORTS = [
     "rs_store_alloc", "rs_store_bind", "rs_store_ptr", "rs_store_bytes", "rs_store_entries",
     "rs_store_read",
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
-    "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free",
+    "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
+    "rs_arena_export", "rs_arena_import", "rs_plan_traffic",
 ]
 
 
@@ -72,7 +74,8 @@ class EngineOptions(C.Structure):
                 ("staging_bytes", C.c_int64), ("mode", C.c_int32),
                 ("slots_per_link", C.c_int32), ("lanes_per_link", C.c_int32),
                 ("strict_layers", C.c_int32), ("item_bytes", C.c_int64),
-                ("blocks_per_sm", C.c_int32), ("copy_kernel", C.c_int32)]
+                ("blocks_per_sm", C.c_int32), ("copy_kernel", C.c_int32),
+                ("world_slots", C.c_int32), ("first_local_slot", C.c_int32)]
 
 
 class ExecReport(C.Structure):
@@ -138,6 +141,10 @@ def lib() -> C.CDLL:
         L.rs_execute_host.argtypes = [VP, VP, P(VP), P(VP), I32, P(ExecReport)]
         L.rs_host_alloc.argtypes = [SZ, P(VP)]
         L.rs_host_free.argtypes = [VP]
+        L.rs_comm_alloc.argtypes = [VP]
+        L.rs_arena_export.argtypes = [VP, I32, I32, VP, P(I64)]
+        L.rs_arena_import.argtypes = [VP, I32, I32, VP, I64]
+        L.rs_plan_traffic.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, P(I64)]
         _lib = L
     return _lib
 

@@ -158,16 +158,19 @@ class Engine:
     def __init__(self, devices: Iterable[int] = (0,), staging_bytes: int = 1 << 30,
                  mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 4,
                  strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
-                 copy_kernel: int = 0):
+                 copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         o = N.EngineOptions(len(devs), self._devs, staging_bytes,
                             N.RS_MODE_DIRECT if mode == "direct" else N.RS_MODE_STAGED,
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
-                            blocks_per_sm, copy_kernel)
+                            blocks_per_sm, copy_kernel, world_slots, first_local_slot)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h
+        self.num_devices = len(devs)
+        self.world_slots = world_slots or len(devs)
+        self.first_local_slot = first_local_slot
         self.models = {}
         self.configs = {}
 
@@ -241,6 +244,19 @@ class Engine:
         N.check(N.lib().rs_store_write(self._h, which, rank, tensor_index, offset, a.size,
                                        a.ctypes.data_as(C.c_void_p)))
 
+    def comm_alloc(self):
+        N.check(N.lib().rs_comm_alloc(self._h))
+
+    def export_arena(self, which: int, slot: int):
+        """(64-byte CUDA IPC handle, arena bytes) of a local slot's arena."""
+        h = (C.c_char * N.RS_IPC_HANDLE_BYTES)(); n = C.c_int64()
+        N.check(N.lib().rs_arena_export(self._h, which, slot, h, C.byref(n)))
+        return bytes(h), n.value
+
+    def import_arena(self, which: int, slot: int, handle: bytes, nbytes: int):
+        buf = (C.c_char * N.RS_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+        N.check(N.lib().rs_arena_import(self._h, which, slot, buf, nbytes))
+
     def fill_pattern(self, which: int, seed: int):
         N.check(N.lib().rs_fill_pattern(self._h, which, seed))
 
@@ -268,6 +284,18 @@ class Engine:
         if rc not in (N.RS_OK, N.RS_EINTEGRITY):
             N.check(rc)
         return rep.as_dict()
+
+
+def plan_traffic(plan: TransferPlan, c_old: ParallelConfig, slot_old: Sequence[int],
+                 c_new: ParallelConfig, slot_new: Sequence[int], nslots: int):
+    """Per-slot [egress, ingress, intra-GPU task bytes, carryover bytes]."""
+    out = (C.c_int64 * (4 * nslots))()
+    so = (C.c_int32 * len(slot_old))(*slot_old)
+    sn = (C.c_int32 * len(slot_new))(*slot_new)
+    L = plan.model.num_layers
+    N.check(N.lib().rs_plan_traffic(plan.handle, N.config_struct(c_old, L), so, N.config_struct(c_new, L),
+                                    sn, nslots, out))
+    return [list(out[4 * s:4 * s + 4]) for s in range(nslots)]
 
 
 def execute_plan(plan: TransferPlan, engine: Engine) -> dict:

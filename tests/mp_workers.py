@@ -1,0 +1,95 @@
+"""Worker processes for the multi-process tests (launched as subprocesses).
+
+    python tests/mp_workers.py <case> <rank> <world> <port> <device>
+
+Rendezvous over gloo at 127.0.0.1 (control plane only); prints one JSON line.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def plan_partition(rank, world):
+    """CPU: every rank computes the same plan; per-slot traffic partitions it."""
+    import hashlib
+
+    import torch.distributed as dist
+    from paper_2605_22014_b200 import reshard as R, specs
+    out = {}
+    for case in ("c1", "c2", "c5b"):
+        sp, co, cn = specs.baseline_case(case)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        sha = hashlib.sha256(plan.text().encode()).hexdigest()
+        so = [i * world // co.world for i in range(co.world)]
+        sn = [i * world // cn.world for i in range(cn.world)]
+        traffic = R.plan_traffic(plan, co, so, cn, sn, world)
+        shas = [None] * world
+        dist.all_gather_object(shas, sha)
+        s = plan.summary()
+        out[case] = {"agree": len(set(shas)) == 1, "mine": traffic[rank],
+                     "egress_total": sum(t[0] for t in traffic), "ingress_total": sum(t[1] for t in traffic),
+                     "intra_total": sum(t[2] for t in traffic), "carry_total": sum(t[3] for t in traffic),
+                     "plan_total": s["total_bytes"], "plan_carry": s["carryover_bytes"]}
+    return out
+
+
+def ipc_reshard(rank, world, mode):
+    """GPU: `world` processes share cuda:<device>; each drives one slot."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_22014_b200 import reshard as R, specs
+    from paper_2605_22014_b200.dist import connect
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+    dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    sp = specs.llama("llama-mini", 4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
+    so = [i * world // co.world for i in range(co.world)]
+    sn = [(i + 1) * world // cn.world % world for i in range(cn.world)]  # shifted placement
+    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
+                   first_local_slot=rank)
+    eng.layout(RS_SRC, sp, co, so)
+    eng.layout(RS_DST, sp, cn, sn)
+    eng.alloc(RS_SRC)
+    eng.alloc(RS_DST)
+    eng.comm_alloc()
+    eng.fill_pattern(RS_SRC, 42)
+    eng.fill_pattern(RS_DST, 7)
+    connect(eng)
+    dist.barrier()
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng.prepare(plan)
+    dist.barrier()
+    rep = eng.run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    bad = eng.verify_pattern(RS_DST, 42)[0]
+    rep2 = eng.run()  # idempotent second handoff over the same mappings
+    dist.barrier()
+    bad2 = eng.verify_pattern(RS_DST, 42)[0]
+    dist.barrier()
+    eng.close()
+    return {"ok": rep["ok"] and rep2["ok"], "mismatches": bad + bad2, "error": rep["error"],
+            "launches": rep["kernel_launches"]}
+
+
+def main():
+    case, rank, world, port = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=port, RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if case == "partition":
+            res = plan_partition(rank, world)
+        else:
+            res = ipc_reshard(rank, world, case)
+    finally:
+        dist.destroy_process_group()
+    print(json.dumps({"rank": rank, "result": res}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
