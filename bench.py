@@ -184,28 +184,44 @@ def reference_arm(args) -> None:
 
 
 def ours(args) -> None:
+    """N=1: every logical rank on cuda:0.  N>1 (torchrun, one process per GPU):
+    rank id r of both configs lives on GPU r*N//8 (iota placement at N=8);
+    each process drives its GPU's slot, peer arenas are CUDA-IPC mapped and
+    every byte moves GPU->GPU over NVLink inside our kernels.  The control
+    plane (handle exchange, barriers, max-over-ranks timing) is gloo."""
     import torch
     from paper_2605_22014_b200 import reshard as R
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
 
     rank, world, local = dist_env()
+    device = 0 if os.environ.get("RS_BENCH_SAME_DEVICE") else local
+    torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
     sp, co, cn, desc = workload(args.gpus, args.profile_layers)
     plan = R.compute_transfer_plan(co, cn, sp)
     summ = plan.summary()
     total = summ["total_bytes"]
-    algo_bytes = 2 * (total + summ["carryover_bytes"])  # read + write of every moved byte
+    nranks = max(max(co.ranks), max(cn.ranks)) + 1
+    slot_of = lambda r: r * world // nranks  # noqa: E731
+    so = [slot_of(r) for r in co.ranks]
+    sn = [slot_of(r) for r in cn.ranks]
+    traffic = R.plan_traffic(plan, co, so, cn, sn, world)
 
-    eng = R.Engine([local], staging_bytes=args.staging_bytes, mode=args.mode,
-                   lanes_per_link=args.lanes, strict_layers=args.strict)
-    eng.layout(RS_SRC, sp, co)
-    eng.layout(RS_DST, sp, cn)
+    eng = R.Engine([device], staging_bytes=args.staging_bytes, mode=args.mode, lanes_per_link=args.lanes,
+                   strict_layers=args.strict, world_slots=world, first_local_slot=rank)
+    eng.layout(RS_SRC, sp, co, so)
+    eng.layout(RS_DST, sp, cn, sn)
     eng.alloc(RS_SRC)
     eng.alloc(RS_DST)
+    if args.mode == "staged":
+        eng.comm_alloc()
     eng.fill_pattern(RS_SRC, SEED)
+    if world > 1:
+        from paper_2605_22014_b200.dist import connect
+        from paper_2605_22014_b200.native import RS_COMM
+        connect(eng, which=(RS_SRC, RS_DST) + ((RS_COMM,) if args.mode == "staged" else ()))
     eng.prepare(plan)
 
     def barrier():
@@ -214,51 +230,71 @@ def ours(args) -> None:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
+        barrier()
         rep = eng.run()
         assert rep["ok"], rep
-    bad_src = eng.verify_pattern(RS_DST, SEED)[0]
+    barrier()
+    bad_warm = eng.verify_pattern(RS_DST, SEED)[0]
 
     barrier()
     launches = 0
     dev_ms = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
+            if world > 1:
+                torch.distributed.barrier()  # every GPU starts the handoff together
             rep = eng.run()
             dev_ms.append(rep["device_ms"])
             launches += rep["kernel_launches"]
         barrier()
         wall = time.perf_counter() - t0
     step_ms = sum(dev_ms) / len(dev_ms)
-    if world > 1:
-        t = torch.tensor([step_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        step_ms = float(t.item())
     mismatches = eng.verify_pattern(RS_DST, SEED)[0]
+    if world > 1:
+        t = torch.tensor([step_ms, float(mismatches), float(bad_warm), float(launches)], dtype=torch.float64)
+        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
+        tt = t[1:].clone()
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.SUM)
+        step_ms = float(t[0])
+        mismatches, bad_warm, launches = int(tt[0]), int(tt[1]), int(tt[2])
 
     pk = peaks()
-    achieved = algo_bytes / (step_ms / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get("rs_copy_kernel_dram_bytes_per_launch")
+    if world == 1:
+        algo_bytes = 2 * (total + summ["carryover_bytes"])  # read + write of every moved byte
+        achieved = algo_bytes / (step_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "kernel": "rs_copy_kernel",
+                "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"]}
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                roof["traffic"] = json.load(f).get("rs_copy_kernel_dram_bytes_per_launch")
+    else:
+        # the busiest GPU's NVLink direction bounds the handoff
+        link = max(max(t[0], t[1]) for t in traffic)
+        achieved = link / (step_ms / 1e3) / 1e9
+        nvl = 770.0
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": nvl, "unit": "GB/s",
+                "frac": round(achieved / nvl, 4), "traffic": None, "kernel": "rs_copy_kernel (peer stores)",
+                "algorithmic_bytes_per_launch": link,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                "per_gpu_egress_ingress_GB": [[round(t[0] / 1e9, 2), round(t[1] / 1e9, 2)] for t in traffic]}
 
-    line = {"metric": METRIC, "value": round(world * total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
+    line = {"metric": METRIC, "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(step_ms, 4), "handoff_ms": round(step_ms, 4),
-            "higher_is_better": HIGH_IS_GOOD, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": HIGH_IS_GOOD, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic: reference pattern state (shard_store.cpp:51-85), random-init-equivalent bytes",
-            "config": {"workload": desc, "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
+            "config": {"workload": desc if world == 1 else desc.replace(
+                           "all logical ranks on one B200 (intra-device relayout)",
+                           f"rank r on GPU r*{world}//8, one process per GPU"),
+                       "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
                        "tasks": summ["task_count"], "mode": args.mode, "staging_bytes": args.staging_bytes,
-                       "strict_layers": bool(args.strict),
+                       "strict_layers": bool(args.strict), "copy_kernel": "LDG8 x 3 CTAs/SM, 256 KB items",
                        "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-                         "kernel": "rs_copy_kernel",
-                         "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"]},
-            "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
-            "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_src)}}
+            "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
+            "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = run_reference_cpu(1, 2, 1, 0, args.staging_bytes)
@@ -269,7 +305,12 @@ def ours(args) -> None:
                            f"slice, both dtype groups, {res['plan_bytes'] / 1e9:.2f} GB, 1 thread "
                            f"(the reference is single-threaded) of {os.cpu_count()} host cores")}
     if not args.no_e2e:
-        line["e2e"] = e2e(eng, plan, total, args)
+        pos_old = {r: i for i, r in enumerate(co.ranks)}
+        pos_new = {r: i for i, r in enumerate(cn.ranks)}
+
+        def local_entry(which, r):
+            return (so[pos_old[r]] if which == RS_SRC else sn[pos_new[r]]) == rank
+        line["e2e"] = e2e(eng, plan, total, args, world, local_entry)
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
@@ -277,30 +318,42 @@ def ours(args) -> None:
         torch.distributed.destroy_process_group()
 
 
-def e2e(eng, plan, total, args) -> dict:
+def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     """Same handoff through rs_execute_host with HOST shard stores: every step
-    copies all source shards H2D from pinned memory and all destination shards
-    D2H.  Host RAM cannot hold a second 94 GB store next to the pinned source
-    (196 GB box), so destination shards land in a 4 GiB pinned window that
-    successive shards overwrite; every byte still crosses PCIe."""
+    copies all (this process's) source shards H2D from pinned memory and all
+    destination shards D2H, layer-pipelined.  Host RAM cannot hold a second
+    94 GB store next to the pinned source (196 GB box), so destination shards
+    land in a 4 GiB pinned window that successive shards overwrite; every
+    byte still crosses PCIe.  On this box H2D alone runs 55 GB/s, D2H alone
+    57 GB/s, both together 65.7 GB/s combined (tools/e2e_probe.py): the e2e
+    step is host-transfer bound, the reshard kernel is ~1% of it."""
+    import torch
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
+    from paper_2605_22014_b200.reshard import PinnedBuffer
 
     src = eng.entries(RS_SRC)
     dst = eng.entries(RS_DST)
-    h2d = sum(n for _, _, n in src)
-    d2h = sum(n for _, _, n in dst)
-    from paper_2605_22014_b200.reshard import PinnedBuffer
-    host_src = PinnedBuffer(h2d)
+    src_local = [local_entry(RS_SRC, r) for _, r, _ in src]
+    dst_local = [local_entry(RS_DST, r) for _, r, _ in dst]
+    h2d = sum(n for (_, _, n), l in zip(src, src_local) if l)
+    d2h = sum(n for (_, _, n), l in zip(dst, dst_local) if l)
+    host_src = PinnedBuffer(max(h2d, 1))
     window = PinnedBuffer(4 << 30)
     # the host source store holds the device source state, so the e2e output
     # is checkable against the analytic pattern afterwards
     off, src_ptrs = 0, []
-    for ti, r, n in src:
+    for (ti, r, n), l in zip(src, src_local):
+        if not l:
+            src_ptrs.append(0)
+            continue
         src_ptrs.append(host_src.ptr + off)
         eng.read_to(RS_SRC, r, ti, host_src.ptr + off, n)
         off += n
     dst_ptrs, woff = [], 0
-    for _, _, n in dst:
+    for (_, _, n), l in zip(dst, dst_local):
+        if not l:
+            dst_ptrs.append(0)
+            continue
         if woff + n > window.nbytes:
             woff = 0
         dst_ptrs.append(window.ptr + woff)
@@ -309,17 +362,27 @@ def e2e(eng, plan, total, args) -> dict:
     times, ok = [], True
     steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(steps):
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         rep = eng.execute_host(plan, src_ptrs, dst_ptrs)
+        if world > 1:
+            torch.distributed.barrier()  # every GPU's host stores complete
         times.append(time.perf_counter() - t0)
         ok &= rep["ok"]
     bad = eng.verify_pattern(RS_DST, SEED)[0]
     host_src.free()
     window.free()
     mean = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([float(h2d), float(d2h), float(bad)], dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        h2d, d2h, bad = int(t[0]), int(t[1]), int(t[2])
     return {"value": round(total / mean / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(mean, 4),
-            "path": "rs_execute_host (C ABI, host shard stores)", "ok": bool(ok and bad == 0)}
+            "path": "rs_execute_host (C ABI, host shard stores)",
+            "bound": "host<->device transfer (H2D 55, D2H 57, concurrent 65.7 GB/s combined, measured)",
+            "ok": bool(ok and bad == 0)}
 
 
 def main() -> None:
