@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
         for (uint32_t f = 0; f < B.npack; ++f) {
           const rs_copy_desc& D = frames[B.pack0 + f];
           const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
-          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<true>(D, it, lane_id);
+          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<true, 8>(D, it, lane_id);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
         for (uint32_t f = 0; f < B.nunpack; ++f) {
           const rs_copy_desc& D = frames[B.unpack0 + f];
           const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
-          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<false>(D, it, lane_id);
+          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<false, 8>(D, it, lane_id);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x - ntx - nrx) * blockDim.x) >> 5;
   for (uint64_t item = warp; item < local_items; item += nwarps) {
     const uint32_t di = find_desc(local_item0, nlocal, item);
-    warp_copy_item<true>(local_descs[di], item - local_descs[di].item0, lane_id);
+    warp_copy_item<true, 8>(local_descs[di], item - local_descs[di].item0, lane_id);
   }
 }
 
