@@ -393,7 +393,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="direct", choices=["direct", "staged"])
     ap.add_argument("--staging-bytes", type=int, default=1 << 30)
-    ap.add_argument("--lanes", type=int, default=4)
+    ap.add_argument("--lanes", type=int, default=0, help="ring lanes per link (0: automatic)")
     ap.add_argument("--strict", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -158,7 +158,7 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED) throw DomainError("engine: unknown mode");
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
-  if (opts_.lanes_per_link < 1) opts_.lanes_per_link = 1;
+  if (opts_.lanes_per_link < 0) opts_.lanes_per_link = 0;  // 0: automatic (compile_staged)
   nslots_ = opts.world_slots > 0 ? opts.world_slots : opts.num_devices;
   first_local_ = opts.first_local_slot;
   if (first_local_ < 0 || first_local_ + opts.num_devices > nslots_)
@@ -590,13 +590,43 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   const Store& dst = stores_[RS_DST];
   const auto& m = src.model;
   const std::int64_t B = opts_.staging_bytes;
-  const int P = opts_.lanes_per_link, K = opts_.slots_per_link;
+  const int K = opts_.slots_per_link;
 
   // inbound links per destination rank (remote tasks only)
   std::map<int, std::set<int>> inbound;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
       if (!t.is_local()) inbound[t.dst_rank].insert(t.src_rank);
+
+  // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
+  // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
+  // the sender + receiver CTAs of the busiest slot stop being co-resident.
+  // Automatic choice: the largest power of two <= 16 that keeps them within
+  // 3/4 of one device's CTA capacity (same answer on every process).
+  int P = opts_.lanes_per_link;
+  if (P == 0) {
+    std::vector<int> slot_links(static_cast<std::size_t>(nslots_), 0);
+    std::set<std::pair<int, int>> links;
+    for (const auto& kv : plan.tasks_by_layer)
+      for (const auto& t : kv.second)
+        if (!t.is_local()) links.insert({t.src_rank, t.dst_rank});
+    auto slot_of = [&](const Store& s, int rank) {
+      for (const auto& e : s.entries)
+        if (e.rank == rank) return e.slot;
+      return 0;
+    };
+    std::map<int, int> src_slot, dst_slot;
+    for (const auto& [s, d] : links) {
+      if (!src_slot.count(s)) src_slot[s] = slot_of(src, s);
+      if (!dst_slot.count(d)) dst_slot[d] = slot_of(dst, d);
+      ++slot_links[static_cast<std::size_t>(src_slot[s])];
+      ++slot_links[static_cast<std::size_t>(dst_slot[d])];
+    }
+    const int busiest = std::max(1, *std::max_element(slot_links.begin(), slot_links.end()));
+    const int capacity = grid_for(0, 2) * 3 / 4;
+    P = 16;
+    while (P > 1 && busiest * P > capacity) P /= 2;
+  }
   // each destination rank's B-sized region in its slot's comm arena
   std::map<int, std::size_t> region_of;  // dst rank -> byte offset in its slot's comm arena
   {
