@@ -76,6 +76,10 @@ struct TensorSpec {
   std::optional<int> tp_shard_axis;
   TensorRole role = TensorRole::kParameter;
   std::int64_t element_bytes = 0;  // extension: 0 -> ModelSpec::bytes_per_element
+  // extension (distributed optimizer, BASELINE config 3): under a config with
+  // distributed_optimizer() the TP block is further split into dp ceil chunks
+  // along this axis, one per DP rank; nullopt = DP-replicated
+  std::optional<int> dp_shard_axis;
   std::int64_t element_count() const;
 };
 
@@ -130,6 +134,9 @@ class ParallelConfig {
   std::vector<int> stage_ranks(int stage) const;
   bool same_layout(const ParallelConfig& o) const;
   ParallelConfig with_generation(std::uint64_t gen) const;
+  // extension: DP ranks shard tensors that declare a dp_shard_axis (ZeRO-1)
+  bool distributed_optimizer() const { return dist_opt_; }
+  ParallelConfig with_distributed_optimizer(bool on) const;
 
  private:
   std::uint64_t gen_ = 0;
@@ -137,11 +144,14 @@ class ParallelConfig {
   std::vector<int> ranks_;
   std::vector<int> stage_of_;
   std::unordered_map<int, int> index_;  // rank id -> position (first occurrence)
+  bool dist_opt_ = false;
 };
 
 std::vector<std::string> validate_config(const ParallelConfig& config, const ModelSpec& model);
 
 std::optional<Interval> tp_block(std::int64_t axis_len, int tp_degree, int tp_index);
+// Ceil chunk `index` of `parts` over [iv.lo, iv.hi) (extension: DP chunks inside a TP block)
+std::optional<Interval> dp_chunk(const Interval& iv, int parts, int index);
 std::optional<ShardView> view(const TensorSpec& tensor, const ParallelConfig& config, int rank);
 std::map<int, ShardView> owners(const TensorSpec& tensor, const ParallelConfig& config);
 

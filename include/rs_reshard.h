@@ -52,6 +52,8 @@ typedef struct {
   int32_t num_ranks;
   const int32_t* ranks;       /* ordered rank ids (placement is semantic) */
   const int32_t* layer_stage; /* num_layers entries, or NULL: default ceil split */
+  int32_t distributed_optimizer; /* extension: DP-shard tensors with a dp_shard_axis (ZeRO-1) */
+  int32_t reserved;
 } rs_config;
 
 typedef struct {

@@ -36,6 +36,7 @@ typedef struct { int nd; iv_t b[MAXD]; } box_t;
 typedef struct {
   char id[128];
   int layer, nd, axis, bpe;       /* axis -1: replicated */
+  int dp_axis;                    /* extension: -1, or the distributed-optimizer DP split axis */
   int64_t shape[MAXD];
 } tspec_t;
 
@@ -51,11 +52,13 @@ typedef struct {
   int32_t tp, pp, dp, nranks;
   const int32_t* ranks;
   const int32_t* layer_stage; /* NULL: default ceil split */
+  int32_t dist_opt;           /* extension (no reference counterpart): DP-shard dp_axis tensors */
+  int32_t reserved;
 } orc_config;
 
 typedef struct {
   uint64_t gen;
-  int tp, pp, dp, n, L;
+  int tp, pp, dp, n, L, dist_opt;
   int* ranks;
   int* stage;
 } cfg_t;
@@ -134,6 +137,11 @@ static int parse_spec(const char* text, spec_t* sp, char* err, size_t errn) {
         snprintf(err, errn, "spec parse: bad tensor line"); return 1;
       }
       t->axis = (axis[0] == '-') ? -1 : atoi(axis);
+      t->dp_axis = -1;
+      {
+        const char* dpo = strstr(line, " dp=");  /* optional extension token */
+        if (dpo) t->dp_axis = atoi(dpo + 4);
+      }
       char* q = shape;
       while (*q && t->nd < MAXD) {
         t->shape[t->nd++] = strtoll(q, &q, 10);
@@ -153,7 +161,7 @@ static void free_spec(spec_t* sp) { free(sp->t); sp->t = NULL; }
 /* default_layer_assignment: parallel_config.cpp:19-29 */
 static void load_cfg(const orc_config* c, int L, cfg_t* out) {
   out->gen = c->gen; out->tp = c->tp; out->pp = c->pp; out->dp = c->dp;
-  out->n = c->nranks; out->L = L;
+  out->n = c->nranks; out->L = L; out->dist_opt = c->dist_opt;
   out->ranks = (int*)malloc(sizeof(int) * (size_t)(c->nranks > 0 ? c->nranks : 1));
   for (int i = 0; i < c->nranks; ++i) out->ranks[i] = c->ranks[i];
   out->stage = (int*)malloc(sizeof(int) * (size_t)(L > 0 ? L : 1));
@@ -193,11 +201,21 @@ static int tp_block(int64_t len, int tp, int idx, iv_t* out) {
   return 1;
 }
 
-/* view: topology.cpp:16-37 (rank given by its index in the rank list) */
-static int view_at(const tspec_t* t, const cfg_t* c, int idx, box_t* out) {
-  int tp, pp, dp;
-  coord_of(c, idx, &tp, &pp, &dp);
-  if (c->stage[t->layer] != pp) return 0;
+/* Extension (distributed optimizer; no reference counterpart, parity
+ * unpinned): ceil chunk idx of parts over [iv.lo, iv.hi). */
+static int dp_chunk(iv_t iv, int parts, int idx, iv_t* out) {
+  int64_t len = iv.hi - iv.lo, blk = (len + parts - 1) / parts;
+  int64_t lo = iv.lo + (int64_t)idx * blk, hi = lo + blk < iv.hi ? lo + blk : iv.hi;
+  if (lo >= hi) return 0;
+  out->lo = lo; out->hi = hi;
+  return 1;
+}
+
+static int dp_sharded(const tspec_t* t, const cfg_t* c) { return c->dist_opt && t->dp_axis >= 0; }
+
+/* view: topology.cpp:16-37 (rank given by its index in the rank list),
+ * plus the DP chunk of the TP block for distributed-optimizer tensors */
+static int view_coord(const tspec_t* t, const cfg_t* c, int tp, int dp, box_t* out) {
   out->nd = t->nd;
   for (int i = 0; i < t->nd; ++i) { out->b[i].lo = 0; out->b[i].hi = t->shape[i]; }
   if (t->axis >= 0) {
@@ -205,7 +223,19 @@ static int view_at(const tspec_t* t, const cfg_t* c, int idx, box_t* out) {
     if (!tp_block(t->shape[t->axis], c->tp, tp, &b)) return 0;
     out->b[t->axis] = b;
   }
+  if (dp_sharded(t, c)) {
+    iv_t ch;
+    if (!dp_chunk(out->b[t->dp_axis], c->dp, dp, &ch)) return 0;
+    out->b[t->dp_axis] = ch;
+  }
   return 1;
+}
+
+static int view_at(const tspec_t* t, const cfg_t* c, int idx, box_t* out) {
+  int tp, pp, dp;
+  coord_of(c, idx, &tp, &pp, &dp);
+  if (c->stage[t->layer] != pp) return 0;
+  return view_coord(t, c, tp, dp, out);
 }
 
 /* validate_config: parallel_config.cpp:73-123 (first violation only is needed) */
@@ -326,54 +356,67 @@ static int compute_plan(const spec_t* sp, const cfg_t* co, const cfg_t* cn, int 
     if (sharded) {
       for (int i = 0; i < co->tp; ++i) { iv_t b; if (tp_block(alen, co->tp, i, &b)) { btp[nblk] = i; biv[nblk] = b; ++nblk; } }
     } else { btp[0] = -1; biv[0].lo = 0; biv[0].hi = 1; nblk = 1; }
+    /* extension: distributed-optimizer DP chunks (parity unpinned) */
+    int dpo = dp_sharded(t, co), dpn = dp_sharded(t, cn), dax = t->dp_axis;
     for (int dtp = 0; dtp < cn->tp; ++dtp) {
-      box_t vd; vd.nd = t->nd;
-      for (int i = 0; i < t->nd; ++i) { vd.b[i].lo = 0; vd.b[i].hi = t->shape[i]; }
-      if (sharded) { iv_t b; if (!tp_block(alen, cn->tp, dtp, &b)) continue; vd.b[ax] = b; }
+      box_t vdt; vdt.nd = t->nd;
+      for (int i = 0; i < t->nd; ++i) { vdt.b[i].lo = 0; vdt.b[i].hi = t->shape[i]; }
+      if (sharded) { iv_t b; if (!tp_block(alen, cn->tp, dtp, &b)) continue; vdt.b[ax] = b; }
       for (int ddp = 0; ddp < cn->dp; ++ddp) {
+        box_t vd = vdt;
+        if (dpn) { iv_t ch; if (!dp_chunk(vdt.b[dax], cn->dp, ddp, &ch)) continue; vd.b[dax] = ch; }
         int dst = rank_at(cn, dtp, ddp, sn);
-        int have_old = 0, otp = -1; box_t vdo;
+        int have_old = 0, otp = -1, odp = -1; box_t vdo;
         int oidx = cfg_index(co, dst);
         if (oidx >= 0) {
           int a, b, c; coord_of(co, oidx, &a, &b, &c);
           if (b == so) {
-            otp = a; have_old = 1;  /* old_coord present */
-            vdo.nd = t->nd;
-            for (int i = 0; i < t->nd; ++i) { vdo.b[i].lo = 0; vdo.b[i].hi = t->shape[i]; }
-            if (sharded) { iv_t bb; if (tp_block(alen, co->tp, a, &bb)) vdo.b[ax] = bb; else have_old = 2; }
+            otp = a; odp = c;
+            have_old = view_coord(t, co, a, c, &vdo) ? 1 : 2;  /* 2: on the stage, empty view */
           }
         }
         for (int k = 0; k < nblk; ++k) {
-          ++pairs;
-          box_t r = vd;
+          box_t rt = vd;
           if (sharded) {
             iv_t iv = { vd.b[ax].lo > biv[k].lo ? vd.b[ax].lo : biv[k].lo,
                         vd.b[ax].hi < biv[k].hi ? vd.b[ax].hi : biv[k].hi };
-            if (iv.lo >= iv.hi) continue;
-            r.b[ax] = iv;
+            if (iv.lo >= iv.hi) { ++pairs; continue; }
+            rt.b[ax] = iv;
           }
-          int64_t bytes = box_count(&r) * t->bpe;
-          int self = have_old && (!sharded || otp == btp[k]);
-          if (self) {
-            /* a self-holding rank always has a view here (have_old==2 cannot pair) */
-            if (layout_identical(&vdo, &vd, &r)) {
-              keep_t kk = { (uint32_t)ti, t->layer, dst, r, bytes, 0 };
-              push_keep(plan, kk);
-            } else {
-              task_t tt = { (uint32_t)ti, t->layer, dst, dst, r, bytes, 0 };
-              push_task(plan, tt);
+          int nsrc_dp = dpo ? co->dp : 1;
+          for (int s = 0; s < nsrc_dp; ++s) {
+            ++pairs;
+            box_t r = rt;
+            if (dpo) {
+              box_t sv;
+              if (!view_coord(t, co, sharded ? btp[k] : 0, s, &sv)) continue;
+              iv_t iv = { rt.b[dax].lo > sv.b[dax].lo ? rt.b[dax].lo : sv.b[dax].lo,
+                          rt.b[dax].hi < sv.b[dax].hi ? rt.b[dax].hi : sv.b[dax].hi };
+              if (iv.lo >= iv.hi) continue;
+              r.b[dax] = iv;
             }
-            continue;
+            int64_t bytes = box_count(&r) * t->bpe;
+            int self = have_old == 1 && (!sharded || otp == btp[k]) && (!dpo || odp == s);
+            if (self) {
+              if (layout_identical(&vdo, &vd, &r)) {
+                keep_t kk = { (uint32_t)ti, t->layer, dst, r, bytes, 0 };
+                push_keep(plan, kk);
+              } else {
+                task_t tt = { (uint32_t)ti, t->layer, dst, dst, r, bytes, 0 };
+                push_task(plan, tt);
+              }
+              continue;
+            }
+            int sdp = dpo ? s : (balance ? (int)(cursor++ % co->dp) : 0);
+            int src;
+            if (sharded) src = rank_at(co, btp[k], sdp, so);
+            else {
+              src = rank_at(co, 0, sdp, so);
+              for (int x = 1; x < co->tp; ++x) { int q = rank_at(co, x, sdp, so); if (q < src) src = q; }
+            }
+            task_t tt = { (uint32_t)ti, t->layer, src, dst, r, bytes, 0 };
+            push_task(plan, tt);
           }
-          int sdp = balance ? (int)(cursor++ % co->dp) : 0;
-          int src;
-          if (sharded) src = rank_at(co, btp[k], sdp, so);
-          else {
-            src = rank_at(co, 0, sdp, so);
-            for (int x = 1; x < co->tp; ++x) { int q = rank_at(co, x, sdp, so); if (q < src) src = q; }
-          }
-          task_t tt = { (uint32_t)ti, t->layer, src, dst, r, bytes, 0 };
-          push_task(plan, tt);
         }
       }
     }

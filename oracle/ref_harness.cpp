@@ -36,6 +36,8 @@ struct ref_config {
   int32_t tp, pp, dp, nranks;
   const int32_t* ranks;
   const int32_t* layer_stage;
+  int32_t distributed_optimizer;  // product extension: the reference cannot express it
+  int32_t reserved;
 };
 
 struct ref_report {

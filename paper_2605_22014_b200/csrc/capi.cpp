@@ -68,7 +68,8 @@ reshard::ParallelConfig to_config(const rs_config* c, int num_layers) {
   std::vector<int> ranks(c->ranks, c->ranks + c->num_ranks);
   std::vector<int> stages = c->layer_stage ? std::vector<int>(c->layer_stage, c->layer_stage + num_layers)
                                            : reshard::ParallelConfig::default_layer_assignment(num_layers, c->pp);
-  return reshard::ParallelConfig(c->generation_id, c->tp, c->pp, c->dp, std::move(ranks), std::move(stages));
+  return reshard::ParallelConfig(c->generation_id, c->tp, c->pp, c->dp, std::move(ranks), std::move(stages))
+      .with_distributed_optimizer(c->distributed_optimizer != 0);
 }
 
 // Copies s into buf (truncating); *needed is the full size incl. the NUL.

@@ -142,6 +142,9 @@ std::vector<std::string> ModelSpec::validate() const {
         (*t.tp_shard_axis < 0 || *t.tp_shard_axis >= static_cast<int>(t.shape.size())))
       v.push_back("tensor " + t.tensor_id + ": tp_shard_axis out of range");
     if (t.element_bytes < 0) v.push_back("tensor " + t.tensor_id + ": element_bytes < 0");
+    if (t.dp_shard_axis &&
+        (*t.dp_shard_axis < 0 || *t.dp_shard_axis >= static_cast<int>(t.shape.size())))
+      v.push_back("tensor " + t.tensor_id + ": dp_shard_axis out of range");
   }
   return v;
 }
@@ -172,6 +175,11 @@ ModelSpec ModelSpec::parse(const std::string& text) {
       std::string shape, axis, role;
       if (!(ls >> t.tensor_id >> t.layer >> shape >> axis >> role >> t.element_bytes))
         fail("bad tensor record");
+      std::string opt;
+      while (ls >> opt) {  // optional key=value extensions
+        if (opt.rfind("dp=", 0) == 0) t.dp_shard_axis = std::stoi(opt.substr(3));
+        else fail("unknown tensor option " + opt);
+      }
       std::size_t pos = 0;
       while (pos <= shape.size()) {
         std::size_t comma = shape.find(',', pos);
@@ -204,7 +212,9 @@ std::string ModelSpec::to_text() const {
     os << " " << (t.tp_shard_axis ? std::to_string(*t.tp_shard_axis) : std::string("-")) << " "
        << (t.role == TensorRole::kParameter ? "param"
            : t.role == TensorRole::kOptimizerMoment1 ? "m1" : "m2")
-       << " " << element_bytes(t) << "\n";
+       << " " << element_bytes(t);
+    if (t.dp_shard_axis) os << " dp=" << *t.dp_shard_axis;
+    os << "\n";
   }
   return os.str();
 }

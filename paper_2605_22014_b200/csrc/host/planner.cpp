@@ -90,64 +90,113 @@ TransferPlan compute_transfer_plan(const ParallelConfig& c_old, const ParallelCo
       old_blocks.push_back({-1, {0, 1}});
     }
 
+    // Extension (distributed optimizer): DP-sharded views split the TP block
+    // into dp ceil chunks along dp_shard_axis.  Sources that are DP-sharded
+    // are unique per (tp, dp) coordinate, so the destination view is tiled by
+    // (old TP block x old DP chunk); replicated sources keep the reference's
+    // dp0 / round-robin choice.  Without dp sharding this is exactly the
+    // reference loop (same order, same pairs_checked).
+    const bool dp_old_sharded = c_old.distributed_optimizer() && t.dp_shard_axis.has_value();
+    const bool dp_new_sharded = c_new.distributed_optimizer() && t.dp_shard_axis.has_value();
+    const std::size_t daxis = t.dp_shard_axis ? static_cast<std::size_t>(*t.dp_shard_axis) : 0;
+
     const ShardView full = ShardView::full(t.shape);
+    auto old_view = [&](int tp_i, int dp_i) -> std::optional<ShardView> {
+      ShardView v = full;
+      if (sharded) {
+        auto b = tp_block(axis_len, tp_old, tp_i);
+        if (!b) return std::nullopt;
+        v.raw(axis) = *b;
+      }
+      if (dp_old_sharded) {
+        auto c = dp_chunk(v.dim(daxis), dp_old, dp_i);
+        if (!c) return std::nullopt;
+        v.raw(daxis) = *c;
+      }
+      return v;
+    };
     for (int dtp = 0; dtp < tp_new; ++dtp) {
-      ShardView v_dst = full;
+      ShardView v_dst_tp = full;
       if (sharded) {
         auto b = tp_block(axis_len, tp_new, dtp);
         if (!b) continue;
-        v_dst.raw(axis) = *b;
+        v_dst_tp.raw(axis) = *b;
       }
       for (int ddp = 0; ddp < dp_new; ++ddp) {
+        ShardView v_dst = v_dst_tp;
+        if (dp_new_sharded) {
+          auto c = dp_chunk(v_dst.dim(daxis), dp_new, ddp);
+          if (!c) continue;  // short axis: this dp index owns nothing
+          v_dst.raw(daxis) = *c;
+        }
         const int dst = new_rank(dtp, ddp);
 
         // The destination's own old view of this tensor, if it had one.
         bool held_before = false;  // dst sat on the tensor's old stage
-        int held_tp = -1;
+        int held_tp = -1, held_dp = -1;
         std::optional<ShardView> v_held;
         if (c_old.contains(dst)) {
           const RankCoord oc = c_old.coord_of(dst);
           if (oc.pp == s_old) {
             held_before = true;
             held_tp = oc.tp;
-            ShardView vh = full;
-            bool present = true;
-            if (sharded) {
-              if (auto b = tp_block(axis_len, tp_old, oc.tp)) vh.raw(axis) = *b;
-              else present = false;
-            }
-            if (present) v_held = vh;
+            held_dp = oc.dp;
+            v_held = old_view(oc.tp, oc.dp);
           }
         }
 
         for (const OldBlock& ob : old_blocks) {
-          ++pairs;
-          ShardView region = v_dst;
+          ShardView region_tp = v_dst;
           if (sharded) {
-            Interval& iv = region.raw(axis);
+            Interval& iv = region_tp.raw(axis);
             iv.lo = std::max(v_dst.dim(axis).lo, ob.iv.lo);
             iv.hi = std::min(v_dst.dim(axis).hi, ob.iv.hi);
-            if (iv.lo >= iv.hi) continue;
+            if (iv.lo >= iv.hi) {
+              ++pairs;
+              continue;
+            }
           }
-          const std::int64_t bytes = region.element_count() * ebytes;
+          const int dp_sources = dp_old_sharded ? dp_old : 1;
+          for (int sdp = 0; sdp < dp_sources; ++sdp) {
+            ++pairs;
+            ShardView region = region_tp;
+            if (dp_old_sharded) {
+              auto src_view = old_view(sharded ? ob.tp_index : 0, sdp);
+              if (!src_view) continue;
+              Interval& iv = region.raw(daxis);
+              iv.lo = std::max(region_tp.dim(daxis).lo, src_view->dim(daxis).lo);
+              iv.hi = std::min(region_tp.dim(daxis).hi, src_view->dim(daxis).hi);
+              if (iv.lo >= iv.hi) continue;
+            }
+            const std::int64_t bytes = region.element_count() * ebytes;
 
-          if (held_before && (!sharded || held_tp == ob.tp_index)) {
-            if (same_local_layout(*v_held, v_dst, region))
-              plan.carryover_by_layer[t.layer].push_back({ti, t.layer, dst, region, bytes});
-            else
-              plan.tasks_by_layer[t.layer].push_back({ti, t.layer, dst, dst, region, bytes});
-            continue;
-          }
+            const bool self = held_before && (!sharded || held_tp == ob.tp_index) &&
+                              (!dp_old_sharded || held_dp == sdp) && v_held.has_value();
+            if (self) {
+              if (same_local_layout(*v_held, v_dst, region))
+                plan.carryover_by_layer[t.layer].push_back({ti, t.layer, dst, region, bytes});
+              else
+                plan.tasks_by_layer[t.layer].push_back({ti, t.layer, dst, dst, region, bytes});
+              continue;
+            }
 
-          const int src_dp = options.balance_sources ? static_cast<int>(round_robin++ % dp_old) : 0;
-          int src;
-          if (sharded) {
-            src = old_rank(ob.tp_index, src_dp);
-          } else {
-            src = old_rank(0, src_dp);
-            for (int k = 1; k < tp_old; ++k) src = std::min(src, old_rank(k, src_dp));
+            int src;
+            if (dp_old_sharded) {
+              // the dp group's holder (lowest rank id if replicated over TP)
+              src = old_rank(sharded ? ob.tp_index : 0, sdp);
+              if (!sharded)
+                for (int k = 1; k < tp_old; ++k) src = std::min(src, old_rank(k, sdp));
+            } else {
+              const int src_dp = options.balance_sources ? static_cast<int>(round_robin++ % dp_old) : 0;
+              if (sharded) {
+                src = old_rank(ob.tp_index, src_dp);
+              } else {
+                src = old_rank(0, src_dp);
+                for (int k = 1; k < tp_old; ++k) src = std::min(src, old_rank(k, src_dp));
+              }
+            }
+            plan.tasks_by_layer[t.layer].push_back({ti, t.layer, src, dst, region, bytes});
           }
-          plan.tasks_by_layer[t.layer].push_back({ti, t.layer, src, dst, region, bytes});
         }
       }
     }

@@ -40,6 +40,7 @@ class TensorSpec:
     tp_shard_axis: Optional[int]
     role: str = "param"
     bpe: int = 4
+    dp_axis: Optional[int] = None  # extension: distributed-optimizer DP split axis
 
     def element_count(self) -> int:
         n = 1
@@ -63,7 +64,8 @@ class ModelSpec:
         for t in self.tensors:
             axis = "-" if t.tp_shard_axis is None else str(t.tp_shard_axis)
             shape = ",".join(str(d) for d in t.shape)
-            out.append(f"tensor {t.tensor_id} {t.layer} {shape} {axis} {t.role} {t.bpe}")
+            dp = "" if t.dp_axis is None else f" dp={t.dp_axis}"
+            out.append(f"tensor {t.tensor_id} {t.layer} {shape} {axis} {t.role} {t.bpe}{dp}")
         return "\n".join(out) + "\n"
 
     @staticmethod
@@ -79,9 +81,13 @@ class ModelSpec:
                 spec = ModelSpec(tok[1], int(tok[3]), tensors, int(tok[5]))
             elif tok[0] == "tensor":
                 axis = None if tok[4] == "-" else int(tok[4])
+                dp = None
+                for opt in tok[7:]:
+                    if opt.startswith("dp="):
+                        dp = int(opt[3:])
                 tensors.append(TensorSpec(tok[1], int(tok[2]),
                                           [int(x) for x in tok[3].split(",")],
-                                          axis, tok[5], int(tok[6])))
+                                          axis, tok[5], int(tok[6]), dp))
             else:
                 raise ValueError(f"spec parse: unknown record {tok[0]!r}")
         if spec is None:
@@ -106,6 +112,7 @@ class ParallelConfig:
     dp: int
     ranks: List[int]
     layer_stage: Optional[List[int]] = None  # None: default ceil split
+    dist_opt: bool = False  # extension: DP-shard tensors that declare a dp_axis (ZeRO-1)
 
     @property
     def world(self) -> int:
@@ -149,11 +156,23 @@ def group_spec(spec: ModelSpec, bpe: int) -> ModelSpec:
 #   SwiGLU fc1 stored per rank as [gate_r; up_r] -> [2, ffn, h] axis 1.
 # ---------------------------------------------------------------------------
 
+def dp_axis_for(shape: Sequence[int]) -> int:
+    """Distributed-optimizer split axis: the first axis of extent >= 64 (chunks
+    stay large and balanced: embed/head rows, QKV head_dim, fc1 ffn), else 0."""
+    for i, d in enumerate(shape):
+        if d >= 64:
+            return i
+    return 0
+
+
 def _emit(tensors: List[TensorSpec], layer: int, name: str, shape: Sequence[int],
-          axis: Optional[int], state: Sequence[tuple]) -> None:
+          axis: Optional[int], state: Sequence[tuple], zero: bool = False) -> None:
     for suffix, role, bpe in state:
+        # ZeRO-1: fp32 optimizer state (master, m, v) is DP-sharded, bf16
+        # weights stay DP-replicated
+        dp = dp_axis_for(shape) if zero and bpe == 4 and suffix != "param" else None
         tensors.append(TensorSpec(f"L{layer}.{name}.{suffix}", layer, list(shape), axis,
-                                  role, bpe))
+                                  role, bpe, dp))
 
 
 def gpt2_124m(num_layers: int = 12) -> ModelSpec:
@@ -201,26 +220,28 @@ MIXED_STATE = (("param", "param", 2), ("master", "param", 4), ("m1", "m1", 4),
 
 
 def llama(arch: str, num_layers: Optional[int] = None,
-          state: Sequence[tuple] = MIXED_STATE) -> ModelSpec:
+          state: Sequence[tuple] = MIXED_STATE, zero: bool = False) -> ModelSpec:
+    """Llama family spec.  zero=True annotates the fp32 optimizer state for the
+    distributed optimizer (it is DP-sharded under a config with dist_opt)."""
     h, layers, nq, nkv, hd, ffn, vocab = LLAMA[arch]
     L = layers if num_layers is None else num_layers
     ts: List[TensorSpec] = []
     qpg = nq // nkv
     for l in range(L):
         if l == 0:
-            _emit(ts, l, "embed", (vocab, h), 0, state)
-        _emit(ts, l, "input_norm", (h,), None, state)
-        _emit(ts, l, "attn.qkv", (nkv, qpg + 2, hd, h), 0, state)
-        _emit(ts, l, "attn.o", (h, nq * hd), 1, state)
-        _emit(ts, l, "post_norm", (h,), None, state)
-        _emit(ts, l, "mlp.fc1", (2, ffn, h), 1, state)
-        _emit(ts, l, "mlp.fc2", (h, ffn), 1, state)
+            _emit(ts, l, "embed", (vocab, h), 0, state, zero)
+        _emit(ts, l, "input_norm", (h,), None, state, zero)
+        _emit(ts, l, "attn.qkv", (nkv, qpg + 2, hd, h), 0, state, zero)
+        _emit(ts, l, "attn.o", (h, nq * hd), 1, state, zero)
+        _emit(ts, l, "post_norm", (h,), None, state, zero)
+        _emit(ts, l, "mlp.fc1", (2, ffn, h), 1, state, zero)
+        _emit(ts, l, "mlp.fc2", (h, ffn), 1, state, zero)
         if l == L - 1:
-            _emit(ts, l, "final_norm", (h,), None, state)
-            _emit(ts, l, "lm_head", (vocab, h), 0, state)
+            _emit(ts, l, "final_norm", (h,), None, state, zero)
+            _emit(ts, l, "lm_head", (vocab, h), 0, state, zero)
     default = 4 if any(s[2] == 4 for s in state) else state[0][2]
     suffix = "" if num_layers is None else f"-L{L}"
-    return ModelSpec(f"{arch}{suffix}", L, ts, default)
+    return ModelSpec(f"{arch}{suffix}{'-zero' if zero else ''}", L, ts, default)
 
 
 # ---------------------------------------------------------------------------
@@ -235,6 +256,10 @@ def baseline_case(name: str):
         return llama("llama2-7b"), iota_config(1, 4, 2, 1), iota_config(2, 2, 2, 1)
     if name == "c3":  # Llama-3-8B TP8 -> TP4DP2 (reference replicated-DP semantics)
         return llama("llama3-8b"), iota_config(1, 8, 1, 1), iota_config(2, 4, 1, 2)
+    if name == "c3z":  # BASELINE config 3 proper: TP8 -> TP4DP2 with the distributed
+        # optimizer re-partitioning fp32 master/m/v across the 2 DP ranks (extension)
+        c_new = dataclasses.replace(iota_config(2, 4, 1, 2), dist_opt=True)
+        return llama("llama3-8b", zero=True), iota_config(1, 8, 1, 1), c_new
     if name == "c4":  # Llama-2-13B TP2PP4 -> TP4PP2 with uneven 21/19 split
         spec = llama("llama2-13b")
         return spec, iota_config(1, 2, 4, 1), iota_config(2, 4, 2, 1, layer_stage=[0] * 21 + [1] * 19)
@@ -251,9 +276,9 @@ def sliced_case(name: str, num_layers: int):
     if name == "c1":
         spec = gpt2_124m(num_layers)
     else:
-        arch = {"c2": "llama2-7b", "c3": "llama3-8b", "c4": "llama2-13b",
+        arch = {"c2": "llama2-7b", "c3": "llama3-8b", "c3z": "llama3-8b", "c4": "llama2-13b",
                 "c5": "llama2-7b", "c5b": "llama2-7b"}[name]
-        spec = llama(arch, num_layers)
+        spec = llama(arch, num_layers, zero=name == "c3z")
     c_old = dataclasses.replace(c_old, layer_stage=None)
     c_new = dataclasses.replace(c_new, layer_stage=None)
     return spec, c_old, c_new
@@ -326,3 +351,21 @@ def random_case(seed: int):
 def iter_random_cases(n: int, base_seed: int = 20260517) -> Iterable[tuple]:
     for i in range(n):
         yield (base_seed + i,) + random_case(base_seed + i)
+
+
+def random_zero_case(seed: int):
+    """A random pair with distributed-optimizer sharding (extension): some
+    tensors get a dp axis, and either config may enable dist_opt."""
+    spec, c_old, c_new = random_case(seed)
+    rng = random.Random(seed ^ 0x5EED)
+    for t in spec.tensors:
+        if rng.random() < 0.6:
+            t.dp_axis = rng.randrange(len(t.shape))
+    c_old = dataclasses.replace(c_old, dist_opt=rng.random() < 0.6)
+    c_new = dataclasses.replace(c_new, dist_opt=rng.random() < 0.6)
+    return spec, c_old, c_new
+
+
+def iter_random_zero_cases(n: int, base_seed: int = 31337) -> Iterable[tuple]:
+    for i in range(n):
+        yield (base_seed + i,) + random_zero_case(base_seed + i)

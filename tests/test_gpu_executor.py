@@ -218,3 +218,25 @@ def test_full_size_c2_on_one_gpu():
     assert eng.verify_pattern(RS_DST, SEED)[0] == 0
     assert eng.verify_pattern(RS_SRC, SEED)[0] == 0  # sources untouched
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_distributed_optimizer_repartition(mode, oracle_c):
+    """ZeRO-1 re-partition on the device (extension): random pairs vs the C
+    oracle's bytes, plus a 4-layer slice of BASELINE config 3 (Llama-3-8B
+    TP8 -> TP4DP2 with the distributed optimizer) vs the analytic pattern."""
+    for seed, sp, co, cn in specs.iter_random_zero_cases(40):
+        eng = make_engine(sp, co, cn, mode, 1 << 16, lanes_per_link=1)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        rep = R.execute_plan(plan, eng)
+        orep, ostore = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 16)
+        assert rep["ok"] and orep["ok"], seed
+        for (ti, rank), want in ostore.entries.items():
+            assert np.array_equal(eng.read(RS_DST, rank, ti), want), (seed, ti, rank)
+        eng.close()
+    sp, co, cn = specs.sliced_case("c3z", 4)
+    eng = make_engine(sp, co, cn, mode, 256 << 20)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()

@@ -126,3 +126,15 @@ def test_oracle_matches_reference_library(oracle_c, oracle_ref):
         ra.pop("seconds"); rb.pop("seconds")
         assert ra == rb
         assert store_digest(sa) == store_digest(sb)
+
+
+def test_distributed_optimizer_execution_is_analytic(oracle_c):
+    """The restatement's executor on ZeRO plans lands every byte where the
+    extended view function says (the analytic pattern of C_new)."""
+    for seed, sp, co, cn in specs.iter_random_zero_cases(60):
+        text, _ = oracle_c.plan_text(sp, co, cn)
+        rep, store = oracle_c.execute(sp, co, cn, text, 42, 4096)
+        assert rep["ok"], seed
+        want = oracle_c.store_pattern(sp, cn, 42)
+        for k, arr in want.entries.items():
+            assert (store.entries[k] == arr).all(), (seed, k)

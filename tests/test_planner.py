@@ -137,3 +137,27 @@ def test_planner_scalability():
     R.compute_transfer_plan(specs.iota_config(1, 8, 16, 4), specs.iota_config(2, 4, 32, 4), sp, stats=half)
     assert stats.pairs_checked <= 2.2 * half.pairs_checked
     assert plan.summary()["task_count"] > 0
+
+
+def test_distributed_optimizer_extension_matches_oracle(oracle_c):
+    """ZeRO-1 re-partition (BASELINE config 3; no reference counterpart, so the
+    C restatement carries the same extension): plans identical, exact cover."""
+    for seed, sp, co, cn in specs.iter_random_zero_cases(300):
+        for bal in (False, True):
+            plan = R.compute_transfer_plan(co, cn, sp, R.PlanOptions(bal))
+            assert plan.text() == oracle_c.plan_text(sp, co, cn, bal)[0], (seed, bal)
+        assert R.verify_plan(plan, co, cn) == [], seed
+
+
+def test_c3_distributed_optimizer_plan(oracle_c):
+    sp, co, cn = specs.baseline_case("c3z")
+    plan = R.compute_transfer_plan(co, cn, sp)
+    assert plan.text() == oracle_c.plan_text(sp, co, cn)[0]
+    assert R.verify_plan(plan, co, cn) == []
+    # the dp-sharded fp32 state halves what the replicated-DP plan moves
+    rep = R.compute_transfer_plan(*specs.baseline_case("c3")[1:], specs.baseline_case("c3")[0])
+    assert plan.total_bytes() < 0.55 * rep.total_bytes()
+    # each DP rank of the new config holds half of every sharded fp32 tensor
+    ti = next(i for i, t in enumerate(sp.tensors) if t.tensor_id == "L0.embed.master")
+    v0, v1 = R.view(sp, ti, cn, 0), R.view(sp, ti, cn, 4)
+    assert v0 and v1 and v0 != v1
