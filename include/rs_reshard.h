@@ -94,6 +94,8 @@ typedef struct {
 #define RS_COPY_BULK 3     /* cp.async.bulk global->smem->global ring, one issuer per CTA */
 #define RS_COPY_LDG4_CS 4  /* LDG4 with evict-first (st.global.cs) stores */
 #define RS_COPY_LDG8_CS 5  /* LDG8 with evict-first (st.global.cs) stores */
+#define RS_COPY_LDG16 6    /* warp engine, 16 loads in flight per lane */
+#define RS_COPY_CTA8 7     /* CTA-cooperative items (rows dealt to the CTA's warps), 8 loads/lane */
 
 typedef struct {
   int32_t ok;

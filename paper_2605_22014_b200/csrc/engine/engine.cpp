@@ -387,6 +387,8 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_BULK: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 3 : 1;
     case RS_COPY_LDG4_CS: return 4;
     case RS_COPY_LDG8_CS: return 5;
+    case RS_COPY_LDG16: return 6;
+    case RS_COPY_CTA8: return 7;
     default: return 2;
   }
 }
@@ -401,6 +403,12 @@ int Engine::copy_grid(int dev) const {
       return d.sms * per_sm;
     }
     case 3: return d.sms;  // one bulk issuer CTA per SM
+    case 6:
+    case 7: {
+      int per_sm = std::max(1, rs_kernel_max_blocks_per_sm(copy_variant(dev) == 6 ? 5 : 6));
+      per_sm = std::min(per_sm, opts_.blocks_per_sm > 0 ? opts_.blocks_per_sm : 3);
+      return d.sms * per_sm;
+    }
     default: return grid_for(dev, 0);
   }
 }

@@ -170,6 +170,31 @@ __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __rest
   }
 }
 
+// CTA-cooperative variant: an item belongs to a whole CTA and its rows are
+// dealt to the CTA's warps, so the grid keeps 8x fewer item streams open at a
+// time (DRAM page locality) with the same bytes in flight per warp.
+template <int U>
+__global__ void __launch_bounds__(256) rs_copy_cta_kernel(const rs_copy_desc* __restrict__ descs,
+                                                          const uint64_t* __restrict__ item0,
+                                                          uint32_t ndesc, uint64_t item_begin,
+                                                          uint64_t item_end) {
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (uint64_t item = item_begin + blockIdx.x; item < item_end; item += gridDim.x) {
+    const uint32_t di = find_desc(item0, ndesc, item);
+    const rs_copy_desc& D = descs[di];
+    const uint64_t r0 = (item - D.item0) * D.rows_per_item;
+    const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+    const char* src = reinterpret_cast<const char*>(D.src);
+    char* dst = reinterpret_cast<char*>(D.dst);
+    for (uint64_t r = r0 + w; r < r1; r += nw) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      warp_copy_any<true, U>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+    }
+  }
+}
+
 // ------------------------------------------------------ TMA bulk-copy ring
 //
 // One elected thread per CTA streams rows through a ring of kStages shared
@@ -601,6 +626,12 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
     case 5:
       rs_copy_kernel<8, true><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
+    case 6:
+      rs_copy_kernel<16><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 7:
+      rs_copy_cta_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
     case 3: {
       static bool configured = false;
       const int smem = kBulkStages * static_cast<int>(kBulkStageBytes);
@@ -647,6 +678,8 @@ int rs_kernel_max_blocks_per_sm(int which) {
   int n = 0;
   if (which == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel<4>, 256, 0);
   else if (which == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel<8>, 256, 0);
+  else if (which == 5) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_kernel<16>, 256, 0);
+  else if (which == 6) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_cta_kernel<8>, 256, 0);
   else if (which == 4) n = 1;  // bulk ring: one CTA (one issuer, ~200 KB smem) per SM
   else if (which == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_pattern_kernel<false>, 256, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel, 256, 0);
