@@ -1,0 +1,67 @@
+#!/usr/bin/env python3
+"""Every BASELINE configuration on one B200 (all logical ranks on cuda:0).
+
+Full size where source + destination state fit in HBM, else a 16-layer slice
+of the same resize.  DIRECT (copy engine) and STAGED (rings, B = 256 MiB per
+destination rank, automatic lanes).  Prints one JSON line per (config, mode)
+with the 1-GPU HBM roofline fraction (2 x (plan + carryover) bytes over the
+measured copy peak) and the analytic-pattern check of every destination byte.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2605_22014_b200 import reshard as R  # noqa: E402
+from paper_2605_22014_b200 import specs  # noqa: E402
+from paper_2605_22014_b200.native import RS_DST, RS_SRC  # noqa: E402
+
+HBM = 6466.1
+
+
+def run(case, mode, layers=None):
+    sp, co, cn = specs.sliced_case(case, layers) if layers else specs.baseline_case(case)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    s = plan.summary()
+    eng = R.Engine([0], staging_bytes=256 << 20, mode=mode)
+    eng.layout(RS_SRC, sp, co)
+    eng.layout(RS_DST, sp, cn)
+    need = eng.store_bytes(RS_SRC) + eng.store_bytes(RS_DST)
+    free, _ = torch.cuda.mem_get_info()
+    if need + (2 << 30) > free:
+        eng.close()
+        return None
+    eng.alloc(RS_SRC)
+    eng.alloc(RS_DST)
+    eng.fill_pattern(RS_SRC, 42)
+    eng.fill_pattern(RS_DST, 7)
+    eng.prepare(plan)
+    for _ in range(2):
+        eng.run()
+    ms = [eng.run()["device_ms"] for _ in range(5)]
+    bad = eng.verify_pattern(RS_DST, 42)[0]
+    rep = eng.run()
+    eng.close()
+    mean = sum(ms) / len(ms)
+    algo = 2 * (s["total_bytes"] + s["carryover_bytes"])
+    return {"config": case, "slice_layers": layers, "mode": mode, "plan_GB": round(s["total_bytes"] / 1e9, 2),
+            "carry_GB": round(s["carryover_bytes"] / 1e9, 2), "state_GB": round(need / 1e9, 1),
+            "ms": round(mean, 3), "reshard_GBps": round(s["total_bytes"] / mean / 1e6, 1),
+            "hbm_frac": round(algo / (mean / 1e3) / 1e9 / HBM, 4),
+            "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad}
+
+
+def main():
+    for case in ("c1", "c2", "c3", "c3z", "c4", "c5", "c5b"):
+        for mode in ("direct", "staged"):
+            r = run(case, mode)
+            if r is None:
+                r = run(case, mode, 16)
+            print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
