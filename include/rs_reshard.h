@@ -179,11 +179,12 @@ int rs_run(rs_engine* e, rs_exec_report* report);   /* launch + wait */
 int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
 
 /* Host-resident stores: host_src[k] / host_dst[k] follow the (tensor, ascending
- * rank) entry order of the src / dst layout.  Each layer's source shards are
- * copied H2D, resharded on the device, and the destination shards copied D2H,
- * pipelined across layers on separate streams; device memory is bounded by a
- * window of layers.  Requires a prepared plan and laid-out (not allocated)
- * stores. */
+ * rank) entry order of the src / dst layout (rs_store_entries); entries on
+ * other processes' slots are ignored.  Each layer's source shards are copied
+ * H2D, resharded on the device, and the destination shards copied D2H,
+ * pipelined across layers on three streams (DIRECT mode; STAGED copies all in,
+ * runs, copies all out).  The device stores must be allocated or bound;
+ * window_layers is reserved (the current pipeline keeps full device stores). */
 int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
                     void* const* host_dst, int32_t window_layers, rs_exec_report* report);
 
