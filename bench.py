@@ -229,9 +229,23 @@ def ours(args) -> None:
         if world > 1:
             torch.distributed.barrier()
 
+    if args.mode == "xfer":
+        # comparator: our pack/unpack kernels around torch.distributed p2p
+        # (NCCL between GPUs; gloo + host staging when processes share a GPU)
+        from paper_2605_22014_b200 import xfer
+        same = bool(os.environ.get("RS_BENCH_SAME_DEVICE"))
+        group = None if (world == 1 or same) else torch.distributed.new_group(backend="nccl")
+
+        def one_step():
+            info = xfer.run(eng, device, host_staging=same, group=group)
+            return {"ok": True, "device_ms": info["seconds"] * 1e3, "kernel_launches": 1 + 2 * info["rounds"]}
+    else:
+        def one_step():
+            return eng.run()
+
     for _ in range(args.warmup):
         barrier()
-        rep = eng.run()
+        rep = one_step()
         assert rep["ok"], rep
     barrier()
     bad_warm = eng.verify_pattern(RS_DST, SEED)[0]
@@ -244,7 +258,7 @@ def ours(args) -> None:
         for _ in range(args.steps):
             if world > 1:
                 torch.distributed.barrier()  # every GPU starts the handoff together
-            rep = eng.run()
+            rep = one_step()
             dev_ms.append(rep["device_ms"])
             launches += rep["kernel_launches"]
         barrier()
@@ -391,7 +405,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="direct", choices=["direct", "staged"])
+    ap.add_argument("--mode", default="direct", choices=["direct", "staged", "xfer"])
     ap.add_argument("--staging-bytes", type=int, default=1 << 30)
     ap.add_argument("--lanes", type=int, default=0, help="ring lanes per link (0: automatic)")
     ap.add_argument("--strict", type=int, default=0)

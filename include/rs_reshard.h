@@ -42,6 +42,7 @@ extern "C" {
 
 #define RS_MODE_DIRECT 0 /* every byte moved straight src -> dst (peer stores), zero staging */
 #define RS_MODE_STAGED 1 /* remote frames through bounded per-link staging rings */
+#define RS_MODE_XFER 2   /* comparator: kernels pack/unpack, the caller moves bytes (NCCL) */
 
 typedef struct rs_plan rs_plan;
 typedef struct rs_engine rs_engine;
@@ -187,6 +188,17 @@ int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
  * window_layers is reserved (the current pipeline keeps full device stores). */
 int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
                     void* const* host_dst, int32_t window_layers, rs_exec_report* report);
+
+/* RS_MODE_XFER (the NCCL send/recv comparator, one local device): after
+ * rs_prepare, the caller runs step 0 (local copies) once, then for every
+ * round r: step 1 (pack r), moves each tx link's round_bytes[r] from its
+ * buffer to the peer's matching rx link buffer (ncclSend/ncclRecv, links in
+ * index order on both sides), then step 2 (unpack r).  Steps synchronise the
+ * engine stream before returning.  dir: 0 tx, 1 rx. */
+int rs_xfer_info(rs_engine* e, int32_t* rounds, int32_t* ntx, int32_t* nrx);
+int rs_xfer_link(rs_engine* e, int32_t dir, int32_t index, int32_t* peer_slot, int32_t* src_rank,
+                 int32_t* dst_rank, void** buffer, int64_t* buffer_bytes, int64_t* round_bytes);
+int rs_xfer_step(rs_engine* e, int32_t what, int32_t round);
 
 /* Page-locked host memory for host shard stores (full-bandwidth H2D/D2H). */
 int rs_host_alloc(size_t bytes, void** out);

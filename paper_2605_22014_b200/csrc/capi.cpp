@@ -419,3 +419,35 @@ int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int rs_xfer_info(rs_engine* e, int32_t* rounds, int32_t* ntx, int32_t* nrx) {
+  return guarded([&] {
+    *rounds = e->impl.xfer_rounds();
+    *ntx = static_cast<int32_t>(e->impl.xfer_links(0).size());
+    *nrx = static_cast<int32_t>(e->impl.xfer_links(1).size());
+  });
+}
+
+int rs_xfer_link(rs_engine* e, int32_t dir, int32_t index, int32_t* peer_slot, int32_t* src_rank, int32_t* dst_rank,
+                 void** buffer, int64_t* buffer_bytes, int64_t* round_bytes) {
+  return guarded([&] {
+    const auto& links = e->impl.xfer_links(dir ? 1 : 0);
+    if (index < 0 || index >= static_cast<int32_t>(links.size())) throw std::invalid_argument("xfer: link index");
+    const auto& l = links[static_cast<std::size_t>(index)];
+    *peer_slot = l.peer_slot;
+    *src_rank = l.src_rank;
+    *dst_rank = l.dst_rank;
+    *buffer = l.buf;
+    *buffer_bytes = static_cast<int64_t>(l.buf_bytes);
+    if (round_bytes)
+      for (std::size_t r = 0; r < l.round_bytes.size(); ++r) round_bytes[r] = static_cast<int64_t>(l.round_bytes[r]);
+  });
+}
+
+int rs_xfer_step(rs_engine* e, int32_t what, int32_t round) {
+  return guarded([&] { e->impl.xfer_step(what, round); });
+}
+
+}  // extern "C"

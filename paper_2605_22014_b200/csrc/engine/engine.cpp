@@ -156,7 +156,8 @@ std::int64_t Store::total_bytes() const {
 Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.num_devices < 1 || !opts.device_ids) throw DomainError("engine: no devices");
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
-  if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED) throw DomainError("engine: unknown mode");
+  if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
+    throw DomainError("engine: unknown mode");
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
   if (opts_.lanes_per_link < 0) opts_.lanes_per_link = 0;  // 0: automatic (compile_staged)
   nslots_ = opts.world_slots > 0 ? opts.world_slots : opts.num_devices;
@@ -507,6 +508,8 @@ void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
   programs_.resize(devices_.size());
   if (opts_.mode == RS_MODE_DIRECT) {
     compile_direct(plan);
+  } else if (opts_.mode == RS_MODE_XFER) {
+    compile_xfer(plan);
   } else {
     if (comm_.size() != devices_.size()) comm_alloc();
     compile_staged(plan);
@@ -916,6 +919,7 @@ void Engine::upload_programs() {
 
 rs_exec_report Engine::run() {
   if (!prepared_) throw DomainError("engine: prepare a plan first");
+  if (opts_.mode == RS_MODE_XFER) throw DomainError("xfer mode: the caller drives rounds with rs_xfer_step");
   rs_exec_report rep = planned_;
   const auto t0 = std::chrono::steady_clock::now();
   int launches = 0;

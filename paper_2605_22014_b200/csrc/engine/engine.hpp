@@ -147,7 +147,31 @@ class Engine {
   int num_slots() const { return nslots_; }
   int local_of(int slot) const;  // local device index of a slot, -1 if remote
 
+  // RS_MODE_XFER (engine_xfer.cpp): host-driven point-to-point transport --
+  // the comparator path.  Per round, our kernels pack each cross-GPU link's
+  // chunks into a send buffer, the caller moves the buffers (NCCL
+  // send/recv), our kernels unpack the receive buffers.
+  struct XferLink {
+    int peer_slot = 0;
+    int src_rank = 0, dst_rank = 0;
+    char* buf = nullptr;
+    std::uint64_t buf_bytes = 0;
+    std::vector<std::uint64_t> round_bytes;
+  };
+  int xfer_rounds() const { return xfer_rounds_; }
+  const std::vector<XferLink>& xfer_links(int dir) const { return dir ? xfer_rx_ : xfer_tx_; }
+  void xfer_step(int what, int round);  // 0 local copies, 1 pack round, 2 unpack round
+
  private:
+  void compile_xfer(const reshard::TransferPlan& plan);
+  struct XferRound {
+    std::uint64_t pack_begin = 0, pack_end = 0, unpack_begin = 0, unpack_end = 0;  // item ranges
+  };
+  int xfer_rounds_ = 0;
+  std::vector<XferLink> xfer_tx_, xfer_rx_;  // this process's links (single local device)
+  std::vector<XferRound> xfer_round_items_;
+  std::vector<rs_copy_desc> xfer_descs_;
+  DeviceBuffer xfer_buffers_, d_xfer_descs_, d_xfer_item0_;
   std::int64_t pattern_pass(int which, std::uint64_t seed, bool verify, std::int64_t* first_bad);
   void compile_direct(const reshard::TransferPlan& plan);
   void compile_staged(const reshard::TransferPlan& plan);

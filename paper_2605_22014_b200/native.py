@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libreshard_b200.so")
 RS_OK, RS_EDOMAIN, RS_EINTEGRITY, RS_ESYSTEM = 0, 1, 2, 3
 RS_SRC, RS_DST, RS_COMM = 0, 1, 2
 RS_IPC_HANDLE_BYTES = 64
-RS_MODE_DIRECT, RS_MODE_STAGED = 0, 1
+RS_MODE_DIRECT, RS_MODE_STAGED, RS_MODE_XFER = 0, 1, 2
 
 EXPORTS = [
     "rs_last_error", "rs_version", "rs_validate_config", "rs_view", "rs_plan_compute",
@@ -26,7 +26,8 @@ EXPORTS = [
     "rs_store_read",
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
-    "rs_arena_export", "rs_arena_import", "rs_plan_traffic",
+    "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
+    "rs_xfer_step",
 ]
 
 
@@ -146,6 +147,9 @@ def lib() -> C.CDLL:
         L.rs_arena_export.argtypes = [VP, I32, I32, VP, P(I64)]
         L.rs_arena_import.argtypes = [VP, I32, I32, VP, I64]
         L.rs_plan_traffic.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, P(I64)]
+        L.rs_xfer_info.argtypes = [VP, P(I32), P(I32), P(I32)]
+        L.rs_xfer_link.argtypes = [VP, I32, I32, P(I32), P(I32), P(I32), P(VP), P(I64), P(I64)]
+        L.rs_xfer_step.argtypes = [VP, I32, I32]
         _lib = L
     return _lib
 

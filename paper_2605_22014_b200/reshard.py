@@ -161,8 +161,8 @@ class Engine:
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
-        o = N.EngineOptions(len(devs), self._devs, staging_bytes,
-                            N.RS_MODE_DIRECT if mode == "direct" else N.RS_MODE_STAGED,
+        modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
+        o = N.EngineOptions(len(devs), self._devs, staging_bytes, modes[mode],
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
                             blocks_per_sm, copy_kernel, world_slots, first_local_slot)
         h = C.c_void_p()
@@ -246,6 +246,24 @@ class Engine:
 
     def comm_alloc(self):
         N.check(N.lib().rs_comm_alloc(self._h))
+
+    # -- RS_MODE_XFER (comparator transport) -------------------------------
+    def xfer_info(self):
+        r, t, x = C.c_int32(), C.c_int32(), C.c_int32()
+        N.check(N.lib().rs_xfer_info(self._h, C.byref(r), C.byref(t), C.byref(x)))
+        return r.value, t.value, x.value
+
+    def xfer_link(self, direction: int, index: int, rounds: int) -> dict:
+        peer, s, d = C.c_int32(), C.c_int32(), C.c_int32()
+        buf, nb = C.c_void_p(), C.c_int64()
+        rb = (C.c_int64 * max(1, rounds))()
+        N.check(N.lib().rs_xfer_link(self._h, direction, index, C.byref(peer), C.byref(s), C.byref(d),
+                                     C.byref(buf), C.byref(nb), rb))
+        return {"peer_slot": peer.value, "src_rank": s.value, "dst_rank": d.value, "ptr": buf.value or 0,
+                "nbytes": nb.value, "round_bytes": [rb[i] for i in range(rounds)]}
+
+    def xfer_step(self, what: int, rnd: int = 0):
+        N.check(N.lib().rs_xfer_step(self._h, what, rnd))
 
     def export_arena(self, which: int, slot: int):
         """(64-byte CUDA IPC handle, arena bytes) of a local slot's arena."""

@@ -76,6 +76,33 @@ def ipc_reshard(rank, world, mode):
             "launches": rep["kernel_launches"]}
 
 
+def xfer_reshard(rank, world):
+    """GPU: the NCCL-style comparator transport across processes; with gloo
+    (CPU test plumbing) the link buffers are staged through host memory."""
+    import torch
+    from paper_2605_22014_b200 import reshard as R, specs, xfer
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+    dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    sp = specs.llama("llama-mini", 4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
+    so = [i * world // co.world for i in range(co.world)]
+    sn = [(i + 1) * world // cn.world % world for i in range(cn.world)]
+    eng = R.Engine([dev], staging_bytes=64 << 10, mode="xfer", world_slots=world, first_local_slot=rank)
+    eng.layout(RS_SRC, sp, co, so)
+    eng.layout(RS_DST, sp, cn, sn)
+    eng.alloc(RS_SRC)
+    eng.alloc(RS_DST)
+    eng.fill_pattern(RS_SRC, 42)
+    eng.fill_pattern(RS_DST, 7)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng.prepare(plan)
+    info = xfer.run(eng, dev, host_staging=True)
+    bad = eng.verify_pattern(RS_DST, 42)[0]
+    eng.close()
+    return {"ok": True, "mismatches": bad, "rounds": info["rounds"], "bytes_sent": info["bytes_sent"]}
+
+
 def main():
     case, rank, world, port = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=port, RANK=str(rank), WORLD_SIZE=str(world))
@@ -84,6 +111,8 @@ def main():
     try:
         if case == "partition":
             res = plan_partition(rank, world)
+        elif case == "xfer":
+            res = xfer_reshard(rank, world)
         else:
             res = ipc_reshard(rank, world, case)
     finally:
