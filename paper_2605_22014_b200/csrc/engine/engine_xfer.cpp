@@ -65,13 +65,21 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
     std::vector<std::vector<Frame>> batches;
     std::uint64_t fill = 0;
   };
-  // cross-GPU links, counted globally (deterministic on every process)
+  // cross-GPU links, counted globally (deterministic on every process).  A
+  // carryover or local task crosses GPUs too when its rank id is placed on
+  // different slots in the two configurations.
   std::map<int, std::set<int>> inbound;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second) {
       const Entry* se = src.find(t.src_rank, t.tensor_index);
       const Entry* de = dst.find(t.dst_rank, t.tensor_index);
       if (se && de && se->slot != de->slot) inbound[t.dst_rank].insert(t.src_rank);
+    }
+  for (const auto& kv : plan.carryover_by_layer)
+    for (const auto& k : kv.second) {
+      const Entry* se = src.find(k.rank, k.tensor_index);
+      const Entry* de = dst.find(k.rank, k.tensor_index);
+      if (se && de && se->slot != de->slot) inbound[k.rank].insert(k.rank);
     }
   std::map<std::pair<int, int>, Link> links;
 
@@ -83,11 +91,39 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
     std::map<std::pair<int, int>, std::size_t> last_batch_size;
     for (auto& [k, l] : links) last_batch_size[k] = l.batches.empty() ? 0 : l.batches.back().size();
     rs_exec_report delta{};
-    auto local_copy = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb) {
-      if (se->slot != me) return;
-      if (!se->ptr || !de->ptr) throw DomainError("xfer: local shard without device memory");
-      append_copy(p.local, addr_of(se->ptr), se->view, addr_of(de->ptr), de->view, box, eb,
-                  static_cast<std::uint32_t>(layer));
+    // Same GPU: one local copy.  Different GPUs: chunks on link (src, dst).
+    auto route = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb, int src_rank,
+                     int dst_rank) {
+      if (se->slot == de->slot) {
+        if (se->slot != me) return;
+        if (!se->ptr || !de->ptr) throw DomainError("xfer: local shard without device memory");
+        append_copy(p.local, addr_of(se->ptr), se->view, addr_of(de->ptr), de->view, box, eb,
+                    static_cast<std::uint32_t>(layer));
+        return;
+      }
+      const auto key = std::make_pair(src_rank, dst_rank);
+      Link& l = links[key];
+      if (l.slot_bytes == 0) {
+        l.src_rank = src_rank;
+        l.dst_rank = dst_rank;
+        l.sslot = se->slot;
+        l.dslot = de->slot;
+        std::uint64_t sb = static_cast<std::uint64_t>(B) / inbound[dst_rank].size();
+        l.slot_bytes = sb >= 4096 ? sb / 256 * 256 : sb / 16 * 16;
+      }
+      if (static_cast<std::uint64_t>(eb) > l.slot_bytes)
+        throw IntegrityError("staging: link buffer of " + std::to_string(l.slot_bytes) +
+                             " bytes cannot hold one element");
+      for (const auto& c : reshard::chunk_bounds(box, static_cast<std::int64_t>(l.slot_bytes), eb)) {
+        const std::uint64_t nb = static_cast<std::uint64_t>(c.element_count() * eb);
+        std::uint64_t off = (l.fill + 15) / 16 * 16;
+        if (l.batches.empty() || off + nb > l.slot_bytes) {
+          l.batches.emplace_back();
+          off = 0;
+        }
+        l.batches.back().push_back({se, de, c, eb, off});
+        l.fill = off + nb;
+      }
     };
     try {
       if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end())
@@ -98,7 +134,7 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
           if (!se->view.contains(k.bounds)) throw IntegrityError(escapes("slice_local", k.bounds, se->view));
           if (!de->view.contains(k.bounds)) throw IntegrityError(escapes("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
-          local_copy(se, de, k.bounds, eb);
+          route(se, de, k.bounds, eb, k.rank, k.rank);
           delta.carryover_bytes += k.bounds.element_count() * eb;
         }
       if (auto it = plan.tasks_by_layer.find(layer); it != plan.tasks_by_layer.end())
@@ -114,33 +150,7 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
           const std::int64_t n = t.bounds.element_count() * eb;
           if (t.is_local()) delta.local_copy_bytes += n;
           else delta.bytes_moved += n;
-          if (se->slot == de->slot) {  // same GPU: no transport
-            local_copy(se, de, t.bounds, eb);
-            continue;
-          }
-          const auto key = std::make_pair(t.src_rank, t.dst_rank);
-          Link& l = links[key];
-          if (l.slot_bytes == 0) {
-            l.src_rank = t.src_rank;
-            l.dst_rank = t.dst_rank;
-            l.sslot = se->slot;
-            l.dslot = de->slot;
-            std::uint64_t sb = static_cast<std::uint64_t>(B) / inbound[t.dst_rank].size();
-            l.slot_bytes = sb >= 4096 ? sb / 256 * 256 : sb / 16 * 16;
-          }
-          if (static_cast<std::uint64_t>(eb) > l.slot_bytes)
-            throw IntegrityError("staging: link buffer of " + std::to_string(l.slot_bytes) +
-                                 " bytes cannot hold one element");
-          for (const auto& c : reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(l.slot_bytes), eb)) {
-            const std::uint64_t nb = static_cast<std::uint64_t>(c.element_count() * eb);
-            std::uint64_t off = (l.fill + 15) / 16 * 16;
-            if (l.batches.empty() || off + nb > l.slot_bytes) {
-              l.batches.emplace_back();
-              off = 0;
-            }
-            l.batches.back().push_back({se, de, c, eb, off});
-            l.fill = off + nb;
-          }
+          route(se, de, t.bounds, eb, t.src_rank, t.dst_rank);
         }
     } catch (const IntegrityError& e) {
       p.local.resize(mark);
