@@ -97,6 +97,7 @@ typedef struct {
 #define RS_COPY_LDG8_CS 5  /* LDG8 with evict-first (st.global.cs) stores */
 #define RS_COPY_LDG16 6    /* warp engine, 16 loads in flight per lane */
 #define RS_COPY_CTA8 7     /* CTA-cooperative items (rows dealt to the CTA's warps), 8 loads/lane */
+#define RS_COPY_BULK_MW 8  /* TMA bulk rings, 4 independent issuer warps per SM */
 
 typedef struct {
   int32_t ok;

@@ -390,6 +390,7 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_LDG8_CS: return 5;
     case RS_COPY_LDG16: return 6;
     case RS_COPY_CTA8: return 7;
+    case RS_COPY_BULK_MW: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 8 : 2;
     default: return 2;
   }
 }
@@ -403,7 +404,8 @@ int Engine::copy_grid(int dev) const {
       per_sm = std::min(per_sm, opts_.blocks_per_sm > 0 ? opts_.blocks_per_sm : 3);
       return d.sms * per_sm;
     }
-    case 3: return d.sms;  // one bulk issuer CTA per SM
+    case 3:
+    case 8: return d.sms;  // one bulk-ring CTA (1 or 4 issuers) per SM
     case 6:
     case 7: {
       int per_sm = std::max(1, rs_kernel_max_blocks_per_sm(copy_variant(dev) == 6 ? 5 : 6));
@@ -875,6 +877,8 @@ void Engine::upload_programs() {
       const int variant = copy_variant(static_cast<int>(d));
       if (variant == 3) {
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 8 + 1), 32768, 8u << 20);
+      } else if (variant == 8) {  // 4 issuers per SM
+        item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 32 + 1), 32768, 1u << 20);
       } else {
         // 256 KB items (full-size sweep optimum); smaller when the work is small so
         // every warp still gets ~8 items

@@ -335,6 +335,92 @@ __global__ void __launch_bounds__(32, 1) rs_copy_bulk_kernel(const rs_copy_desc*
   bulk_wait_all();
 }
 
+// Multi-issuer TMA bulk ring: every warp's elected lane runs an independent
+// kMwStages-deep ring of kMwStageBytes stages over its own work items (the
+// warp-granular item schedule of rs_copy_kernel), so an SM keeps
+// kMwWarps x kMwLag stages of bulk loads in flight instead of one issuer's.
+constexpr int kMwWarps = 4;
+constexpr int kMwStages = 6;
+constexpr int kMwLag = 4;
+constexpr uint32_t kMwStageBytes = 8192;
+constexpr int kMwPieces = 16;
+
+__global__ void __launch_bounds__(kMwWarps * 32, 1) rs_copy_bulk_mw_kernel(const rs_copy_desc* __restrict__ descs,
+                                                                           const uint64_t* __restrict__ item0,
+                                                                           uint32_t ndesc, uint64_t item_begin,
+                                                                           uint64_t item_end) {
+  extern __shared__ __align__(128) unsigned char ring_all[];
+  __shared__ __align__(8) uint64_t bars_all[kMwWarps][kMwStages];
+  __shared__ BulkPiece pieces_all[kMwWarps][kMwStages][kMwPieces];
+  __shared__ int npieces_all[kMwWarps][kMwStages];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) != 0) return;
+  unsigned char* ring = ring_all + w * kMwStages * kMwStageBytes;
+  uint64_t* bars = bars_all[w];
+  auto& pieces = pieces_all[w];
+  int* npieces = npieces_all[w];
+  for (int s = 0; s < kMwStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  uint64_t chunk = 0, drained = 0;
+  int s = 0, n = 0;
+  uint32_t fill = 0;
+  auto drain_one = [&]() {
+    const int ds = static_cast<int>(drained % kMwStages);
+    mbar_wait(&bars[ds], static_cast<uint32_t>((drained / kMwStages) & 1));
+    for (int k = 0; k < npieces[ds]; ++k) {
+      const BulkPiece& p = pieces[ds][k];
+      bulk_store(reinterpret_cast<void*>(p.dst), ring + ds * kMwStageBytes + p.off, p.bytes);
+    }
+    bulk_commit();
+    ++drained;
+  };
+  auto issue = [&]() {
+    npieces[s] = n;
+    mbar_expect_tx(&bars[s], fill);
+    for (int k = 0; k < n; ++k) {
+      const BulkPiece& p = pieces[s][k];
+      bulk_load(ring + s * kMwStageBytes + p.off, reinterpret_cast<const void*>(p.src), p.bytes, &bars[s]);
+    }
+    ++chunk;
+    if (chunk > static_cast<uint64_t>(kMwLag)) drain_one();
+    s = static_cast<int>(chunk % kMwStages);
+    n = 0;
+    fill = 0;
+    if (chunk >= static_cast<uint64_t>(kMwStages)) bulk_wait_read<kMwStages - kMwLag - 1>();
+  };
+
+  const uint64_t worker = static_cast<uint64_t>(blockIdx.x) * kMwWarps + w;
+  const uint64_t workers = static_cast<uint64_t>(gridDim.x) * kMwWarps;
+  for (uint64_t item = item_begin + worker; item < item_end; item += workers) {
+    const uint32_t di = find_desc(item0, ndesc, item);
+    const rs_copy_desc& D = descs[di];
+    const uint64_t r0 = (item - D.item0) * D.rows_per_item;
+    const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+    for (uint64_t r = r0; r < r1; ++r) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      uint64_t src = D.src + so, dst = D.dst + dof, left = D.row_bytes;
+      while (left) {
+        uint32_t room = kMwStageBytes - fill;
+        if (room == 0 || n == kMwPieces) {
+          issue();
+          room = kMwStageBytes;
+        }
+        const uint32_t b = static_cast<uint32_t>(left < room ? left : static_cast<uint64_t>(room));
+        pieces[s][n++] = BulkPiece{src, dst, fill, b};
+        fill += b;
+        src += b;
+        dst += b;
+        left -= b;
+      }
+    }
+  }
+  if (n) issue();
+  while (drained < chunk) drain_one();
+  bulk_wait_all();
+}
+
 // ------------------------------------------------------------- pattern
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -632,6 +718,17 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
     case 7:
       rs_copy_cta_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
+    case 8: {
+      static bool configured_mw = false;
+      const int smem = kMwWarps * kMwStages * static_cast<int>(kMwStageBytes);
+      if (!configured_mw) {
+        cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_mw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured_mw = true;
+      }
+      rs_copy_bulk_mw_kernel<<<grid, kMwWarps * 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    }
     case 3: {
       static bool configured = false;
       const int smem = kBulkStages * static_cast<int>(kBulkStageBytes);
