@@ -390,7 +390,12 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_LDG8_CS: return 5;
     case RS_COPY_LDG16: return 6;
     case RS_COPY_CTA8: return 7;
-    case RS_COPY_BULK_MW: return programs_[static_cast<std::size_t>(dev)].all_aligned ? 8 : 2;
+    case RS_COPY_BULK_MW:
+    case RS_COPY_BULK_MW + 1:
+    case RS_COPY_BULK_MW + 2:
+    case RS_COPY_BULK_MW + 3:
+    case RS_COPY_BULK_MW + 4:  // issuer-count / ring-shape variants (kernels.cu launch_bulk_mw)
+      return programs_[static_cast<std::size_t>(dev)].all_aligned ? opts_.copy_kernel : 2;
     default: return 2;
   }
 }
@@ -405,7 +410,11 @@ int Engine::copy_grid(int dev) const {
       return d.sms * per_sm;
     }
     case 3:
-    case 8: return d.sms;  // one bulk-ring CTA (1 or 4 issuers) per SM
+    case 8:
+    case 9:
+    case 10:
+    case 11:
+    case 12: return d.sms;  // one bulk-ring CTA (1..16 issuers) per SM
     case 6:
     case 7: {
       int per_sm = std::max(1, rs_kernel_max_blocks_per_sm(copy_variant(dev) == 6 ? 5 : 6));
@@ -877,7 +886,7 @@ void Engine::upload_programs() {
       const int variant = copy_variant(static_cast<int>(d));
       if (variant == 3) {
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 8 + 1), 32768, 8u << 20);
-      } else if (variant == 8) {  // 4 issuers per SM
+      } else if (variant >= 8) {  // 4..16 bulk issuers per SM
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 32 + 1), 32768, 1u << 20);
       } else {
         // 256 KB items (full-size sweep optimum); smaller when the work is small so

@@ -339,12 +339,9 @@ __global__ void __launch_bounds__(32, 1) rs_copy_bulk_kernel(const rs_copy_desc*
 // kMwStages-deep ring of kMwStageBytes stages over its own work items (the
 // warp-granular item schedule of rs_copy_kernel), so an SM keeps
 // kMwWarps x kMwLag stages of bulk loads in flight instead of one issuer's.
-constexpr int kMwWarps = 4;
-constexpr int kMwStages = 6;
-constexpr int kMwLag = 4;
-constexpr uint32_t kMwStageBytes = 8192;
 constexpr int kMwPieces = 16;
 
+template <int kMwWarps, int kMwStages, int kMwLag, uint32_t kMwStageBytes>
 __global__ void __launch_bounds__(kMwWarps * 32, 1) rs_copy_bulk_mw_kernel(const rs_copy_desc* __restrict__ descs,
                                                                            const uint64_t* __restrict__ item0,
                                                                            uint32_t ndesc, uint64_t item_begin,
@@ -694,6 +691,21 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
   }
 }
 
+template <int W, int S, int L, uint32_t T>
+cudaError_t launch_bulk_mw(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc, uint64_t item_begin,
+                           uint64_t item_end, int grid, cudaStream_t stream) {
+  static bool configured = false;
+  const int smem = W * S * static_cast<int>(T);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_mw_kernel<W, S, L, T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  rs_copy_bulk_mw_kernel<W, S, L, T><<<grid, W * 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -718,17 +730,11 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
     case 7:
       rs_copy_cta_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
-    case 8: {
-      static bool configured_mw = false;
-      const int smem = kMwWarps * kMwStages * static_cast<int>(kMwStageBytes);
-      if (!configured_mw) {
-        cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_mw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured_mw = true;
-      }
-      rs_copy_bulk_mw_kernel<<<grid, kMwWarps * 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
-      break;
-    }
+    case 8: return launch_bulk_mw<4, 6, 4, 8192>(descs, item0, ndesc, item_begin, item_end, grid, stream);
+    case 9: return launch_bulk_mw<8, 3, 2, 8192>(descs, item0, ndesc, item_begin, item_end, grid, stream);
+    case 10: return launch_bulk_mw<4, 3, 2, 16384>(descs, item0, ndesc, item_begin, item_end, grid, stream);
+    case 11: return launch_bulk_mw<8, 6, 4, 4096>(descs, item0, ndesc, item_begin, item_end, grid, stream);
+    case 12: return launch_bulk_mw<16, 3, 2, 4096>(descs, item0, ndesc, item_begin, item_end, grid, stream);
     case 3: {
       static bool configured = false;
       const int smem = kBulkStages * static_cast<int>(kBulkStageBytes);

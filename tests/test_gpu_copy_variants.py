@@ -16,7 +16,7 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("copy_kernel", [0, 1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("copy_kernel", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 @pytest.mark.parametrize("case", ["c1", "mini"])
 def test_copy_variant_bitexact(copy_kernel, case):
     if case == "c1":
