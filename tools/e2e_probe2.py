@@ -39,7 +39,15 @@ def main():
     mirror = R.PinnedBuffer(s_end - s_base)
     window = R.PinnedBuffer(4 << 30)
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    cpy = cudart.cudaMemcpyAsync
+    import glob
+    libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib",
+                                  "libcudart.so*")) + ["/usr/local/cuda/lib64/libcudart.so"]
+    rt = ctypes.CDLL(libs[0])
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+
+    def cpy(dst, src, n, kind, stream):
+        rc = rt.cudaMemcpyAsync(dst, src, n, kind, stream)
+        assert rc == 0, rc
 
     def per_entry():
         for (p, _), n in src:
