@@ -1022,6 +1022,54 @@ rs_exec_report Engine::run() {
   return rep;
 }
 
+// Host<->device copies of a set of store entries, merged into runs: entries
+// that are back to back in the device arena AND in the caller's host buffers
+// become one copy (never touching a byte outside the entries), cut into
+// <= 256 MiB pieces.  Thousands of per-shard copies cap concurrent H2D + D2H
+// at 65 GB/s on a B200 host; merged runs reach 96 GB/s
+// (profiles/r1/e2e_probe2.json).
+void Engine::copy_runs(const Store& s, const std::vector<std::size_t>& idx, void* const* host, bool to_device) {
+  struct Piece {
+    char* dev;
+    char* hst;
+    std::size_t n;
+    int local;
+  };
+  std::vector<Piece> ps;
+  ps.reserve(idx.size());
+  for (std::size_t k : idx) {
+    const Entry& e = s.entries[k];
+    if (!e.nbytes) continue;
+    ps.push_back({e.ptr, static_cast<char*>(host[k]), static_cast<std::size_t>(e.nbytes), local_of(e.slot)});
+  }
+  std::sort(ps.begin(), ps.end(), [](const Piece& a, const Piece& b) {
+    return a.local != b.local ? a.local < b.local : a.dev < b.dev;
+  });
+  std::vector<Piece> runs;
+  for (const Piece& p : ps) {
+    if (!runs.empty()) {
+      Piece& r = runs.back();
+      if (r.local == p.local && p.dev == r.dev + r.n && p.hst == r.hst + r.n) {
+        r.n += p.n;
+        continue;
+      }
+    }
+    runs.push_back(p);
+  }
+  constexpr std::size_t kPiece = 256u << 20;
+  for (const Piece& r : runs) {
+    const Device& dv = devices_[static_cast<std::size_t>(r.local)];
+    DeviceGuard g(dv.ordinal);
+    for (std::size_t off = 0; off < r.n; off += kPiece) {
+      const std::size_t n = std::min(kPiece, r.n - off);
+      if (to_device)
+        cuda_check(cudaMemcpyAsync(r.dev + off, r.hst + off, n, cudaMemcpyHostToDevice, dv.h2d), "H2D");
+      else
+        cuda_check(cudaMemcpyAsync(r.hst + off, r.dev + off, n, cudaMemcpyDeviceToHost, dv.d2h), "D2H");
+    }
+  }
+}
+
 rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, int window_layers) {
   (void)window_layers;
   if (!prepared_) throw DomainError("engine: prepare a plan first");
@@ -1087,13 +1135,7 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
     cuda_check(cudaEventRecord(devices_[d].ev_begin, devices_[d].h2d), "event");
   }
   for (std::size_t li = 0; li < nlayers; ++li) {
-    for (std::size_t k : src_by_layer[li]) {
-      const Entry& e = S.entries[k];
-      const Device& dv = devices_[static_cast<std::size_t>(local_of(e.slot))];
-      DeviceGuard g(dv.ordinal);
-      cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
-                                 dv.h2d), "H2D");
-    }
+    copy_runs(S, src_by_layer[li], host_src, true);
     for (std::size_t d = 0; d < ndev; ++d) {
       DeviceGuard g(devices_[d].ordinal);
       cuda_check(cudaEventRecord(ev_in[li * ndev + d], devices_[d].h2d), "event");
@@ -1125,13 +1167,7 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
       for (std::size_t o = 0; o < ndev; ++o)
         cuda_check(cudaStreamWaitEvent(devices_[d].d2h, ev_done[li * ndev + o], 0), "wait");
     }
-    for (std::size_t k : dst_by_layer[li]) {
-      const Entry& e = D.entries[k];
-      const Device& dv = devices_[static_cast<std::size_t>(local_of(e.slot))];
-      DeviceGuard g(dv.ordinal);
-      cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
-                                 dv.d2h), "D2H");
-    }
+    copy_runs(D, dst_by_layer[li], host_dst, false);
   }
   double worst = 0;
   for (auto& dv : devices_) {

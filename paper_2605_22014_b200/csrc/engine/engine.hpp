@@ -173,6 +173,7 @@ class Engine {
   std::vector<rs_copy_desc> xfer_descs_;
   DeviceBuffer xfer_buffers_, d_xfer_descs_, d_xfer_item0_;
   std::int64_t pattern_pass(int which, std::uint64_t seed, bool verify, std::int64_t* first_bad);
+  void copy_runs(const Store& s, const std::vector<std::size_t>& idx, void* const* host, bool to_device);
   void compile_direct(const reshard::TransferPlan& plan);
   void compile_staged(const reshard::TransferPlan& plan);
   void upload_programs();
