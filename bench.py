@@ -338,9 +338,10 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     destination shards D2H, layer-pipelined.  Host RAM cannot hold a second
     94 GB store next to the pinned source (196 GB box), so destination shards
     land in a 4 GiB pinned window that successive shards overwrite; every
-    byte still crosses PCIe.  On this box H2D alone runs 55 GB/s, D2H alone
-    57 GB/s, both together 65.7 GB/s combined (tools/e2e_probe.py): the e2e
-    step is host-transfer bound, the reshard kernel is ~1% of it."""
+    byte still crosses PCIe.  On this box H2D and D2H each run ~55 GB/s and
+    ~96 GB/s combined when the engine merges back-to-back shards into large
+    copies (tools/e2e_probe2.py): the e2e step is host-transfer bound, the
+    reshard kernel is ~1.5 % of it."""
     import torch
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
     from paper_2605_22014_b200.reshard import PinnedBuffer
@@ -395,7 +396,9 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     return {"value": round(total / mean / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(mean, 4),
             "path": "rs_execute_host (C ABI, host shard stores)",
-            "bound": "host<->device transfer (H2D 55, D2H 57, concurrent 65.7 GB/s combined, measured)",
+            "bound": ("host<->device transfer: 188.7 GB per step over PCIe; measured ceiling "
+                      "H2D 55.5 + D2H 55.2 GB/s alone, ~96 GB/s combined concurrent with merged copies "
+                      "(profiles/r1/e2e_probe2.json)"),
             "ok": bool(ok and bad == 0)}
 
 
