@@ -185,8 +185,12 @@ int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
  * other processes' slots are ignored.  Each layer's source shards are copied
  * H2D, resharded on the device, and the destination shards copied D2H,
  * pipelined across layers on three streams (DIRECT mode; STAGED copies all in,
- * runs, copies all out).  The device stores must be allocated or bound;
- * window_layers is reserved (the current pipeline keeps full device stores). */
+ * runs, copies all out).  window_layers == 0: the allocated / bound device
+ * stores are used.  window_layers > 0: only that many layers' shards are
+ * device-resident at a time (layer l in slot l % window_layers; a slot is
+ * refilled after its previous layer's D2H completes) -- device memory is
+ * bounded by window_layers x the largest layer, so states larger than HBM
+ * stream through one GPU (the reference's per-layer bound). */
 int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
                     void* const* host_dst, int32_t window_layers, rs_exec_report* report);
 

@@ -348,6 +348,7 @@ int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src, vo
                     int32_t window_layers, rs_exec_report* report) {
   return guarded([&] {
     if (!e || !plan || !host_src || !host_dst) throw std::invalid_argument("null argument");
+    if (window_layers > 0 && e->impl.window_layers() != window_layers) e->impl.set_window(window_layers);
     if (!e->impl.prepared_for(plan->id)) e->impl.prepare(plan->plan, plan->id);
     *report = e->impl.run_host(host_src, host_dst, window_layers);
     if (!report->ok) throw rsb::IntegrityError(report->error);

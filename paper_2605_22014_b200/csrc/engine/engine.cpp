@@ -267,12 +267,49 @@ void Engine::check_laid_out() const {
 void Engine::alloc(int which) {
   Store& s = stores_[which];
   if (!s.laid_out) throw DomainError("store: layout first");
+  if (window_layers_ > 0) {  // back to full device stores
+    window_.clear();
+    window_layers_ = 0;
+    for (auto& st : stores_)
+      for (auto& e : st.entries) e.ptr = nullptr;
+  }
   s.arenas.clear();
   for (const auto& dv : devices_) s.arenas.emplace_back(dv.ordinal, s.arena_bytes[static_cast<std::size_t>(dv.slot)]);
   for (auto& e : s.entries) {
     const int l = local_of(e.slot);
     if (l >= 0) e.ptr = s.arenas[static_cast<std::size_t>(l)].data() + e.off;
   }
+  prepared_ = false;
+}
+
+void Engine::set_window(int layers) {
+  check_laid_out();
+  if (layers < 1) throw DomainError("window: layers must be >= 1");
+  const int L = stores_[RS_SRC].model.num_layers;
+  window_.clear();
+  for (auto& s : stores_) s.arenas.clear();
+  for (const auto& dv : devices_) {
+    // per model layer: bytes of this slot's source + destination shards
+    std::vector<std::size_t> need(static_cast<std::size_t>(L), 0);
+    for (const auto& s : stores_)
+      for (const auto& e : s.entries)
+        if (e.slot == dv.slot)
+          need[static_cast<std::size_t>(s.model.tensors[e.ti].layer)] += align_up(static_cast<std::size_t>(e.nbytes), kAlign);
+    const std::size_t slot_bytes = need.empty() ? 0 : *std::max_element(need.begin(), need.end());
+    window_.emplace_back(dv.ordinal, slot_bytes * static_cast<std::size_t>(layers));
+    char* base = window_.back().data();
+    std::vector<std::size_t> used(static_cast<std::size_t>(L), 0);  // per layer: its own slot cursor
+    for (auto& s : stores_)
+      for (auto& e : s.entries) {
+        if (e.slot != dv.slot) continue;
+        const int layer = s.model.tensors[e.ti].layer;
+        const auto w = static_cast<std::size_t>(layer % layers);
+        // layer l's source then destination shards fill slot l % layers
+        e.ptr = base + w * slot_bytes + used[static_cast<std::size_t>(layer)];
+        used[static_cast<std::size_t>(layer)] += align_up(static_cast<std::size_t>(e.nbytes), kAlign);
+      }
+  }
+  window_layers_ = layers;
   prepared_ = false;
 }
 
@@ -437,6 +474,7 @@ std::int64_t Engine::verify_pattern(int which, std::uint64_t seed, std::int64_t*
 std::int64_t Engine::pattern_pass(int which, std::uint64_t seed, bool verify, std::int64_t* first_bad) {
   const Store& s = stores_[which];
   if (!s.laid_out) throw DomainError("store: layout first");
+  if (window_layers_ > 0) throw DomainError("pattern fill/verify needs full device stores (this store is windowed)");
   std::int64_t total_bad = 0;
   std::uint64_t first = ~0ull;
   for (int d = 0; d < num_devices(); ++d) {
@@ -1076,6 +1114,8 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
   const auto t0 = std::chrono::steady_clock::now();
   const Store& S = stores_[RS_SRC];
   const Store& D = stores_[RS_DST];
+  if (window_layers_ > 0 && opts_.mode != RS_MODE_DIRECT)
+    throw DomainError("windowed host-store execution runs in RS_MODE_DIRECT");
   if (opts_.mode != RS_MODE_DIRECT) {
     // staged transfers run as one launch: stage everything in, run, stage out
     for (std::size_t k = 0; k < S.entries.size(); ++k) {
@@ -1125,24 +1165,42 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
     auto it = slot_of_layer.find(D.model.tensors[D.entries[k].ti].layer);
     if (it != slot_of_layer.end() && local_of(D.entries[k].slot) >= 0) dst_by_layer[it->second].push_back(k);
   }
-  std::vector<cudaEvent_t> ev_in(nlayers * ndev), ev_done(nlayers * ndev);
+  std::vector<cudaEvent_t> ev_in(nlayers * ndev), ev_done(nlayers * ndev), ev_out(nlayers * ndev);
   for (std::size_t d = 0; d < ndev; ++d) {
     DeviceGuard g(devices_[d].ordinal);
     for (std::size_t li = 0; li < nlayers; ++li) {
       cuda_check(cudaEventCreateWithFlags(&ev_in[li * ndev + d], cudaEventDisableTiming), "event");
       cuda_check(cudaEventCreateWithFlags(&ev_done[li * ndev + d], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&ev_out[li * ndev + d], cudaEventDisableTiming), "event");
     }
     cuda_check(cudaEventRecord(devices_[d].ev_begin, devices_[d].h2d), "event");
   }
+  // Windowed stores: layer l reuses the device slot of the last earlier plan
+  // layer with the same (l % window); its H2D waits for that layer's D2H.
+  std::vector<long> reuse_of(nlayers, -1);
+  if (window_layers_ > 0) {
+    std::map<int, std::size_t> last_in_slot;
+    for (std::size_t li = 0; li < nlayers; ++li) {
+      const int w = programs_[0].layers[li].layer % window_layers_;
+      if (auto it = last_in_slot.find(w); it != last_in_slot.end()) reuse_of[li] = static_cast<long>(it->second);
+      last_in_slot[w] = li;
+    }
+  }
+  // One interleaved enqueue loop (an event must be recorded before a stream
+  // waits on it): H2D(l) -> kernel(l) -> D2H(l), three streams per device.
+  int launches = 0;
   for (std::size_t li = 0; li < nlayers; ++li) {
+    if (reuse_of[li] >= 0)
+      for (std::size_t d = 0; d < ndev; ++d) {
+        DeviceGuard g(devices_[d].ordinal);
+        cuda_check(cudaStreamWaitEvent(devices_[d].h2d, ev_out[static_cast<std::size_t>(reuse_of[li]) * ndev + d], 0),
+                   "wait");
+      }
     copy_runs(S, src_by_layer[li], host_src, true);
     for (std::size_t d = 0; d < ndev; ++d) {
       DeviceGuard g(devices_[d].ordinal);
       cuda_check(cudaEventRecord(ev_in[li * ndev + d], devices_[d].h2d), "event");
     }
-  }
-  int launches = 0;
-  for (std::size_t li = 0; li < nlayers; ++li) {
     for (std::size_t d = 0; d < ndev; ++d) {
       DeviceProgram& p = programs_[d];
       const LayerRange& lr = p.layers[li];
@@ -1160,14 +1218,16 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
       }
       cuda_check(cudaEventRecord(ev_done[li * ndev + d], devices_[d].stream), "event");
     }
-  }
-  for (std::size_t li = 0; li < nlayers; ++li) {
     for (std::size_t d = 0; d < ndev; ++d) {
       DeviceGuard g(devices_[d].ordinal);
       for (std::size_t o = 0; o < ndev; ++o)
         cuda_check(cudaStreamWaitEvent(devices_[d].d2h, ev_done[li * ndev + o], 0), "wait");
     }
     copy_runs(D, dst_by_layer[li], host_dst, false);
+    for (std::size_t d = 0; d < ndev; ++d) {
+      DeviceGuard g(devices_[d].ordinal);
+      cuda_check(cudaEventRecord(ev_out[li * ndev + d], devices_[d].d2h), "event");
+    }
   }
   double worst = 0;
   for (auto& dv : devices_) {
@@ -1181,6 +1241,7 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
   for (std::size_t i = 0; i < ev_in.size(); ++i) {
     cudaEventDestroy(ev_in[i]);
     cudaEventDestroy(ev_done[i]);
+    cudaEventDestroy(ev_out[i]);
   }
   rep.device_ms = worst;
   rep.kernel_launches = launches;

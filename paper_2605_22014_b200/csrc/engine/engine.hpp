@@ -132,6 +132,11 @@ class Engine {
   Store& store(int which) { return stores_[which]; }
 
   void comm_alloc();
+  // Layer window for host-resident stores: only `layers` layers' source and
+  // destination shards live on each local device at a time (slot l % layers),
+  // bounding device memory like the reference's per-layer staging.
+  void set_window(int layers);
+  int window_layers() const { return window_layers_; }
   std::int64_t export_arena(int which, int slot, void* handle) const;
   void import_arena(int which, int slot, const void* handle, std::int64_t bytes);
 
@@ -192,6 +197,8 @@ class Engine {
   std::vector<DeviceProgram> programs_;
   std::vector<DeviceBuffer> comm_;                        // per local device
   std::vector<std::unique_ptr<ImportedArena>> comm_imported_;  // per slot
+  int window_layers_ = 0;
+  std::vector<DeviceBuffer> window_;  // per local device: window_layers_ layer slots
   bool prepared_ = false;
   std::uint64_t prepared_id_ = 0;  // rs_plan identity of the compiled program (0: none)
   std::uint64_t epoch_ = 0;

@@ -294,7 +294,10 @@ class Engine:
         return rep.as_dict()
 
     def execute_host(self, plan: TransferPlan, host_src: Sequence[int], host_dst: Sequence[int],
-                     window_layers: int = 2) -> dict:
+                     window_layers: int = 0) -> dict:
+        """Host shard stores in/out.  window_layers > 0: only that many layers'
+        shards are device-resident at a time (bounded device memory); 0: the
+        allocated / bound device stores are used."""
         rep = N.ExecReport()
         s = (C.c_void_p * len(host_src))(*host_src)
         d = (C.c_void_p * len(host_dst))(*host_dst)
