@@ -87,6 +87,9 @@ typedef struct {
   int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
   int32_t world_slots;      /* device slots in the whole job (0: = num_devices) */
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
+  int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
+  int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
+  int32_t reserved;
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default */

@@ -1026,8 +1026,10 @@ rs_exec_report Engine::run() {
                                     reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                     reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                                     static_cast<std::uint32_t>(p.local.size()), p.local_items, epoch_,
-                                    reinterpret_cast<unsigned int*>(p.d_error.data()), kSpinLimit,
-                                    cap - p.ntx - p.nrx, devices_[d].stream),
+                                    reinterpret_cast<unsigned int*>(p.d_error.data()),
+                                    opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
+                                                         : kSpinLimit,
+                                    opts_.fault_inject, cap - p.ntx - p.nrx, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }

@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
     const uint64_t* __restrict__ local_item0, uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-    unsigned int* error_flag, uint64_t spin_limit) {
+    unsigned int* error_flag, uint64_t spin_limit, int fault_inject) {
   const int lane_id = threadIdx.x & 31;
   const int warp_in_block = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
 
   if (blockIdx.x < ntx + nrx) {
     const bool sender = blockIdx.x < ntx;
+    if (fault_inject == 1 && !sender) return;  // test hook: the receiving peer is gone
     const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
@@ -768,12 +769,13 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-                               unsigned int* error_flag, uint64_t spin_limit, int local_blocks,
-                               cudaStream_t stream) {
+                               unsigned int* error_flag, uint64_t spin_limit, int fault_inject,
+                               int local_blocks, cudaStream_t stream) {
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
   rs_exchange_kernel<<<grid, 256, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,
-                                               local_item0, nlocal, local_items, epoch, error_flag, spin_limit);
+                                               local_item0, nlocal, local_items, epoch, error_flag, spin_limit,
+                                               fault_inject);
   return cudaGetLastError();
 }
 

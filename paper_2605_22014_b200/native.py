@@ -77,7 +77,9 @@ class EngineOptions(C.Structure):
                 ("slots_per_link", C.c_int32), ("lanes_per_link", C.c_int32),
                 ("strict_layers", C.c_int32), ("item_bytes", C.c_int64),
                 ("blocks_per_sm", C.c_int32), ("copy_kernel", C.c_int32),
-                ("world_slots", C.c_int32), ("first_local_slot", C.c_int32)]
+                ("world_slots", C.c_int32), ("first_local_slot", C.c_int32),
+                ("spin_limit", C.c_int64), ("fault_inject", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class ExecReport(C.Structure):

@@ -158,13 +158,15 @@ class Engine:
     def __init__(self, devices: Iterable[int] = (0,), staging_bytes: int = 1 << 30,
                  mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 0,
                  strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
-                 copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0):
+                 copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
+                 spin_limit: int = 0, fault_inject: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
         o = N.EngineOptions(len(devs), self._devs, staging_bytes, modes[mode],
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
-                            blocks_per_sm, copy_kernel, world_slots, first_local_slot)
+                            blocks_per_sm, copy_kernel, world_slots, first_local_slot,
+                            spin_limit, fault_inject, 0)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h

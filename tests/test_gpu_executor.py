@@ -240,3 +240,24 @@ def test_distributed_optimizer_repartition(mode, oracle_c):
     rep = R.execute_plan(plan, eng)
     assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+def test_staged_peer_failure_times_out_not_hangs():
+    """Robustness of the ring transport: when the receiving side of every
+    ring drops out (fault_inject=1), senders exhaust their credits and must
+    give up after spin_limit polls with ok=False and a 'ring wait timed out'
+    report (the reference's failed-layer contract, executor.cpp:210-215)
+    instead of hanging the GPU.  A healthy engine then runs the same plan
+    bit-exact, so a failed handoff leaves the device usable."""
+    sp, co, cn = specs.sliced_case("c1", 2)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng = make_engine(sp, co, cn, "staged", 1 << 16, lanes_per_link=1,
+                      spin_limit=200_000, fault_inject=1)
+    rep = R.execute_plan(plan, eng)
+    assert not rep["ok"]
+    assert "ring wait timed out" in rep["error"]
+    eng.close()
+    eng = make_engine(sp, co, cn, "staged", 1 << 16, lanes_per_link=1)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
