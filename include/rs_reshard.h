@@ -197,6 +197,40 @@ int rs_execute(rs_engine* e, const rs_plan* plan, rs_exec_report* report);
 int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src,
                     void* const* host_dst, int32_t window_layers, rs_exec_report* report);
 
+/* ------------------------------------------------------------ live handoff */
+/* One Switch step of the dual-world handoff, executed for real: the
+ * reference's GenerationMachine::run_switch + atomic_switch
+ * (proj/src/generation.cpp:239-290) price drain + transfer + swap with cost
+ * model constants (transfer_time_s, cost_model.hpp:48-49); here
+ *   drain    = every local reshard stream waits for drain_events[d] (a
+ *              cudaEvent_t the training stream recorded at its iteration
+ *              boundary on local device d; NULL array or entry = nothing
+ *              in flight), device-timed from the call;
+ *   transfer = the prepared plan (rs_prepare / rs_execute), device-timed;
+ *   swap     = RS_SRC and RS_DST exchange roles (the shadow generation's
+ *              store becomes the active one; the old store becomes the next
+ *              handoff's destination) -- the pointer swap of atomic_switch.
+ * A failed transfer leaves the active store untouched and returns
+ * RS_EINTEGRITY with ok = 0 in stats->exec (abort_and_fallback semantics:
+ * generation.cpp:315-340).  Multi-process: every process calls rs_switch;
+ * the caller's barrier after it is the commit point. */
+typedef struct rs_switch_stats {
+  double drain_ms;     /* device time from the call until the last drain event fired */
+  double transfer_ms;  /* device time of the reshard kernels (max over local devices) */
+  double swap_ms;      /* host time of the store swap */
+  double pause_ms;     /* drain + transfer + swap (SwitchStats::pause_s) */
+  int64_t transfer_bytes;  /* plan.total_bytes() (SwitchStats::transfer_bytes) */
+  int32_t swapped;         /* 1 when the stores exchanged roles */
+  int32_t reserved;
+  rs_exec_report exec;
+} rs_switch_stats;
+
+int rs_switch(rs_engine* e, const rs_plan* plan, void* const* drain_events, int32_t swap,
+              rs_switch_stats* stats);
+/* Exchange the RS_SRC and RS_DST stores (layouts, allocations, bindings,
+ * imported peer arenas); the prepared program is dropped. */
+int rs_store_swap(rs_engine* e);
+
 /* RS_MODE_XFER (the NCCL send/recv comparator, one local device): after
  * rs_prepare, the caller runs step 0 (local copies) once, then for every
  * round r: step 1 (pack r), moves each tx link's round_bytes[r] from its

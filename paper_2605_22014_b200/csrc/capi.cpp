@@ -355,6 +355,23 @@ int rs_execute_host(rs_engine* e, const rs_plan* plan, void* const* host_src, vo
   });
 }
 
+int rs_switch(rs_engine* e, const rs_plan* plan, void* const* drain_events, int32_t swap,
+              rs_switch_stats* stats) {
+  return guarded([&] {
+    if (!e || !plan || !stats) throw std::invalid_argument("null argument");
+    if (!e->impl.prepared_for(plan->id)) e->impl.prepare(plan->plan, plan->id);
+    *stats = e->impl.switch_step(drain_events, swap != 0);
+    if (!stats->exec.ok) throw rsb::IntegrityError(stats->exec.error);
+  });
+}
+
+int rs_store_swap(rs_engine* e) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null argument");
+    e->impl.swap_stores();
+  });
+}
+
 }  // extern "C"
 
 extern "C" {

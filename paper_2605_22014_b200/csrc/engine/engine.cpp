@@ -180,6 +180,7 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
     cuda_check(cudaStreamCreateWithFlags(&d.d2h, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&d.ev_begin), "event");
     cuda_check(cudaEventCreate(&d.ev_end), "event");
+    cuda_check(cudaEventCreate(&d.ev_call), "event");
     devices_.push_back(d);
   }
   for (auto& a : devices_)
@@ -194,6 +195,7 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
       else cuda_check(e, "cudaDeviceEnablePeerAccess");
     }
   comm_imported_.resize(static_cast<std::size_t>(nslots_));
+  comm_imported_bytes_.assign(static_cast<std::size_t>(nslots_), 0);
 }
 
 Engine::~Engine() {
@@ -211,6 +213,7 @@ Engine::~Engine() {
     if (d.d2h) cudaStreamDestroy(d.d2h);
     if (d.ev_begin) cudaEventDestroy(d.ev_begin);
     if (d.ev_end) cudaEventDestroy(d.ev_end);
+    if (d.ev_call) cudaEventDestroy(d.ev_call);
   }
 }
 
@@ -395,6 +398,7 @@ void Engine::import_arena(int which, int slot, const void* handle, std::int64_t 
   if (which == RS_COMM) {
     if (static_cast<std::size_t>(bytes) != comm_bytes(slot)) throw DomainError("import: comm arena size mismatch");
     comm_imported_[static_cast<std::size_t>(slot)] = bytes ? std::make_unique<ImportedArena>(dev, h) : nullptr;
+    comm_imported_bytes_[static_cast<std::size_t>(slot)] = static_cast<std::size_t>(bytes);
   } else {
     Store& s = stores_[which];
     if (!s.laid_out) throw DomainError("import: lay out the store first");
@@ -548,6 +552,7 @@ void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
 
   planned_ = rs_exec_report{};
   planned_.failed_layer = -1;
+  planned_total_bytes_ = plan.total_bytes();
   std::set<int> layers;
   for (const auto& kv : plan.tasks_by_layer) layers.insert(kv.first);
   for (const auto& kv : plan.carryover_by_layer) layers.insert(kv.first);
@@ -560,7 +565,23 @@ void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
   } else if (opts_.mode == RS_MODE_XFER) {
     compile_xfer(plan);
   } else {
-    if (comm_.size() != devices_.size()) comm_alloc();
+    // The ring area is B per destination rank of the slot, so it follows the
+    // dst layout: a live-handoff chain changes it every generation.
+    bool stale = comm_.size() != devices_.size();
+    for (std::size_t d = 0; !stale && d < devices_.size(); ++d)
+      stale = comm_[d].size() != comm_bytes(devices_[d].slot);
+    for (int s = 0; s < nslots_; ++s)
+      if (local_of(s) < 0 && comm_imported_[static_cast<std::size_t>(s)] &&
+          comm_imported_bytes_[static_cast<std::size_t>(s)] != comm_bytes(s))
+        throw DomainError("staged: peer comm arena of slot " + std::to_string(s) +
+                          " was sized for another dst layout; re-run rs_comm_alloc on every process and "
+                          "re-exchange the RS_COMM handles");
+    if (stale) {
+      if (nslots_ > num_devices() && !comm_.empty())
+        throw DomainError("staged: comm arena was sized for another dst layout; re-run rs_comm_alloc on every "
+                          "process and re-exchange the RS_COMM handles");
+      comm_alloc();
+    }
     compile_staged(plan);
   }
   upload_programs();
@@ -1060,6 +1081,47 @@ rs_exec_report Engine::run() {
   rep.kernel_launches = launches;
   rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return rep;
+}
+
+// ------------------------------------------------------------ live handoff
+
+// Drain -> transfer -> swap, the Switch phase of generation.cpp:239-290 with
+// each piece executed instead of priced.  The drain is a stream-order wait on
+// the caller's iteration-boundary events, so no host thread blocks on the
+// training stream and the transfer starts the instant the last one fires.
+rs_switch_stats Engine::switch_step(void* const* drain_events, bool swap) {
+  if (!prepared_) throw DomainError("switch: prepare the handoff plan first (Prepare phase)");
+  rs_switch_stats st{};
+  for (std::size_t d = 0; d < devices_.size(); ++d) {
+    DeviceGuard g(devices_[d].ordinal);
+    cuda_check(cudaEventRecord(devices_[d].ev_call, devices_[d].stream), "event");
+    if (drain_events && drain_events[d])
+      cuda_check(cudaStreamWaitEvent(devices_[d].stream, static_cast<cudaEvent_t>(drain_events[d]), 0),
+                 "drain wait");
+  }
+  st.exec = run();  // records ev_begin behind the drain waits
+  for (auto& dv : devices_) {
+    DeviceGuard g(dv.ordinal);
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, dv.ev_call, dv.ev_begin), "elapsed");
+    st.drain_ms = std::max(st.drain_ms, static_cast<double>(ms));
+  }
+  st.transfer_ms = st.exec.device_ms;
+  st.transfer_bytes = planned_total_bytes_;
+  if (st.exec.ok && swap) {
+    const auto t0 = std::chrono::steady_clock::now();
+    swap_stores();
+    st.swap_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    st.swapped = 1;
+  }
+  st.pause_ms = st.drain_ms + st.transfer_ms + st.swap_ms;
+  return st;
+}
+
+void Engine::swap_stores() {
+  std::swap(stores_[RS_SRC], stores_[RS_DST]);
+  prepared_ = false;  // compiled descriptors point into the old roles
+  prepared_id_ = 0;
 }
 
 // Host<->device copies of a set of store entries, merged into runs: entries

@@ -116,6 +116,7 @@ struct Device {
   cudaStream_t stream = nullptr;              // reshard kernels
   cudaStream_t h2d = nullptr, d2h = nullptr;  // host-store copies (rs_execute_host)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_call = nullptr;  // rs_switch: the moment the switch was requested
 };
 
 class Engine {
@@ -147,6 +148,9 @@ class Engine {
   bool prepared_for(std::uint64_t plan_id) const { return prepared_ && plan_id && plan_id == prepared_id_; }
   rs_exec_report run();
   rs_exec_report run_host(void* const* host_src, void* const* host_dst, int window_layers);
+  // Live-handoff Switch step (rs_switch): drain -> transfer -> swap.
+  rs_switch_stats switch_step(void* const* drain_events, bool swap);
+  void swap_stores();
 
   int num_devices() const { return static_cast<int>(devices_.size()); }
   int num_slots() const { return nslots_; }
@@ -197,12 +201,14 @@ class Engine {
   std::vector<DeviceProgram> programs_;
   std::vector<DeviceBuffer> comm_;                        // per local device
   std::vector<std::unique_ptr<ImportedArena>> comm_imported_;  // per slot
+  std::vector<std::size_t> comm_imported_bytes_;               // per slot
   int window_layers_ = 0;
   std::vector<DeviceBuffer> window_;  // per local device: window_layers_ layer slots
   bool prepared_ = false;
   std::uint64_t prepared_id_ = 0;  // rs_plan identity of the compiled program (0: none)
   std::uint64_t epoch_ = 0;
   rs_exec_report planned_{};  // compile-time report fields (reference semantics)
+  std::int64_t planned_total_bytes_ = 0;
   std::vector<int> plan_layers_;
 };
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
     "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
-    "rs_xfer_step",
+    "rs_xfer_step", "rs_switch", "rs_store_swap",
 ]
 
 
@@ -102,6 +102,19 @@ class ExecReport(C.Structure):
                 "error": self.error.decode()}
 
 
+class SwitchStats(C.Structure):
+    _fields_ = [("drain_ms", C.c_double), ("transfer_ms", C.c_double),
+                ("swap_ms", C.c_double), ("pause_ms", C.c_double),
+                ("transfer_bytes", C.c_int64), ("swapped", C.c_int32),
+                ("reserved", C.c_int32), ("exec", ExecReport)]
+
+    def as_dict(self) -> dict:
+        return {"drain_ms": float(self.drain_ms), "transfer_ms": float(self.transfer_ms),
+                "swap_ms": float(self.swap_ms), "pause_ms": float(self.pause_ms),
+                "transfer_bytes": int(self.transfer_bytes), "swapped": bool(self.swapped),
+                "exec": self.exec.as_dict()}
+
+
 _lib = None
 
 
@@ -152,6 +165,8 @@ def lib() -> C.CDLL:
         L.rs_xfer_info.argtypes = [VP, P(I32), P(I32), P(I32)]
         L.rs_xfer_link.argtypes = [VP, I32, I32, P(I32), P(I32), P(I32), P(VP), P(I64), P(I64)]
         L.rs_xfer_step.argtypes = [VP, I32, I32]
+        L.rs_switch.argtypes = [VP, VP, P(VP), I32, P(SwitchStats)]
+        L.rs_store_swap.argtypes = [VP]
         _lib = L
     return _lib
 

@@ -173,6 +173,7 @@ class Engine:
         self.num_devices = len(devs)
         self.world_slots = world_slots or len(devs)
         self.first_local_slot = first_local_slot
+        self.mode = mode
         self.models = {}
         self.configs = {}
 
@@ -307,6 +308,34 @@ class Engine:
         if rc not in (N.RS_OK, N.RS_EINTEGRITY):
             N.check(rc)
         return rep.as_dict()
+
+    def switch(self, plan: TransferPlan, drain_events: Optional[Sequence[int]] = None,
+               swap: bool = True) -> dict:
+        """Switch step of a live handoff (rs_switch): wait for the training
+        streams' iteration-boundary events (cudaEvent_t handles, one per local
+        device, None entries allowed), run the prepared plan, then swap the
+        stores so RS_SRC is the new generation.  Returns SwitchStats as a
+        dict; a failed transfer comes back with exec.ok False and no swap."""
+        st = N.SwitchStats()
+        ev = None
+        if drain_events is not None:
+            ev = (C.c_void_p * len(drain_events))(*[e or None for e in drain_events])
+        rc = N.lib().rs_switch(self._h, plan.handle, ev, int(swap), C.byref(st))
+        if rc not in (N.RS_OK, N.RS_EINTEGRITY):
+            N.check(rc)
+        out = st.as_dict()
+        if out["swapped"]:
+            self._swap_py()
+        return out
+
+    def swap_stores(self):
+        N.check(N.lib().rs_store_swap(self._h))
+        self._swap_py()
+
+    def _swap_py(self):
+        m, c = self.models, self.configs
+        self.models = {k ^ 1: v for k, v in m.items() if k in (N.RS_SRC, N.RS_DST)}
+        self.configs = {k ^ 1: v for k, v in c.items() if k in (N.RS_SRC, N.RS_DST)}
 
 
 def plan_traffic(plan: TransferPlan, c_old: ParallelConfig, slot_old: Sequence[int],

@@ -103,6 +103,41 @@ def xfer_reshard(rank, world):
     return {"ok": True, "mismatches": bad, "rounds": info["rounds"], "bytes_sent": info["bytes_sent"]}
 
 
+def handoff_chain(rank, world, mode):
+    """GPU: LiveHandoff across processes -- shadow arenas exchanged in
+    Prepare, the commit barrier after every switch, a chain of generations."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_22014_b200 import reshard as R, specs
+    from paper_2605_22014_b200.handoff import LiveHandoff
+    from paper_2605_22014_b200.native import RS_SRC
+    dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    sp = specs.llama("llama-mini", 4)
+    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
+                   first_local_slot=rank)
+
+    def placement(cfg):  # alternate between blocked and shifted placements
+        return [((i * world // cfg.world) + cfg.gen) % world for i in range(cfg.world)]
+
+    h = LiveHandoff(eng, sp, specs.iota_config(1, 4, 2, 1), placement, group=dist.group.WORLD)
+    eng.fill_pattern(RS_SRC, 42)
+    dist.barrier()
+    pauses, bad = [], 0
+    for gen, shape in enumerate([(2, 2, 2), (2, 1, 2), (4, 2, 1)], start=2):
+        h.trigger_resize(specs.iota_config(gen, *shape))
+        h.prepare()
+        st = h.switch()
+        pauses.append(st.pause_s)
+        dist.barrier()
+        bad += eng.verify_pattern(RS_SRC, 42)[0]
+    out = {"ok": h.active.gen == 4 and h.phase.value == "Stable", "mismatches": bad,
+           "pauses": pauses, "launches": 0}
+    dist.barrier()
+    eng.close()
+    return out
+
+
 def main():
     case, rank, world, port = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=port, RANK=str(rank), WORLD_SIZE=str(world))
@@ -113,6 +148,8 @@ def main():
             res = plan_partition(rank, world)
         elif case == "xfer":
             res = xfer_reshard(rank, world)
+        elif case.startswith("handoff-"):
+            res = handoff_chain(rank, world, case.split("-", 1)[1])
         else:
             res = ipc_reshard(rank, world, case)
     finally:

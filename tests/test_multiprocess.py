@@ -66,3 +66,19 @@ def test_two_processes_one_gpu_ipc(mode):
     for o in outs:
         assert o["result"]["ok"], o
         assert o["result"]["mismatches"] == 0, o
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_two_processes_live_handoff_chain(mode):
+    """Runtime hook across processes: three generations through LiveHandoff
+    (shadow arenas exchanged in Prepare, commit barrier after each switch);
+    every active store verifies against the analytic pattern."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    outs = launch("handoff-" + mode, timeout=900)
+    for o in outs:
+        assert o["result"]["ok"], o
+        assert o["result"]["mismatches"] == 0, o
+        assert len(o["result"]["pauses"]) == 3
