@@ -226,4 +226,33 @@ std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelCon
 std::vector<ShardView> chunk_bounds(const ShardView& bounds, std::int64_t max_bytes,
                                     std::int64_t bytes_per_element);
 
+// Placement-aware destination rank ordering (extension):
+// the rank list of c_new (same tp/pp/dp/layer split), drawn from `candidates`
+// (one rank per GPU), that minimises the per-GPU roofline
+//   max_g max(max(out_g, in_g) / nvlink, (out_g + in_g + 2 local_g + 2 carry_g) / hbm)
+// of the plan c_old -> c_new (ties: fewer remote bytes).  Exhaustive when the
+// number of assignments is <= exhaustive_limit, else local search from c_new's
+// own list.  Never returns a list scoring worse than c_new's own (when that
+// list is drawn from the candidates).
+struct PlacementOptions {
+  double nvlink_gbs = 900.0;   // per direction, per GPU
+  double hbm_gbs = 6552.0;     // copy bandwidth (MEASURED_PEAKS.json)
+  std::int64_t exhaustive_limit = 2000000;
+  bool balance_sources = false;
+};
+
+struct PlacementResult {
+  std::vector<int> ranks;  // the chosen rank list for c_new
+  double roofline_s = 0, given_roofline_s = 0;
+  std::int64_t remote_bytes = 0, local_bytes = 0, carryover_bytes = 0, max_link_bytes = 0;
+  std::int64_t given_remote_bytes = 0, given_local_bytes = 0, given_carryover_bytes = 0,
+               given_max_link_bytes = 0;
+  std::int64_t evaluated = 0;
+  bool exhaustive = false;
+};
+
+PlacementResult choose_placement(const ParallelConfig& c_old, const ParallelConfig& c_new,
+                                 const ModelSpec& model, const std::vector<int>& candidates,
+                                 const PlacementOptions& options = {});
+
 }  // namespace reshard

@@ -12,6 +12,7 @@
  *   rs_plan_write      write_plan              proj/include/reshard/transfer_plan.hpp:81
  *   rs_plan_read       read_plan               proj/include/reshard/transfer_plan.hpp:82
  *   rs_plan_summary    plan_cost_summary       proj/include/reshard/transfer_plan.hpp:77
+ *   rs_plan_placement  (extension) rank-list search over compute_transfer_plan
  *   rs_validate_config validate_config         proj/include/reshard/parallel_config.hpp:73-74
  *   rs_view            view / tp_block         proj/include/reshard/topology.hpp:20-25
  *   rs_chunk_bounds    chunk_bounds            proj/include/reshard/executor.hpp:43-44
@@ -89,6 +90,10 @@ typedef struct {
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
   int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
+  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 128, -1: no cap,
+                               slot = B / (inbound links x lanes x K)); B stays the upper bound */
+  int32_t ring_discard;     /* STAGED: 0/1 receivers drop drained slot lines from L2
+                               (discard.global.L2, no write-back), 2: keep them */
   int32_t reserved;
 } rs_engine_options;
 
@@ -173,6 +178,33 @@ int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handl
  * of remote task bytes, local task bytes, carryover bytes, out[4*slot + k]. */
 int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old,
                     const rs_config* c_new, const int32_t* slot_new, int32_t nslots, int64_t* out);
+
+/* Placement-aware destination rank ordering (extension):
+ * fills ranks_out[c_new->num_ranks] with the rank list for c_new's shape,
+ * drawn from candidates[ncand] (one rank per GPU), that minimises the per-GPU
+ * NVLink/HBM roofline of the plan c_old -> c_new; the planner's self-held
+ * regions (proj/src/planner.cpp:139-152) make the list decide how many bytes
+ * cross links.  out reports the chosen and the given (c_new->ranks) lists. */
+typedef struct {
+  double nvlink_gbs;        /* 0: 900 (per direction per GPU) */
+  double hbm_gbs;           /* 0: 6552 (measured copy peak) */
+  int64_t exhaustive_limit; /* 0: 2,000,000 assignments */
+  int32_t balance_sources;
+  int32_t reserved;
+} rs_placement_options;
+
+typedef struct {
+  double roofline_ms, given_roofline_ms;
+  int64_t remote_bytes, local_bytes, carryover_bytes, max_link_bytes;
+  int64_t given_remote_bytes, given_local_bytes, given_carryover_bytes, given_max_link_bytes;
+  int64_t evaluated;
+  int32_t exhaustive;
+  int32_t reserved;
+} rs_placement_result;
+
+int rs_plan_placement(const char* model_spec, const rs_config* c_old, const rs_config* c_new,
+                      const int32_t* candidates, int32_t ncand, const rs_placement_options* opts,
+                      int32_t* ranks_out, rs_placement_result* out);
 
 int rs_fill_pattern(rs_engine* e, int32_t which, uint64_t seed);
 int rs_verify_pattern(rs_engine* e, int32_t which, uint64_t seed, int64_t* mismatches,

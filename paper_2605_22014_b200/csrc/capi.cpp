@@ -436,6 +436,40 @@ int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* 
   });
 }
 
+int rs_plan_placement(const char* model_spec, const rs_config* c_old, const rs_config* c_new,
+                      const int32_t* candidates, int32_t ncand, const rs_placement_options* opts,
+                      int32_t* ranks_out, rs_placement_result* out) {
+  return guarded([&] {
+    if (!candidates || ncand < 1 || !ranks_out || !out) throw std::invalid_argument("bad argument");
+    auto m = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    const auto co = to_config(c_old, m.num_layers), cn = to_config(c_new, m.num_layers);
+    reshard::PlacementOptions po;
+    if (opts) {
+      if (opts->nvlink_gbs < 0 || opts->hbm_gbs < 0 || opts->exhaustive_limit < 0)
+        throw std::invalid_argument("placement: negative option");
+      if (opts->nvlink_gbs > 0) po.nvlink_gbs = opts->nvlink_gbs;
+      if (opts->hbm_gbs > 0) po.hbm_gbs = opts->hbm_gbs;
+      if (opts->exhaustive_limit > 0) po.exhaustive_limit = opts->exhaustive_limit;
+      po.balance_sources = opts->balance_sources != 0;
+    }
+    const auto r = reshard::choose_placement(co, cn, m, std::vector<int>(candidates, candidates + ncand), po);
+    std::copy(r.ranks.begin(), r.ranks.end(), ranks_out);
+    *out = rs_placement_result{};
+    out->roofline_ms = r.roofline_s * 1e3;
+    out->given_roofline_ms = r.given_roofline_s * 1e3;
+    out->remote_bytes = r.remote_bytes;
+    out->local_bytes = r.local_bytes;
+    out->carryover_bytes = r.carryover_bytes;
+    out->max_link_bytes = r.max_link_bytes;
+    out->given_remote_bytes = r.given_remote_bytes;
+    out->given_local_bytes = r.given_local_bytes;
+    out->given_carryover_bytes = r.given_carryover_bytes;
+    out->given_max_link_bytes = r.given_max_link_bytes;
+    out->evaluated = r.evaluated;
+    out->exhaustive = r.exhaustive;
+  });
+}
+
 }  // extern "C"
 
 extern "C" {

@@ -70,5 +70,8 @@ typedef struct {
 typedef struct {
   uint32_t pack0, npack;     // frame descriptors packing into the slot (sender side)
   uint32_t unpack0, nunpack; // frame descriptors unpacking out of the slot (receiver side)
+  uint32_t pack_items;       // work items over the pack frames (frame item0 is batch-relative)
+  uint32_t unpack_items;     // work items over the unpack frames
   uint64_t bytes;            // payload bytes in this batch
+  uint64_t extent;           // slot bytes in use (last frame end), for the L2 discard
 } rs_batch_desc;

@@ -41,6 +41,7 @@ namespace {
 
 constexpr std::size_t kAlign = 256;
 constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
+constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
 constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 std::uint64_t key(int rank, std::uint32_t ti) {
@@ -718,9 +719,17 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       for (int r : ranks) region_of[r] = (i++) * static_cast<std::size_t>(B);
     }
   }
-  std::map<int, std::uint64_t> slot_bytes_of;  // ring slot size per dst rank
+  // Ring slot size per dst rank: B split over its inbound lanes, capped so the
+  // rings stay L2-resident (the receiver unpacks a slot microseconds after
+  // it was packed and then discards its lines): B is the budget, not the
+  // target footprint.
+  const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
+                                 : opts_.ring_slot_kib == 0 ? kRingSlotDefault
+                                                            : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
+  std::map<int, std::uint64_t> slot_bytes_of;
   for (const auto& [d, srcs] : inbound) {
     std::uint64_t sb = static_cast<std::uint64_t>(B) / (srcs.size() * static_cast<std::uint64_t>(P * K));
+    sb = std::min(sb, slot_cap);
     slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
   }
 
@@ -893,6 +902,9 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     L.slots = static_cast<std::uint32_t>(K);
     L.batch0 = static_cast<std::uint32_t>(batches.size());
     L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
+    // work items inside a batch: ~32 per slot so all 8 warps of the lane's
+    // CTA share even a small (L2-resident) slot
+    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / 32, 4096, 65536);
     for (std::size_t b = 0; b < lb.batches.size(); ++b) {
       const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
       rs_batch_desc Bd{};
@@ -901,19 +913,24 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         for (const auto& f : lb.batches[b])
           append_copy(frames, addr(f.se->ptr), f.se->view, slot_addr + f.off, f.region, f.region, f.eb,
                       static_cast<std::uint32_t>(f.layer));
-      for (const auto& f : lb.batches[b]) Bd.bytes += static_cast<std::uint64_t>(f.region.element_count() * f.eb);
+      for (const auto& f : lb.batches[b]) {
+        const std::uint64_t n = static_cast<std::uint64_t>(f.region.element_count() * f.eb);
+        Bd.bytes += n;
+        Bd.extent = std::max(Bd.extent, f.off + n);
+      }
       Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
+      Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
       Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
       if (rx_local)
         for (const auto& f : lb.batches[b])
           append_copy(frames, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
                       f.eb, static_cast<std::uint32_t>(f.layer));
       Bd.nunpack = static_cast<std::uint32_t>(frames.size()) - Bd.unpack0;
+      Bd.unpack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.unpack0, 0, frame_item));
       batches.push_back(Bd);
     }
     all_lanes.push_back(L);
   }
-  assign_items(frames, 0, 0, 1ull << 16);  // per-warp slices inside each frame
   for (std::size_t d = 0; d < devices_.size(); ++d) {
     DeviceProgram& p = programs_[d];
     const int slot = devices_[d].slot;
@@ -1050,7 +1067,8 @@ rs_exec_report Engine::run() {
                                     reinterpret_cast<unsigned int*>(p.d_error.data()),
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
-                                    opts_.fault_inject, cap - p.ntx - p.nrx, devices_[d].stream),
+                                    (opts_.fault_inject == 1 ? 1 : 0) | (opts_.ring_discard != 2 ? 2 : 0),
+                                    cap - p.ntx - p.nrx, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }

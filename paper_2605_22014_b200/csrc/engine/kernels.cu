@@ -617,6 +617,29 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
   return true;
 }
 
+// Drop one 128 B line from L2 without writing it back (its value becomes
+// undefined).  A drained ring slot is rewritten by the next batch, so its
+// dirty lines never need to reach HBM: with slots small enough to stay
+// L2-resident the staging traffic never leaves the L2.
+__device__ __forceinline__ void discard_l2_line(uint64_t a) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
+
+// Frame of batch-relative item `it`: largest f with frames[f].item0 <= it.
+__device__ __forceinline__ uint32_t find_frame(const rs_copy_desc* __restrict__ frames, uint32_t n, uint32_t it) {
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (frames[mid].item0 <= it) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// flags of rs_launch_exchange
+constexpr int kExFaultRx = 1;   // test hook: ring receivers drop out (peer failure)
+constexpr int kExDiscard = 2;   // receivers discard drained slot lines from L2
+
 // Block roles: blocks [0, ntx) send lanes_tx[b], [ntx, ntx + nrx) receive
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
 // never exceeds the co-resident CTA capacity, so every waiting role has its
@@ -626,7 +649,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
     const uint64_t* __restrict__ local_item0, uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-    unsigned int* error_flag, uint64_t spin_limit, int fault_inject) {
+    unsigned int* error_flag, uint64_t spin_limit, int flags) {
   const int lane_id = threadIdx.x & 31;
   const int warp_in_block = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
@@ -634,7 +657,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
 
   if (blockIdx.x < ntx + nrx) {
     const bool sender = blockIdx.x < ntx;
-    if (fault_inject == 1 && !sender) return;  // test hook: the receiving peer is gone
+    if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
     const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
@@ -656,11 +679,11 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
       __syncthreads();
       if (!ok_shared) return;
       if (sender) {
-        // pack: frame f copies its source box into the slot (remote stores)
-        for (uint32_t f = 0; f < B.npack; ++f) {
-          const rs_copy_desc& D = frames[B.pack0 + f];
-          const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
-          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<true, 8>(D, it, lane_id);
+        // pack: the batch's frames copy their source boxes into the slot
+        // (remote stores); one flat item space over the frames, dealt to warps
+        for (uint32_t it = warp_in_block; it < B.pack_items; it += warps_per_block) {
+          const rs_copy_desc& D = frames[B.pack0 + find_frame(frames + B.pack0, B.npack, it)];
+          warp_copy_item<true, 8>(D, it - D.item0, lane_id);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -668,10 +691,17 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
           st_release_sys(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq);
         }
       } else {
-        for (uint32_t f = 0; f < B.nunpack; ++f) {
-          const rs_copy_desc& D = frames[B.unpack0 + f];
-          const uint64_t n = (D.rows + D.rows_per_item - 1) / D.rows_per_item;
-          for (uint64_t it = warp_in_block; it < n; it += warps_per_block) warp_copy_item<false, 8>(D, it, lane_id);
+        for (uint32_t it = warp_in_block; it < B.unpack_items; it += warps_per_block) {
+          const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
+          warp_copy_item<false, 8>(D, it - D.item0, lane_id);
+        }
+        if ((flags & kExDiscard) && B.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
+          // every load of the slot has completed (its data was stored); the
+          // discards are ordered before the credit like writes (bar + fence)
+          __syncthreads();
+          const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(slot) * L.slot_bytes;
+          const uint64_t lines = (B.extent + 127) >> 7;
+          for (uint64_t i = threadIdx.x; i < lines; i += blockDim.x) discard_l2_line(base + (i << 7));
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -769,13 +799,13 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-                               unsigned int* error_flag, uint64_t spin_limit, int fault_inject,
+                               unsigned int* error_flag, uint64_t spin_limit, int flags,
                                int local_blocks, cudaStream_t stream) {
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
   rs_exchange_kernel<<<grid, 256, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,
                                                local_item0, nlocal, local_items, epoch, error_flag, spin_limit,
-                                               fault_inject);
+                                               flags);
   return cudaGetLastError();
 }
 

@@ -24,8 +24,8 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
                                const rs_batch_desc* batches, const rs_copy_desc* frames,
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-                               unsigned int* error_flag, uint64_t spin_limit, int fault_inject,
-                               int local_blocks, cudaStream_t stream);
+                               unsigned int* error_flag, uint64_t spin_limit, int flags,
+                               int local_blocks, cudaStream_t stream);  // flags: 1 fault-inject, 2 L2 discard
 
 int rs_kernel_max_blocks_per_sm(int which);
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
     "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
-    "rs_xfer_step", "rs_switch", "rs_store_swap",
+    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement",
 ]
 
 
@@ -79,6 +79,21 @@ class EngineOptions(C.Structure):
                 ("blocks_per_sm", C.c_int32), ("copy_kernel", C.c_int32),
                 ("world_slots", C.c_int32), ("first_local_slot", C.c_int32),
                 ("spin_limit", C.c_int64), ("fault_inject", C.c_int32),
+                ("ring_slot_kib", C.c_int32), ("ring_discard", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class PlacementOptions(C.Structure):
+    _fields_ = [("nvlink_gbs", C.c_double), ("hbm_gbs", C.c_double), ("exhaustive_limit", C.c_int64),
+                ("balance_sources", C.c_int32), ("reserved", C.c_int32)]
+
+
+class PlacementResult(C.Structure):
+    _fields_ = [("roofline_ms", C.c_double), ("given_roofline_ms", C.c_double),
+                ("remote_bytes", C.c_int64), ("local_bytes", C.c_int64), ("carryover_bytes", C.c_int64),
+                ("max_link_bytes", C.c_int64), ("given_remote_bytes", C.c_int64),
+                ("given_local_bytes", C.c_int64), ("given_carryover_bytes", C.c_int64),
+                ("given_max_link_bytes", C.c_int64), ("evaluated", C.c_int64), ("exhaustive", C.c_int32),
                 ("reserved", C.c_int32)]
 
 
@@ -167,6 +182,8 @@ def lib() -> C.CDLL:
         L.rs_xfer_step.argtypes = [VP, I32, I32]
         L.rs_switch.argtypes = [VP, VP, P(VP), I32, P(SwitchStats)]
         L.rs_store_swap.argtypes = [VP]
+        L.rs_plan_placement.argtypes = [C.c_char_p, P(Config), P(Config), P(I32), I32, P(PlacementOptions),
+                                        P(I32), P(PlacementResult)]
         _lib = L
     return _lib
 

@@ -159,14 +159,15 @@ class Engine:
                  mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 0,
                  strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
-                 spin_limit: int = 0, fault_inject: int = 0):
+                 spin_limit: int = 0, fault_inject: int = 0, ring_slot_kib: int = 0,
+                 ring_discard: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
         o = N.EngineOptions(len(devs), self._devs, staging_bytes, modes[mode],
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
                             blocks_per_sm, copy_kernel, world_slots, first_local_slot,
-                            spin_limit, fault_inject, 0)
+                            spin_limit, fault_inject, ring_slot_kib, ring_discard, 0)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -348,6 +349,29 @@ def plan_traffic(plan: TransferPlan, c_old: ParallelConfig, slot_old: Sequence[i
     N.check(N.lib().rs_plan_traffic(plan.handle, N.config_struct(c_old, L), so, N.config_struct(c_new, L),
                                     sn, nslots, out))
     return [list(out[4 * s:4 * s + 4]) for s in range(nslots)]
+
+
+def choose_placement(c_old: ParallelConfig, c_new: ParallelConfig, model: ModelSpec,
+                     candidates: Optional[Sequence[int]] = None, nvlink_gbs: float = 900.0,
+                     hbm_gbs: float = 6552.0, balance_sources: bool = False,
+                     exhaustive_limit: int = 0):
+    """Placement-aware rank ordering (extension, rs_plan_placement): the rank
+    list for c_new's tp/pp/dp shape, drawn from ``candidates`` (default: the
+    union of both configs' ranks), that minimises the per-GPU NVLink/HBM
+    roofline of the resize.  Returns (ParallelConfig, stats dict)."""
+    import dataclasses
+    cand = sorted(set(c_old.ranks) | set(c_new.ranks)) if candidates is None else list(candidates)
+    arr = (C.c_int32 * max(1, len(cand)))(*cand)
+    out = (C.c_int32 * max(1, c_new.world))()
+    o = N.PlacementOptions(nvlink_gbs, hbm_gbs, exhaustive_limit, int(balance_sources), 0)
+    res = N.PlacementResult()
+    L = model.num_layers
+    N.check(N.lib().rs_plan_placement(model.to_text().encode(), N.config_struct(c_old, L),
+                                      N.config_struct(c_new, L), arr, len(cand), C.byref(o), out,
+                                      C.byref(res)))
+    stats = {f: getattr(res, f) for f, _ in N.PlacementResult._fields_ if f != "reserved"}
+    stats["exhaustive"] = bool(stats["exhaustive"])
+    return dataclasses.replace(c_new, ranks=[out[i] for i in range(c_new.world)]), stats
 
 
 def execute_plan(plan: TransferPlan, engine: Engine) -> dict:

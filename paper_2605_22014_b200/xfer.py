@@ -111,3 +111,106 @@ def run(engine, device: int, rank_of_slot=lambda s: s, host_staging: bool = Fals
     torch.cuda.synchronize()
     return {"rounds": rounds, "tx_links": ntx, "rx_links": nrx, "bytes_sent": moved,
             "seconds": time.perf_counter() - t0}
+
+
+# --------------------------------------------------------------------------
+# NCCL comparator on one GPU.
+#
+# NCCL refuses two ranks on one device, and torch.distributed refuses
+# self-sends, so the 1-GPU comparator talks to libnccl directly: one
+# single-rank communicator, every link's round buffer moved with
+# ncclSend/ncclRecv to peer 0 (NCCL's self-loop, the path its all-to-all uses
+# for the local block).  The job's "GPUs" are virtual slots on the same device:
+# one RS_MODE_XFER engine per slot, so every cross-slot chunk is packed by our
+# kernel into its link buffer, moved by NCCL into the receiving slot's buffer,
+# and unpacked by our kernel -- the paper's pack -> isend/irecv -> unpack
+# executor on the engine's chunk schedule and staging
+# budget.
+
+class _NcclUniqueId(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]
+
+
+class Nccl:
+    """Minimal ctypes binding of the NCCL point-to-point API (test/bench only)."""
+
+    UINT8 = 1  # ncclUint8
+
+    def __init__(self, device: int):
+        import os
+        path = None
+        try:
+            import nvidia.nccl as _n  # the NCCL torch itself loads
+            cand = os.path.join(list(_n.__path__)[0], "lib", "libnccl.so.2")
+            path = cand if os.path.exists(cand) else None
+        except Exception:
+            pass
+        self.lib = C.CDLL(path or "libnccl.so.2")
+        L = self.lib
+        L.ncclCommInitAll.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int)]
+        for f in (L.ncclSend, L.ncclRecv):
+            f.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.ncclCommDestroy.argtypes = [C.c_void_p]
+        L.ncclGetErrorString.restype = C.c_char_p
+        L.ncclGetVersion.argtypes = [C.POINTER(C.c_int)]
+        v = C.c_int()
+        self._check(L.ncclGetVersion(C.byref(v)), "ncclGetVersion")
+        self.version = v.value
+        self.comm = C.c_void_p()
+        devs = (C.c_int * 1)(device)
+        self._check(L.ncclCommInitAll(C.byref(self.comm), 1, devs), "ncclCommInitAll")
+
+    def _check(self, rc: int, what: str):
+        if rc != 0:
+            raise RuntimeError(f"{what}: {self.lib.ncclGetErrorString(rc).decode()}")
+
+    def group(self, sends, recvs, stream: int):
+        """sends/recvs: [(ptr, nbytes)] to / from peer 0, matched in order."""
+        L = self.lib
+        self._check(L.ncclGroupStart(), "ncclGroupStart")
+        for p, n in sends:
+            self._check(L.ncclSend(C.c_void_p(p), n, self.UINT8, 0, self.comm, C.c_void_p(stream)), "ncclSend")
+        for p, n in recvs:
+            self._check(L.ncclRecv(C.c_void_p(p), n, self.UINT8, 0, self.comm, C.c_void_p(stream)), "ncclRecv")
+        self._check(L.ncclGroupEnd(), "ncclGroupEnd")
+
+    def close(self):
+        if self.comm.value:
+            self.lib.ncclCommDestroy(self.comm)
+            self.comm = C.c_void_p()
+
+
+def run_local_slots(engines, nccl: Nccl, device: int) -> dict:
+    """One handoff across virtual slots on one GPU: engines[k] drives slot k
+    (RS_MODE_XFER, prepared); NCCL moves every link's round buffer.  Send and
+    receive lists are both ordered by (src rank, dst rank), so the k-th send
+    to peer 0 matches the k-th receive from peer 0."""
+    rounds = engines[0].xfer_info()[0]
+    tx, rx = [], []
+    for e in engines:
+        _, ntx, nrx = e.xfer_info()
+        tx += [e.xfer_link(0, i, rounds) for i in range(ntx)]
+        rx += [e.xfer_link(1, i, rounds) for i in range(nrx)]
+    key = lambda l: (l["src_rank"], l["dst_rank"])  # noqa: E731
+    tx.sort(key=key)
+    rx.sort(key=key)
+    assert [key(l) for l in tx] == [key(l) for l in rx], "xfer links do not pair up"
+    stream = torch.cuda.current_stream(device)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for e in engines:
+        e.xfer_step(0)
+    moved = 0
+    for r in range(rounds):
+        for e in engines:
+            e.xfer_step(1, r)
+        sends = [(l["ptr"], l["round_bytes"][r]) for l in tx if l["round_bytes"][r]]
+        recvs = [(l["ptr"], l["round_bytes"][r]) for l in rx if l["round_bytes"][r]]
+        if sends:
+            nccl.group(sends, recvs, stream.cuda_stream)
+            stream.synchronize()
+        moved += sum(n for _, n in sends)
+        for e in engines:
+            e.xfer_step(2, r)
+    torch.cuda.synchronize(device)
+    return {"rounds": rounds, "links": len(tx), "bytes_sent": moved, "seconds": time.perf_counter() - t0}

@@ -261,3 +261,28 @@ def test_staged_peer_failure_times_out_not_hangs():
     rep = R.execute_plan(plan, eng)
     assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+@pytest.mark.parametrize("pair", [((4, 2, 1), (2, 2, 1)), ((2, 2, 1), (4, 2, 1)), ((8, 1, 1), (4, 1, 2)),
+                                  ((2, 2, 2), (4, 2, 1))])
+def test_searched_placement_bitexact(mode, pair, oracle_c):
+    """A destination rank list chosen by rs_plan_placement is an ordinary
+    config: its plan (more carryovers / self-sourced tasks, fewer remote
+    bytes) executes bit-exact against the C oracle."""
+    sp = mini_llama(4)
+    (t0, p0, d0), (t1, p1, d1) = pair
+    co, cn = specs.iota_config(1, t0, p0, d0), specs.iota_config(2, t1, p1, d1)
+    cn, st = R.choose_placement(co, cn, sp, candidates=list(range(max(co.world, cn.world))))
+    assert st["remote_bytes"] <= st["given_remote_bytes"]
+    eng = make_engine(sp, co, cn, mode, 1 << 20, lanes_per_link=2)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    text = plan.text()
+    assert text == oracle_c.plan_text(sp, co, cn)[0]
+    rep = R.execute_plan(plan, eng)
+    orep, ostore = oracle_c.execute(sp, co, cn, text, SEED, 1 << 20)
+    assert rep["ok"] and orep["ok"] and rep["bytes_moved"] == orep["bytes_moved"] == st["remote_bytes"]
+    for (ti, rank), want in ostore.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), want), (ti, rank)
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()

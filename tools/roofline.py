@@ -7,6 +7,8 @@ Per GPU g (one rank per GPU, iota placement):
   HBM_g = out_g + in_g + 2*local_g + 2*carry_g   (every moved byte read + written once)
   t_roof = max_g max(out_g / NVL, in_g / NVL, HBM_g / HBM)
 1-GPU relayout: every logical rank on one GPU, HBM = 2*(plan bytes + carryover).
+"placed_*": the same resize with the destination rank list chosen by
+rs_plan_placement (placement-aware ordering over GPUs 0..7).
 """
 import json
 import os
@@ -18,11 +20,14 @@ from paper_2605_22014_b200 import reshard as R  # noqa: E402
 from paper_2605_22014_b200 import specs  # noqa: E402
 
 NVL = 900e9      # per direction per GPU, nominal (770 measured peer copy)
-HBM = 6466.1e9   # MEASURED_PEAKS.json copy (read+write bytes)
+HBM = 6552.3e9   # MEASURED_PEAKS.json copy (read+write bytes)
 
 
-def per_gpu(case: str):
+def per_gpu(case: str, placed: bool = False):
     sp, co, cn = specs.baseline_case(case)
+    if placed:
+        cn, _ = R.choose_placement(co, cn, sp, candidates=list(range(8)), nvlink_gbs=NVL / 1e9,
+                                   hbm_gbs=HBM / 1e9)
     plan = R.compute_transfer_plan(co, cn, sp)
     out, inn, loc, car = {}, {}, {}, {}
     for line in plan.text().splitlines():
@@ -45,7 +50,7 @@ def per_gpu(case: str):
     t_nvl = max(max(o, i) for _, o, i, _ in rows) / NVL
     t_hbm = max(h for *_, h in rows) / HBM
     one_gpu = 2 * (s["total_bytes"] + s["carryover_bytes"]) / HBM
-    return {"case": case, "gpus": len(gpus), "remote_GB": s["remote_bytes"] / 1e9,
+    return {"case": case, "dst_ranks": cn.ranks, "gpus": len(gpus), "remote_GB": s["remote_bytes"] / 1e9,
             "local_GB": s["local_bytes"] / 1e9, "carry_GB": s["carryover_bytes"] / 1e9,
             "max_out_GB": max(r[1] for r in rows) / 1e9, "max_in_GB": max(r[2] for r in rows) / 1e9,
             "t_nvlink_ms": t_nvl * 1e3, "t_hbm_ms": t_hbm * 1e3, "roofline_ms": max(t_nvl, t_hbm) * 1e3,
@@ -54,5 +59,8 @@ def per_gpu(case: str):
 
 
 if __name__ == "__main__":
-    for c in ("c1", "c2", "c3", "c4", "c5", "c5b"):
-        print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in per_gpu(c).items()}))
+    for c in ("c1", "c2", "c3", "c3z", "c4", "c5", "c5b"):
+        for placed in (False, True):
+            row = per_gpu(c, placed)
+            row["placement"] = "searched" if placed else "iota"
+            print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in row.items()}))
