@@ -200,6 +200,11 @@ def ours(args) -> None:
         import torch.distributed as dist
         dist.init_process_group("gloo")
     sp, co, cn, desc = workload(args.gpus, args.profile_layers)
+    if args.placement == "searched":
+        # placement-aware destination rank list (rs_plan_placement); changes the
+        # plan (more self-held bytes), so it is a different workload: labelled
+        cn, _ = R.choose_placement(co, cn, sp, candidates=sorted(set(co.ranks) | set(cn.ranks)))
+        desc += f" [searched dst rank list {cn.ranks}]"
     plan = R.compute_transfer_plan(co, cn, sp)
     summ = plan.summary()
     total = summ["total_bytes"]
@@ -210,6 +215,7 @@ def ours(args) -> None:
     traffic = R.plan_traffic(plan, co, so, cn, sn, world)
 
     eng = R.Engine([device], staging_bytes=args.staging_bytes, mode=args.mode, lanes_per_link=args.lanes,
+                   ring_slot_kib=args.ring_slot_kib,
                    strict_layers=args.strict, world_slots=world, first_local_slot=rank)
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
@@ -304,7 +310,7 @@ def ours(args) -> None:
                            "all logical ranks on one B200 (intra-device relayout)",
                            f"rank r on GPU r*{world}//8, one process per GPU"),
                        "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
-                       "tasks": summ["task_count"], "mode": args.mode, "staging_bytes": args.staging_bytes,
+                       "tasks": summ["task_count"], "mode": args.mode, "placement": args.placement, "staging_bytes": args.staging_bytes,
                        "strict_layers": bool(args.strict), "copy_kernel": "LDG8 x 3 CTAs/SM, 256 KB items",
                        "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
@@ -412,6 +418,9 @@ def main() -> None:
     ap.add_argument("--staging-bytes", type=int, default=1 << 30)
     ap.add_argument("--lanes", type=int, default=0, help="ring lanes per link (0: automatic)")
     ap.add_argument("--strict", type=int, default=0)
+    ap.add_argument("--placement", default="iota", choices=["iota", "searched"],
+                    help="destination rank list: BASELINE iota, or rs_plan_placement's choice")
+    ap.add_argument("--ring-slot-kib", type=int, default=0, help="STAGED ring slot cap (0: default, -1: none)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

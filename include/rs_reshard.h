@@ -80,7 +80,7 @@ typedef struct {
   const int32_t* device_ids;
   int64_t staging_bytes;    /* per-destination-rank staging budget B */
   int32_t mode;             /* RS_MODE_* */
-  int32_t slots_per_link;   /* ring depth K (>= 2), STAGED */
+  int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 4), STAGED */
   int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
   int32_t strict_layers;    /* 1: one launch per layer (layer barrier), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
@@ -90,10 +90,10 @@ typedef struct {
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
   int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
-  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 128, -1: no cap,
+  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 1024, -1: no cap,
                                slot = B / (inbound links x lanes x K)); B stays the upper bound */
-  int32_t ring_discard;     /* STAGED: 0/1 receivers drop drained slot lines from L2
-                               (discard.global.L2, no write-back), 2: keep them */
+  int32_t ring_discard;     /* STAGED: 1 = receivers drop drained slot lines from L2
+                               (discard.global.L2, no write-back); 0/2 = keep them (default) */
   int32_t reserved;
 } rs_engine_options;
 

@@ -41,7 +41,7 @@ namespace {
 
 constexpr std::size_t kAlign = 256;
 constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
-constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
+constexpr std::uint64_t kRingSlotDefault = 1u << 20;  // default ring slot cap (rs_engine_options.ring_slot_kib)
 constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 std::uint64_t key(int rank, std::uint32_t ti) {
@@ -159,6 +159,7 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
     throw DomainError("engine: unknown mode");
+  if (opts_.slots_per_link == 0) opts_.slots_per_link = 4;  // ring depth default (profiles/r1/ring_sweep_v2.jsonl)
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
   if (opts_.lanes_per_link < 0) opts_.lanes_per_link = 0;  // 0: automatic (compile_staged)
   nslots_ = opts.world_slots > 0 ? opts.world_slots : opts.num_devices;
@@ -683,31 +684,58 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
   // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
   // the sender + receiver CTAs of the busiest slot stop being co-resident.
-  // Automatic choice: the largest power of two <= 16 that keeps them within
-  // 3/4 of one device's CTA capacity (same answer on every process).
-  int P = opts_.lanes_per_link;
-  if (P == 0) {
-    std::vector<int> slot_links(static_cast<std::size_t>(nslots_), 0);
-    std::set<std::pair<int, int>> links;
-    for (const auto& kv : plan.tasks_by_layer)
-      for (const auto& t : kv.second)
-        if (!t.is_local()) links.insert({t.src_rank, t.dst_rank});
+  // Automatic choice: lanes proportional to each link's bytes (a link's
+  // lanes finish together, so the launch ends when the heaviest link does),
+  // scaled so every slot's sender + receiver lanes fit 3/4 of one device's
+  // CTA capacity, at least one and at most 32 per link (same answer on every
+  // process: the plan and the placement are global).
+  std::map<std::pair<int, int>, std::uint64_t> link_bytes;
+  for (const auto& kv : plan.tasks_by_layer)
+    for (const auto& t : kv.second)
+      if (!t.is_local()) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
+  std::map<std::pair<int, int>, int> lanes_of;
+  if (opts_.lanes_per_link > 0) {
+    for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
+  } else if (!link_bytes.empty()) {
     auto slot_of = [&](const Store& s, int rank) {
       for (const auto& e : s.entries)
         if (e.rank == rank) return e.slot;
       return 0;
     };
     std::map<int, int> src_slot, dst_slot;
-    for (const auto& [s, d] : links) {
-      if (!src_slot.count(s)) src_slot[s] = slot_of(src, s);
-      if (!dst_slot.count(d)) dst_slot[d] = slot_of(dst, d);
-      ++slot_links[static_cast<std::size_t>(src_slot[s])];
-      ++slot_links[static_cast<std::size_t>(dst_slot[d])];
+    std::vector<std::uint64_t> slot_bytes(static_cast<std::size_t>(nslots_), 0);
+    for (const auto& [lk, b] : link_bytes) {
+      if (!src_slot.count(lk.first)) src_slot[lk.first] = slot_of(src, lk.first);
+      if (!dst_slot.count(lk.second)) dst_slot[lk.second] = slot_of(dst, lk.second);
+      slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
+      slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
     }
-    const int busiest = std::max(1, *std::max_element(slot_links.begin(), slot_links.end()));
     const int capacity = grid_for(0, 2) * 3 / 4;
-    P = 16;
-    while (P > 1 && busiest * P > capacity) P /= 2;
+    const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
+    const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
+    std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
+    for (const auto& [lk, b] : link_bytes) {
+      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, 32);
+      lanes_of[lk] = n;
+      slot_lanes[static_cast<std::size_t>(src_slot[lk.first])] += n;
+      slot_lanes[static_cast<std::size_t>(dst_slot[lk.second])] += n;
+    }
+    // the max(1, .) floor can overshoot a slot with many light links: trim
+    // the widest links touching it
+    for (int sl = 0; sl < nslots_; ++sl)
+      while (slot_lanes[static_cast<std::size_t>(sl)] > capacity) {
+        std::pair<int, int> widest{-1, -1};
+        int w = 1;
+        for (const auto& [lk, n] : lanes_of)
+          if ((src_slot[lk.first] == sl || dst_slot[lk.second] == sl) && n > w) {
+            w = n;
+            widest = lk;
+          }
+        if (widest.first < 0) break;  // every link at one lane: the launch check reports it
+        --lanes_of[widest];
+        --slot_lanes[static_cast<std::size_t>(src_slot[widest.first])];
+        --slot_lanes[static_cast<std::size_t>(dst_slot[widest.second])];
+      }
   }
   // each destination rank's B-sized region in its slot's comm arena
   std::map<int, std::size_t> region_of;  // dst rank -> byte offset in its slot's comm arena
@@ -719,16 +747,19 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       for (int r : ranks) region_of[r] = (i++) * static_cast<std::size_t>(B);
     }
   }
-  // Ring slot size per dst rank: B split over its inbound lanes, capped so the
-  // rings stay L2-resident (the receiver unpacks a slot microseconds after
-  // it was packed and then discards its lines): B is the budget, not the
-  // target footprint.
+  // Ring slot size per dst rank: B split over its inbound lanes, capped at
+  // 1 MiB by default -- B is the budget, not the target footprint.  Larger
+  // slots buy nothing (the lane copy rate, not the handshake, bounds a batch
+  // beyond ~1 MiB), smaller ones pay the per-batch handshake
+  // (profiles/r1/ring_sweep_v2.jsonl).
   const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
                                  : opts_.ring_slot_kib == 0 ? kRingSlotDefault
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
+  std::map<int, std::uint64_t> inbound_lanes;  // dst rank -> lanes into it
+  for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
   std::map<int, std::uint64_t> slot_bytes_of;
   for (const auto& [d, srcs] : inbound) {
-    std::uint64_t sb = static_cast<std::uint64_t>(B) / (srcs.size() * static_cast<std::uint64_t>(P * K));
+    std::uint64_t sb = static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(K));
     sb = std::min(sb, slot_cap);
     slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
   }
@@ -803,6 +834,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
                                  " inbound links)");
           const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
           const auto lk = std::make_pair(t.src_rank, t.dst_rank);
+          const int P = lanes_of.at(lk);
           if (!link_first_lane.count(lk)) {
             link_first_lane[lk] = static_cast<int>(lanes.size());
             for (int p = 0; p < P; ++p) lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, {}, 0});
@@ -1067,7 +1099,7 @@ rs_exec_report Engine::run() {
                                     reinterpret_cast<unsigned int*>(p.d_error.data()),
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
-                                    (opts_.fault_inject == 1 ? 1 : 0) | (opts_.ring_discard != 2 ? 2 : 0),
+                                    (opts_.fault_inject == 1 ? 1 : 0) | (opts_.ring_discard == 1 ? 2 : 0),
                                     cap - p.ntx - p.nrx, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;

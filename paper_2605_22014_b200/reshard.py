@@ -156,7 +156,7 @@ class Engine:
     """Device engine: stores for C_old (RS_SRC) and C_new (RS_DST) + execution."""
 
     def __init__(self, devices: Iterable[int] = (0,), staging_bytes: int = 1 << 30,
-                 mode: str = "direct", slots_per_link: int = 2, lanes_per_link: int = 0,
+                 mode: str = "direct", slots_per_link: int = 0, lanes_per_link: int = 0,
                  strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
                  spin_limit: int = 0, fault_inject: int = 0, ring_slot_kib: int = 0,

@@ -286,3 +286,29 @@ def test_searched_placement_bitexact(mode, pair, oracle_c):
         assert np.array_equal(eng.read(RS_DST, rank, ti), want), (ti, rank)
     assert eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("K,cap_kib,discard", [(2, 0, 1), (2, -1, 0), (8, 64, 1), (3, 4, 0)])
+def test_ring_geometry_variants_bitexact(K, cap_kib, discard, golden, oracle_c):
+    """Ring depth K, the slot cap and the L2 discard of drained slots change
+    how frames are batched and when slot lines may be dropped -- never the
+    destination bytes (reference digests, 40 random pairs + full GPT-2 C1)."""
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(40, golden["random_pairs"]["base_seed"]):
+        eng = make_engine(sp, co, cn, "staged", 1 << 16, lanes_per_link=1, slots_per_link=K,
+                          ring_slot_kib=cap_kib, ring_discard=discard)
+        rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+        assert rep["ok"], (seed, rep)
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            rows[seed]["exec"]["4096"]["dst_sha"], seed
+        eng.close()
+    sp, co, cn = specs.baseline_case("c1")
+    eng = make_engine(sp, co, cn, "staged", 256 << 20, slots_per_link=K, ring_slot_kib=cap_kib,
+                      ring_discard=discard)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    for _ in range(2):
+        rep = R.execute_plan(plan, eng)
+        assert rep["ok"] and rep["peak_staging_bytes"] <= 256 << 20
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            golden["c1_exec"]["1073741824"]["dst_sha"]
+    eng.close()

@@ -19,7 +19,17 @@ from paper_2605_22014_b200 import reshard as R  # noqa: E402
 from paper_2605_22014_b200 import specs  # noqa: E402
 from paper_2605_22014_b200.native import RS_DST, RS_SRC  # noqa: E402
 
-HBM = 6466.1
+def _peak():
+    import json as _j
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(_j.load(f)["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        return 6466.1
+
+
+HBM = _peak()
 
 
 def run(case, mode, layers=None):
