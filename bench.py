@@ -65,16 +65,36 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        nvml = None
+        try:  # NVML: a sample costs microseconds, so short timed regions still get many
+            import pynvml as nvml
+            nvml.nvmlInit()
+            h = nvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nvml.nvmlDeviceGetMaxClockInfo(h, nvml.NVML_CLOCK_SM)
+            bits = [(0x8, "Active"), (0x40, "Active"), (0x20, "Active"), (0x4, "Active")]
+        except Exception:
+            nvml = None
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if nvml is not None:
+                    sm = nvml.nvmlDeviceGetClockInfo(h, nvml.NVML_CLOCK_SM)
+                    r = nvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append([str(self.index), str(sm), str(mx)] +
+                                     ["Active" if r & b else "Not Active" for b, _ in bits])
+                else:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if nvml is not None else 0.2)
+        if nvml is not None:
+            try:
+                nvml.nvmlShutdown()
+            except Exception:
+                pass
 
     def __enter__(self):
         self._t.start()
@@ -222,7 +242,7 @@ def ours(args) -> None:
     eng.alloc(RS_SRC)
     eng.alloc(RS_DST)
     if args.mode == "staged":
-        eng.comm_alloc()
+        eng.comm_alloc(plan)
     eng.fill_pattern(RS_SRC, SEED)
     if world > 1:
         from paper_2605_22014_b200.dist import connect
@@ -282,13 +302,17 @@ def ours(args) -> None:
     pk = peaks()
     if world == 1:
         algo_bytes = 2 * (total + summ["carryover_bytes"])  # read + write of every moved byte
+        kernel = "rs_copy_kernel"
+        if args.mode == "staged":  # ring path: each remote byte also crosses a ring slot (write + read)
+            algo_bytes += 2 * summ["remote_bytes"]
+            kernel = "rs_exchange_kernel"
         achieved = algo_bytes / (step_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "kernel": "rs_copy_kernel",
+                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "kernel": kernel,
                 "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"]}
         tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
+        if os.path.exists(tp) and args.mode == "direct" and not args.profile_layers:
+            with open(tp) as f:  # measured on this exact launch (full-size C2, DIRECT)
                 roof["traffic"] = json.load(f).get("rs_copy_kernel_dram_bytes_per_launch")
     else:
         # the busiest GPU's NVLink direction bounds the handoff

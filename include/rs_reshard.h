@@ -80,7 +80,7 @@ typedef struct {
   const int32_t* device_ids;
   int64_t staging_bytes;    /* per-destination-rank staging budget B */
   int32_t mode;             /* RS_MODE_* */
-  int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 4), STAGED */
+  int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 2), STAGED */
   int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
   int32_t strict_layers;    /* 1: one launch per layer (layer barrier), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
@@ -90,7 +90,7 @@ typedef struct {
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
   int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
-  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 1024, -1: no cap,
+  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 256, -1: no cap,
                                slot = B / (inbound links x lanes x K)); B stays the upper bound */
   int32_t ring_discard;     /* STAGED: 1 = receivers drop drained slot lines from L2
                                (discard.global.L2, no write-back); 0/2 = keep them (default) */
@@ -170,7 +170,13 @@ int rs_store_free(rs_engine* e, int32_t which);
  * on the slot + ring flags, allocated by rs_comm_alloc). */
 #define RS_COMM 2
 #define RS_IPC_HANDLE_BYTES 64
-int rs_comm_alloc(rs_engine* e);
+int rs_comm_alloc(rs_engine* e);                           /* B per destination rank */
+/* Plan-sized staging: each destination rank's region holds exactly the
+ * plan's rings (<= B; ring slots are capped, so usually far less than B).
+ * rs_prepare allocates this itself in a single process when the arena is
+ * missing or too small; with several processes every process calls it with
+ * the same plan before exchanging the RS_COMM handles. */
+int rs_comm_alloc_plan(rs_engine* e, const rs_plan* plan);
 int rs_arena_export(rs_engine* e, int32_t which, int32_t slot, void* handle, int64_t* arena_bytes);
 int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handle, int64_t arena_bytes);
 

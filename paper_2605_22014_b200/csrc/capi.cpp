@@ -395,6 +395,13 @@ int rs_comm_alloc(rs_engine* e) {
   return guarded([&] { e->impl.comm_alloc(); });
 }
 
+int rs_comm_alloc_plan(rs_engine* e, const rs_plan* plan) {
+  return guarded([&] {
+    if (!e || !plan) throw std::invalid_argument("bad argument");
+    e->impl.comm_alloc_plan(plan->plan);
+  });
+}
+
 int rs_arena_export(rs_engine* e, int32_t which, int32_t slot, void* handle, int64_t* arena_bytes) {
   return guarded([&] {
     if (!handle || !arena_bytes) throw std::invalid_argument("null argument");

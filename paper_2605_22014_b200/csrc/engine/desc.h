@@ -64,8 +64,10 @@ typedef struct {
   uint32_t slots;
   uint32_t nbatches;
   uint32_t batch0;          // index of the lane's first batch in the batch table
-  uint32_t pad;
+  uint32_t flags;           // RS_LANE_PEER: sender and receiver are not one device of one process
 } rs_lane_desc;
+
+#define RS_LANE_PEER 1u       // flags / fences at .sys scope (else .gpu)
 
 typedef struct {
   uint32_t pack0, npack;     // frame descriptors packing into the slot (sender side)

@@ -41,7 +41,7 @@ namespace {
 
 constexpr std::size_t kAlign = 256;
 constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
-constexpr std::uint64_t kRingSlotDefault = 1u << 20;  // default ring slot cap (rs_engine_options.ring_slot_kib)
+constexpr std::uint64_t kRingSlotDefault = 256u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
 constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 std::uint64_t key(int rank, std::uint32_t ti) {
@@ -159,7 +159,7 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
     throw DomainError("engine: unknown mode");
-  if (opts_.slots_per_link == 0) opts_.slots_per_link = 4;  // ring depth default (profiles/r1/ring_sweep_v2.jsonl)
+  if (opts_.slots_per_link == 0) opts_.slots_per_link = 2;  // ring depth default (profiles/r1/ring_sweep_v3.jsonl)
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
   if (opts_.lanes_per_link < 0) opts_.lanes_per_link = 0;  // 0: automatic (compile_staged)
   nslots_ = opts.world_slots > 0 ? opts.world_slots : opts.num_devices;
@@ -341,14 +341,28 @@ void Engine::bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t
 // ------------------------------------------------------ comm arenas and IPC
 
 std::size_t Engine::comm_bytes(int slot) const {
-  std::set<int> ranks;
-  for (const auto& e : stores_[RS_DST].entries)
-    if (e.slot == slot) ranks.insert(e.rank);
-  return static_cast<std::size_t>(opts_.staging_bytes) * ranks.size() + kFlagBytes;
+  if (comm_layout_valid_) return comm_layout_.slot_bytes.at(static_cast<std::size_t>(slot));
+  return make_comm_layout(nullptr).slot_bytes.at(static_cast<std::size_t>(slot));
 }
 
 void Engine::comm_alloc() {
   if (!stores_[RS_DST].laid_out) throw DomainError("comm: lay out the dst store first");
+  comm_layout_ = make_comm_layout(nullptr);
+  comm_layout_valid_ = true;
+  alloc_comm_arenas();
+}
+
+// Plan-sized rings: each dst rank's region holds exactly its rings (<= B),
+// so resident staging is what the rings use, not B per rank.
+void Engine::comm_alloc_plan(const reshard::TransferPlan& plan) {
+  if (!stores_[RS_DST].laid_out || !stores_[RS_SRC].laid_out) throw DomainError("comm: lay out both stores first");
+  const RingGeometry geo = ring_geometry(plan);
+  comm_layout_ = make_comm_layout(&geo.ring_bytes_of);
+  comm_layout_valid_ = true;
+  alloc_comm_arenas();
+}
+
+void Engine::alloc_comm_arenas() {
   comm_.clear();
   for (const auto& dv : devices_) {
     const std::size_t n = comm_bytes(dv.slot);
@@ -569,20 +583,34 @@ void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
   } else {
     // The ring area is B per destination rank of the slot, so it follows the
     // dst layout: a live-handoff chain changes it every generation.
-    bool stale = comm_.size() != devices_.size();
+    // The comm arena must hold this plan's rings for the current dst layout:
+    // B per rank (rs_comm_alloc) or plan-sized (rs_comm_alloc_plan).  One
+    // process: (re)allocate plan-sized when it does not.  Several processes:
+    // the arenas are IPC-shared, so every process must re-run the alloc.
+    bool stale = !comm_layout_valid_ || comm_.size() != devices_.size();
     for (std::size_t d = 0; !stale && d < devices_.size(); ++d)
       stale = comm_[d].size() != comm_bytes(devices_[d].slot);
+    if (!stale) {
+      const RingGeometry geo = ring_geometry(plan);
+      std::map<int, int> slot_of_rank;
+      for (const auto& e : stores_[RS_DST].entries) slot_of_rank[e.rank] = e.slot;
+      for (const auto& [r, need] : geo.ring_bytes_of) {
+        const auto& regs = comm_layout_.regions.at(static_cast<std::size_t>(slot_of_rank.at(r)));
+        auto it = regs.find(r);
+        if (it == regs.end() || it->second.second < need) stale = true;
+      }
+    }
     for (int s = 0; s < nslots_; ++s)
       if (local_of(s) < 0 && comm_imported_[static_cast<std::size_t>(s)] &&
           comm_imported_bytes_[static_cast<std::size_t>(s)] != comm_bytes(s))
         throw DomainError("staged: peer comm arena of slot " + std::to_string(s) +
-                          " was sized for another dst layout; re-run rs_comm_alloc on every process and "
-                          "re-exchange the RS_COMM handles");
+                          " was sized for another dst layout or plan; re-run rs_comm_alloc_plan on every process "
+                          "and re-exchange the RS_COMM handles");
     if (stale) {
-      if (nslots_ > num_devices() && !comm_.empty())
-        throw DomainError("staged: comm arena was sized for another dst layout; re-run rs_comm_alloc on every "
-                          "process and re-exchange the RS_COMM handles");
-      comm_alloc();
+      if (nslots_ > num_devices())
+        throw DomainError("staged: comm arena missing or sized for another dst layout or plan; run "
+                          "rs_comm_alloc_plan on every process and exchange the RS_COMM handles");
+      comm_alloc_plan(plan);
     }
     compile_staged(plan);
   }
@@ -668,13 +696,15 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
   planned_.ok = 1;
 }
 
-void Engine::compile_staged(const reshard::TransferPlan& plan) {
+// Ring geometry of a plan (STAGED): lanes per link, slot size and ring bytes
+// per destination rank.  Deterministic from the plan and the layouts, so
+// every process computes the same rings for every slot.
+Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) const {
   const Store& src = stores_[RS_SRC];
   const Store& dst = stores_[RS_DST];
-  const auto& m = src.model;
   const std::int64_t B = opts_.staging_bytes;
   const int K = opts_.slots_per_link;
-
+  RingGeometry geo;
   // inbound links per destination rank (remote tasks only)
   std::map<int, std::set<int>> inbound;
   for (const auto& kv : plan.tasks_by_layer)
@@ -693,7 +723,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
       if (!t.is_local()) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
-  std::map<std::pair<int, int>, int> lanes_of;
+  auto& lanes_of = geo.lanes_of;
   if (opts_.lanes_per_link > 0) {
     for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
   } else if (!link_bytes.empty()) {
@@ -737,32 +767,72 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         --slot_lanes[static_cast<std::size_t>(dst_slot[widest.second])];
       }
   }
-  // each destination rank's B-sized region in its slot's comm arena
-  std::map<int, std::size_t> region_of;  // dst rank -> byte offset in its slot's comm arena
-  {
-    std::map<int, std::set<int>> ranks_on_slot;
-    for (const auto& e : dst.entries) ranks_on_slot[e.slot].insert(e.rank);
-    for (const auto& [slot, ranks] : ranks_on_slot) {
-      std::size_t i = 0;
-      for (int r : ranks) region_of[r] = (i++) * static_cast<std::size_t>(B);
-    }
-  }
   // Ring slot size per dst rank: B split over its inbound lanes, capped at
-  // 1 MiB by default -- B is the budget, not the target footprint.  Larger
-  // slots buy nothing (the lane copy rate, not the handshake, bounds a batch
-  // beyond ~1 MiB), smaller ones pay the per-batch handshake
-  // (profiles/r1/ring_sweep_v2.jsonl).
+  // 256 KiB by default -- B is the budget, not the target footprint.  With
+  // GPU-scope handshakes for same-device lanes, 128-256 KiB slots x K = 2
+  // keep the rings small enough to stay largely L2-resident (less HBM
+  // traffic than the 4x of a DRAM-resident ring) while a batch is still long
+  // against its handshake; 32 KiB slots pay the handshake, >= 1 MiB slots
+  // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).
   const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
                                  : opts_.ring_slot_kib == 0 ? kRingSlotDefault
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
-  std::map<int, std::uint64_t> inbound_lanes;  // dst rank -> lanes into it
+  auto& inbound_lanes = geo.inbound_lanes;
   for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
-  std::map<int, std::uint64_t> slot_bytes_of;
+  auto& slot_bytes_of = geo.slot_bytes_of;
   for (const auto& [d, srcs] : inbound) {
     std::uint64_t sb = static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(K));
     sb = std::min(sb, slot_cap);
     slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
+    geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(K);
   }
+
+  return geo;
+}
+
+// Comm arena layout over every slot: the dst ranks of a slot in ascending
+// order, each with `ring_bytes[rank]` (plan-sized) or B bytes, then the flags.
+Engine::CommLayout Engine::make_comm_layout(const std::map<int, std::uint64_t>* ring_bytes) const {
+  CommLayout L;
+  L.regions.resize(static_cast<std::size_t>(nslots_));
+  L.slot_bytes.assign(static_cast<std::size_t>(nslots_), kFlagBytes);
+  std::map<int, std::set<int>> ranks_on_slot;
+  for (const auto& e : stores_[RS_DST].entries) ranks_on_slot[e.slot].insert(e.rank);
+  for (const auto& [slot, ranks] : ranks_on_slot) {
+    std::size_t off = 0;
+    for (int r : ranks) {
+      std::size_t b = static_cast<std::size_t>(opts_.staging_bytes);
+      if (ring_bytes) {
+        auto it = ring_bytes->find(r);
+        b = it == ring_bytes->end() ? 0 : align_up(static_cast<std::size_t>(it->second), kAlign);
+      }
+      L.regions[static_cast<std::size_t>(slot)][r] = {off, b};
+      off += b;
+    }
+    L.slot_bytes[static_cast<std::size_t>(slot)] = off + kFlagBytes;
+  }
+  return L;
+}
+
+void Engine::compile_staged(const reshard::TransferPlan& plan) {
+  const Store& src = stores_[RS_SRC];
+  const Store& dst = stores_[RS_DST];
+  const auto& m = src.model;
+  const std::int64_t B = opts_.staging_bytes;
+  const int K = opts_.slots_per_link;
+
+  const RingGeometry geo = ring_geometry(plan);
+  const auto& lanes_of = geo.lanes_of;
+  const auto& slot_bytes_of = geo.slot_bytes_of;
+  const auto& inbound_lanes = geo.inbound_lanes;
+  // each destination rank's region in its slot's comm arena (the layout the
+  // arena was allocated with: B per rank, or plan-sized, rs_comm_alloc_plan)
+  std::map<int, std::size_t> region_of, region_bytes;
+  for (std::size_t sl = 0; sl < comm_layout_.regions.size(); ++sl)
+    for (const auto& [r, ob] : comm_layout_.regions[sl]) {
+      region_of[r] = ob.first;
+      region_bytes[r] = ob.second;
+    }
 
   struct Frame {
     const Entry* se;
@@ -830,7 +900,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);
           if (static_cast<std::uint64_t>(eb) > sb)
             throw IntegrityError("staging: ring slot of " + std::to_string(sb) + " bytes cannot hold one element (B=" +
-                                 std::to_string(B) + " over " + std::to_string(inbound[t.dst_rank].size()) +
+                                 std::to_string(B) + " over " + std::to_string(inbound_lanes.at(t.dst_rank)) +
                                  " inbound links)");
           const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
           const auto lk = std::make_pair(t.src_rank, t.dst_rank);
@@ -894,8 +964,16 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   for (std::size_t i = 0; i < lanes.size(); ++i) {
     const auto& lb = lanes[i];
     std::uint64_t& used = ring_used[lb.dst_rank];
-    where[i].ring_off = region_of.at(lb.dst_rank) + used;
+    auto reg = region_of.find(lb.dst_rank);
+    if (reg == region_of.end())
+      throw DomainError("staged: comm arena has no ring region for dst rank " + std::to_string(lb.dst_rank) +
+                        "; re-run rs_comm_alloc for this dst layout");
+    where[i].ring_off = reg->second + used;
     used += lb.slot_bytes * static_cast<std::uint64_t>(K);
+    if (used > region_bytes.at(lb.dst_rank))
+      throw DomainError("staged: ring region of dst rank " + std::to_string(lb.dst_rank) + " (" +
+                        std::to_string(region_bytes.at(lb.dst_rank)) + " bytes) is smaller than this plan's rings; " +
+                        "re-run rs_comm_alloc_plan with this plan");
     auto& fr = flag_used[static_cast<std::size_t>(lb.dslot)];
     auto& fc = flag_used[static_cast<std::size_t>(lb.sslot)];
     if (fr + flags_per_lane > kFlagBytes || fc + flags_per_lane > kFlagBytes)
@@ -932,6 +1010,10 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     L.ready_flags = L.ready_flags_rx = ready ? addr(ready) + where[i].ready_off : 0;
     L.credit_flags = L.credit_flags_tx = credit ? addr(credit) + where[i].credit_off : 0;
     L.slots = static_cast<std::uint32_t>(K);
+    // GPU-scope synchronisation only when both ends are this process's same
+    // slot; every cross-slot lane (another GPU, or another process sharing a
+    // GPU through IPC) synchronises at system scope
+    L.flags = lb.sslot == lb.dslot ? 0u : RS_LANE_PEER;
     L.batch0 = static_cast<std::uint32_t>(batches.size());
     L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
     // work items inside a batch: ~32 per slot so all 8 warps of the lane's

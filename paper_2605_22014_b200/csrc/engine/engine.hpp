@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -132,7 +133,8 @@ class Engine {
   const Store& store(int which) const { return stores_[which]; }
   Store& store(int which) { return stores_[which]; }
 
-  void comm_alloc();
+  void comm_alloc();                                      // B per dst rank
+  void comm_alloc_plan(const reshard::TransferPlan& plan);  // exactly this plan's rings
   // Layer window for host-resident stores: only `layers` layers' source and
   // destination shards live on each local device at a time (slot l % layers),
   // bounding device memory like the reference's per-layer staging.
@@ -185,6 +187,19 @@ class Engine {
   void copy_runs(const Store& s, const std::vector<std::size_t>& idx, void* const* host, bool to_device);
   void compile_direct(const reshard::TransferPlan& plan);
   void compile_staged(const reshard::TransferPlan& plan);
+  struct RingGeometry {
+    std::map<std::pair<int, int>, int> lanes_of;     // (src rank, dst rank) -> lanes
+    std::map<int, std::uint64_t> inbound_lanes;      // dst rank -> lanes into it
+    std::map<int, std::uint64_t> slot_bytes_of;      // dst rank -> ring slot bytes
+    std::map<int, std::uint64_t> ring_bytes_of;      // dst rank -> bytes of all its rings
+  };
+  RingGeometry ring_geometry(const reshard::TransferPlan& plan) const;
+  struct CommLayout {
+    std::vector<std::map<int, std::pair<std::size_t, std::size_t>>> regions;  // per slot: rank -> (offset, bytes)
+    std::vector<std::size_t> slot_bytes;                                      // per slot, incl. flags
+  };
+  CommLayout make_comm_layout(const std::map<int, std::uint64_t>* ring_bytes) const;
+  void alloc_comm_arenas();
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
   int copy_variant(int dev) const;
@@ -200,6 +215,8 @@ class Engine {
   Store stores_[2];
   std::vector<DeviceProgram> programs_;
   std::vector<DeviceBuffer> comm_;                        // per local device
+  CommLayout comm_layout_;                                // layout of the comm arenas, every slot
+  bool comm_layout_valid_ = false;
   std::vector<std::unique_ptr<ImportedArena>> comm_imported_;  // per slot
   std::vector<std::size_t> comm_imported_bytes_;               // per slot
   int window_layers_ = 0;

@@ -601,12 +601,35 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Same-device lanes (sender and receiver CTAs on one GPU, one process) only
+// need GPU scope: cheaper fences and flag accesses than .sys.
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Publish everything this CTA wrote (after a __syncthreads) with one release.
+__device__ __forceinline__ void publish(uint64_t* flag, uint64_t v, bool peer) {
+  if (peer) {
+    __threadfence_system();
+    st_release_sys(flag, v);
+  } else {
+    __threadfence();
+    st_release_gpu(flag, v);
+  }
+}
+
 // Spin with a bounded budget; on expiry raise the error flag (no hangs on a
 // protocol bug: the host reports failed_layer instead).
 __device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
-                                         unsigned int* error_flag, uint64_t spin_limit) {
+                                         unsigned int* error_flag, uint64_t spin_limit, bool peer) {
   uint64_t spins = 0;
-  while (ld_acquire_sys(flag) < want) {
+  while ((peer ? ld_acquire_sys(flag) : ld_acquire_gpu(flag)) < want) {
     if (*reinterpret_cast<volatile unsigned int*>(error_flag)) return false;
     if (++spins > spin_limit) {
       atomicExch(error_flag, 1u);
@@ -659,6 +682,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
     const bool sender = blockIdx.x < ntx;
     if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
     const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
+    const bool peer = (L.flags & RS_LANE_PEER) != 0;
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
       const uint32_t slot = b % L.slots;
@@ -669,10 +693,10 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
           // slot reuse: the receiver must have drained batch b - slots
           ok = b < L.slots ||
                wait_geq(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + slot,
-                        epoch + b - L.slots + 1, error_flag, spin_limit);
+                        epoch + b - L.slots + 1, error_flag, spin_limit, peer);
         } else {
           ok = wait_geq(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + slot, seq, error_flag,
-                        spin_limit);
+                        spin_limit, peer);
         }
         ok_shared = ok;
       }
@@ -686,10 +710,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
           warp_copy_item<true, 8>(D, it - D.item0, lane_id);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-          __threadfence_system();
-          st_release_sys(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq);
-        }
+        if (threadIdx.x == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq, peer);
       } else {
         for (uint32_t it = warp_in_block; it < B.unpack_items; it += warps_per_block) {
           const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
@@ -704,10 +725,7 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
           for (uint64_t i = threadIdx.x; i < lines; i += blockDim.x) discard_l2_line(base + (i << 7));
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-          __threadfence_system();
-          st_release_sys(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, seq);
-        }
+        if (threadIdx.x == 0) publish(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, seq, peer);
       }
     }
     return;

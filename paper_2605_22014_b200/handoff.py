@@ -194,7 +194,7 @@ class LiveHandoff:
         eng.alloc(RS_DST)
         self._allocate("shadow_store", eng.store_bytes(RS_DST))
         if getattr(eng, "mode", "direct") == "staged":
-            eng.comm_alloc()  # rings are B per destination rank: they follow the shadow layout
+            eng.comm_alloc(plan)  # plan-sized rings (<= B per dst rank): they follow the shadow layout
             self._connect((RS_DST, RS_COMM))
         else:
             self._connect((RS_DST,))

@@ -27,7 +27,7 @@ EXPORTS = [
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
     "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
-    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement",
+    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan",
 ]
 
 
@@ -174,6 +174,7 @@ def lib() -> C.CDLL:
         L.rs_host_alloc.argtypes = [SZ, P(VP)]
         L.rs_host_free.argtypes = [VP]
         L.rs_comm_alloc.argtypes = [VP]
+        L.rs_comm_alloc_plan.argtypes = [VP, VP]
         L.rs_arena_export.argtypes = [VP, I32, I32, VP, P(I64)]
         L.rs_arena_import.argtypes = [VP, I32, I32, VP, I64]
         L.rs_plan_traffic.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, P(I64)]

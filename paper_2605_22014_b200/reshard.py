@@ -248,8 +248,13 @@ class Engine:
         N.check(N.lib().rs_store_write(self._h, which, rank, tensor_index, offset, a.size,
                                        a.ctypes.data_as(C.c_void_p)))
 
-    def comm_alloc(self):
-        N.check(N.lib().rs_comm_alloc(self._h))
+    def comm_alloc(self, plan: Optional["TransferPlan"] = None):
+        """STAGED staging arena: B per destination rank, or exactly ``plan``'s
+        rings (rs_comm_alloc_plan)."""
+        if plan is None:
+            N.check(N.lib().rs_comm_alloc(self._h))
+        else:
+            N.check(N.lib().rs_comm_alloc_plan(self._h, plan.handle))
 
     # -- RS_MODE_XFER (comparator transport) -------------------------------
     def xfer_info(self):

@@ -55,12 +55,12 @@ def ipc_reshard(rank, world, mode):
     eng.layout(RS_DST, sp, cn, sn)
     eng.alloc(RS_SRC)
     eng.alloc(RS_DST)
-    eng.comm_alloc()
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng.comm_alloc(plan if mode == "staged" else None)  # plan-sized rings, same on every process
     eng.fill_pattern(RS_SRC, 42)
     eng.fill_pattern(RS_DST, 7)
     connect(eng)
     dist.barrier()
-    plan = R.compute_transfer_plan(co, cn, sp)
     eng.prepare(plan)
     dist.barrier()
     rep = eng.run()

@@ -312,3 +312,26 @@ def test_ring_geometry_variants_bitexact(K, cap_kib, discard, golden, oracle_c):
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
             golden["c1_exec"]["1073741824"]["dst_sha"]
     eng.close()
+
+
+def test_plan_sized_staging_arena():
+    """rs_comm_alloc_plan sizes each destination rank's ring region to the
+    plan's rings (<= B); rs_prepare re-sizes a single-process arena that is
+    too small for a new plan; results stay bit-exact."""
+    sp = mini_llama(4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 1)
+    B = 64 << 20
+    eng = make_engine(sp, co, cn, "staged", B, ring_slot_kib=64)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng.comm_alloc(plan)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    assert 0 < rep["peak_staging_bytes"] < B
+    eng.close()
+    # an arena sized for a lighter plan is grown by prepare (single process)
+    eng = make_engine(sp, co, cn, "staged", B)
+    light = R.compute_transfer_plan(co, specs.iota_config(2, 4, 2, 1), sp)  # identity layout: no rings
+    eng.comm_alloc(light)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()

@@ -35,7 +35,7 @@ def staged(sp, co, cn, plan, B, mode, steps, warmup):
     eng.alloc(RS_SRC)
     eng.alloc(RS_DST)
     if mode == "staged":
-        eng.comm_alloc()
+        eng.comm_alloc(plan)
     eng.fill_pattern(RS_SRC, SEED)
     eng.fill_pattern(RS_DST, 7)
     eng.prepare(plan)

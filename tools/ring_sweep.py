@@ -37,7 +37,7 @@ def main():
                     eng.layout(RS_DST, sp, cn)
                     eng.alloc(RS_SRC)
                     eng.alloc(RS_DST)
-                    eng.comm_alloc()
+                    eng.comm_alloc(plan)
                     eng.fill_pattern(RS_SRC, 42)
                     eng.fill_pattern(RS_DST, 7)
                     row = {"case": case, "layers": layers, "B_MiB": B >> 20, "discard": discard == 1,
