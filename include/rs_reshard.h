@@ -92,8 +92,10 @@ typedef struct {
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
   int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 256, -1: no cap,
                                slot = B / (inbound links x lanes x K)); B stays the upper bound */
-  int32_t ring_discard;     /* STAGED: 1 = receivers drop drained slot lines from L2
-                               (discard.global.L2, no write-back); 0/2 = keep them (default) */
+  int32_t ring_discard;     /* STAGED L2 treatment of ring slots: 0 = default (1|4); else bit
+                               flags 1 = receivers drop drained slot lines (discard.global.L2,
+                               no write-back), 4 = L2 policies (shards evict-first, slots
+                               evict-last); 2 = neither */
   int32_t reserved;
 } rs_engine_options;
 

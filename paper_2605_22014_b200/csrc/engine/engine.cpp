@@ -773,7 +773,9 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   // keep the rings small enough to stay largely L2-resident (less HBM
   // traffic than the 4x of a DRAM-resident ring) while a batch is still long
   // against its handshake; 32 KiB slots pay the handshake, >= 1 MiB slots
-  // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).
+  // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).  The kernel adds
+  // evict-first / evict-last L2 policies and discards drained slots by
+  // default (ring_sweep_v4.jsonl: 15.4 -> 13.1 ms on the C5 slice).
   const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
                                  : opts_.ring_slot_kib == 0 ? kRingSlotDefault
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
@@ -1171,6 +1173,8 @@ rs_exec_report Engine::run() {
       if (!p.ntx && !p.nrx && !p.local_items) continue;
       DeviceGuard g(devices_[d].ordinal);
       const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
+      // ring slots in L2: 0 = default (discard + policies), else bit flags (2 = neither)
+      const int ring_l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;
       cuda_check(rs_launch_exchange(lanes, static_cast<std::uint32_t>(p.ntx), lanes + p.ntx,
                                     static_cast<std::uint32_t>(p.nrx),
                                     reinterpret_cast<const rs_batch_desc*>(p.d_batches.data()),
@@ -1181,7 +1185,7 @@ rs_exec_report Engine::run() {
                                     reinterpret_cast<unsigned int*>(p.d_error.data()),
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
-                                    (opts_.fault_inject == 1 ? 1 : 0) | (opts_.ring_discard == 1 ? 2 : 0),
+                                    (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0),
                                     cap - p.ntx - p.nrx, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;

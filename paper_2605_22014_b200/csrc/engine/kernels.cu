@@ -589,6 +589,67 @@ __global__ void __launch_bounds__(256) rs_pattern_kernel(const rs_pattern_desc* 
   }
 }
 
+// ------------------------------------------------- L2 eviction-priority hints
+//
+// Ring staging wants the opposite of plain streaming: the slot a sender just
+// packed should survive in L2 until the receiver unpacks it, while the source
+// and destination shards stream through once.  createpolicy gives 64-bit L2
+// cache policies; .L2::cache_hint loads / stores carry them.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <bool kReadOnly>
+__device__ __forceinline__ uint4 load_hint(const uint4* p, uint64_t pol) {
+  uint4 r;
+  if constexpr (kReadOnly)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void store_hint(uint4* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
+
+// warp_copy_item with L2 policies on the 16 B path (other widths unhinted).
+template <bool kReadOnly, int U>
+__device__ __forceinline__ void warp_copy_item_hint(const rs_copy_desc& D, uint64_t local_item, int lane,
+                                                    uint64_t lpol, uint64_t spol) {
+  if (D.vec_log2 != 4) {
+    warp_copy_item<kReadOnly, U>(D, local_item, lane);
+    return;
+  }
+  const uint64_t r0 = local_item * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  for (uint64_t r = r0; r < r1; ++r) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    const uint4* s = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(D.src) + so);
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<char*>(D.dst) + dof);
+    const uint64_t n = D.row_bytes / 16;
+    uint64_t i = static_cast<uint64_t>(lane);
+    for (; i + 32 * (U - 1) < n; i += 32 * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = load_hint<kReadOnly>(s + i + 32 * u, lpol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) store_hint(d + i + 32 * u, v[u], spol);
+    }
+    for (; i < n; i += 32) store_hint(d + i, load_hint<kReadOnly>(s + i, lpol), spol);
+  }
+}
+
 // ------------------------------------------------------------- exchange
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -662,6 +723,7 @@ __device__ __forceinline__ uint32_t find_frame(const rs_copy_desc* __restrict__ 
 // flags of rs_launch_exchange
 constexpr int kExFaultRx = 1;   // test hook: ring receivers drop out (peer failure)
 constexpr int kExDiscard = 2;   // receivers discard drained slot lines from L2
+constexpr int kExHints = 4;     // L2 policies: shards evict-first, ring slots evict-last
 
 // Block roles: blocks [0, ntx) send lanes_tx[b], [ntx, ntx + nrx) receive
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
@@ -683,6 +745,8 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
     if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
     const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
     const bool peer = (L.flags & RS_LANE_PEER) != 0;
+    const uint64_t pol_first = (flags & kExHints) ? policy_evict_first() : 0;
+    const uint64_t pol_last = (flags & kExHints) ? policy_evict_last() : 0;
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
       const uint32_t slot = b % L.slots;
@@ -707,14 +771,16 @@ __global__ void __launch_bounds__(256) rs_exchange_kernel(
         // (remote stores); one flat item space over the frames, dealt to warps
         for (uint32_t it = warp_in_block; it < B.pack_items; it += warps_per_block) {
           const rs_copy_desc& D = frames[B.pack0 + find_frame(frames + B.pack0, B.npack, it)];
-          warp_copy_item<true, 8>(D, it - D.item0, lane_id);
+          if (flags & kExHints) warp_copy_item_hint<true, 8>(D, it - D.item0, lane_id, pol_first, pol_last);
+          else warp_copy_item<true, 8>(D, it - D.item0, lane_id);
         }
         __syncthreads();
         if (threadIdx.x == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq, peer);
       } else {
         for (uint32_t it = warp_in_block; it < B.unpack_items; it += warps_per_block) {
           const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
-          warp_copy_item<false, 8>(D, it - D.item0, lane_id);
+          if (flags & kExHints) warp_copy_item_hint<false, 8>(D, it - D.item0, lane_id, pol_first, pol_first);
+          else warp_copy_item<false, 8>(D, it - D.item0, lane_id);
         }
         if ((flags & kExDiscard) && B.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
           // every load of the slot has completed (its data was stored); the

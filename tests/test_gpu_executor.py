@@ -288,7 +288,7 @@ def test_searched_placement_bitexact(mode, pair, oracle_c):
     eng.close()
 
 
-@pytest.mark.parametrize("K,cap_kib,discard", [(2, 0, 1), (2, -1, 0), (8, 64, 1), (3, 4, 0)])
+@pytest.mark.parametrize("K,cap_kib,discard", [(2, 0, 1), (2, -1, 2), (8, 64, 5), (3, 4, 4), (2, 0, 0)])
 def test_ring_geometry_variants_bitexact(K, cap_kib, discard, golden, oracle_c):
     """Ring depth K, the slot cap and the L2 discard of drained slots change
     how frames are batched and when slot lines may be dropped -- never the

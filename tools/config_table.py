@@ -58,13 +58,13 @@ def run(case, mode, layers=None):
     rep = eng.run()
     eng.close()
     mean = sum(ms) / len(ms)
-    algo = 2 * (s["total_bytes"] + s["carryover_bytes"])
-    if mode == "staged":  # ring path touches every remote byte 4x (src, slot w, slot r, dst)
-        algo += 2 * s["remote_bytes"]
+    algo = 2 * (s["total_bytes"] + s["carryover_bytes"])  # floor: every moved byte read + written once
+    ring = algo + 2 * s["remote_bytes"]  # STAGED with DRAM-resident rings (slot write + read)
     return {"config": case, "slice_layers": layers, "mode": mode, "plan_GB": round(s["total_bytes"] / 1e9, 2),
             "carry_GB": round(s["carryover_bytes"] / 1e9, 2), "state_GB": round(need / 1e9, 1),
             "ms": round(mean, 3), "reshard_GBps": round(s["total_bytes"] / mean / 1e6, 1),
             "hbm_frac": round(algo / (mean / 1e3) / 1e9 / HBM, 4),
+            "hbm_frac_vs_dram_ring": round(ring / (mean / 1e3) / 1e9 / HBM, 4) if mode == "staged" else None,
             "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad}
 
 

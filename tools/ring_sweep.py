@@ -27,12 +27,13 @@ def main():
     sp, co, cn = specs.sliced_case(case, layers)
     plan = R.compute_transfer_plan(co, cn, sp)
     s = plan.summary()
-    for discard in (1, 2):
+    modes = [int(x) for x in os.environ.get("RS_SWEEP_L2MODES", "0,1,4,5").split(",")]
+    for l2mode in modes:
         for lanes in lanes_list:
             for K in depths:
                 for cap in caps:
                     eng = R.Engine([0], staging_bytes=B, mode="staged", slots_per_link=K, lanes_per_link=lanes,
-                                   ring_slot_kib=cap, ring_discard=discard)
+                                   ring_slot_kib=cap, ring_discard=l2mode)
                     eng.layout(RS_SRC, sp, co)
                     eng.layout(RS_DST, sp, cn)
                     eng.alloc(RS_SRC)
@@ -40,7 +41,7 @@ def main():
                     eng.comm_alloc(plan)
                     eng.fill_pattern(RS_SRC, 42)
                     eng.fill_pattern(RS_DST, 7)
-                    row = {"case": case, "layers": layers, "B_MiB": B >> 20, "discard": discard == 1,
+                    row = {"case": case, "layers": layers, "B_MiB": B >> 20, "l2_discard": bool(l2mode & 1), "l2_hints": bool(l2mode & 4),
                            "lanes": lanes, "K": K, "slot_cap_KiB": cap}
                     try:
                         eng.prepare(plan)
