@@ -203,6 +203,70 @@ def reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def xfer_one_gpu(args) -> None:
+    """--mode xfer at N=1: the NCCL send/recv comparator on one B200.  Every
+    rank gets its own virtual device slot (one RS_MODE_XFER engine each), so
+    every cross-rank chunk is packed by our kernel, moved by ncclSend/ncclRecv
+    (NCCL's self-loop on a single-rank communicator, libnccl called directly)
+    and unpacked by our kernel, round by round on the engine's chunk schedule
+    and budget B -- the paper's executor shape.  The step is
+    host-driven (NCCL group per round, stream syncs), so it is timed by the
+    host clock around fully synchronised steps."""
+    import torch
+    from paper_2605_22014_b200 import reshard as R
+    from paper_2605_22014_b200 import xfer
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+
+    torch.cuda.set_device(0)
+    sp, co, cn, desc = workload(1, args.profile_layers)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    summ = plan.summary()
+    total = summ["total_bytes"]
+    nslots = max(max(co.ranks), max(cn.ranks)) + 1
+    nccl = xfer.Nccl(0)
+    engs = []
+    for s in range(nslots):
+        e = R.Engine([0], staging_bytes=args.staging_bytes, mode="xfer", world_slots=nslots, first_local_slot=s)
+        e.layout(RS_SRC, sp, co, list(co.ranks))
+        e.layout(RS_DST, sp, cn, list(cn.ranks))
+        e.alloc(RS_SRC)
+        e.alloc(RS_DST)
+        e.fill_pattern(RS_SRC, SEED)
+        engs.append(e)
+    for e in engs:
+        e.prepare(plan)
+    for _ in range(args.warmup):
+        xfer.run_local_slots(engs, nccl, 0)
+    with ClockSampler(0) as clk:
+        infos = [xfer.run_local_slots(engs, nccl, 0) for _ in range(args.steps)]
+    bad = sum(e.verify_pattern(RS_DST, SEED)[0] for e in engs)
+    step_ms = statistics.mean(i["seconds"] for i in infos) * 1e3
+    pk = peaks()
+    algo = 2 * (total + summ["carryover_bytes"])
+    achieved = algo / (step_ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+            "handoff_ms": round(step_ms, 4), "higher_is_better": HIGH_IS_GOOD, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: reference pattern state (shard_store.cpp:51-85)",
+            "config": {"workload": desc + " -- NCCL comparator: one virtual slot per rank",
+                       "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"], "mode": "xfer",
+                       "transport": f"ncclSend/ncclRecv self-loop, NCCL {nccl.version}",
+                       "staging_bytes": args.staging_bytes, "rounds": infos[0]["rounds"],
+                       "links": infos[0]["links"], "bytes_through_nccl": infos[0]["bytes_sent"],
+                       "timing": "host clock around synchronised steps (host-driven rounds)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+                         "kernel": "rs_copy_kernel pack/unpack + NCCL copy",
+                         "algorithmic_bytes_per_launch": algo, "peak_source": pk["source"]},
+            "clocks": clk.summary(), "gpu_launches": None,
+            "correct": {"dst_pattern_mismatches": int(bad)}}
+    print(json.dumps(line), flush=True)
+    for e in engs:
+        e.close()
+    nccl.close()
+
+
 def ours(args) -> None:
     """N=1: every logical rank on cuda:0.  N>1 (torchrun, one process per GPU):
     rank id r of both configs lives on GPU r*N//8 (iota placement at N=8);
@@ -457,6 +521,8 @@ def main() -> None:
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+    elif args.mode == "xfer" and dist_env()[1] == 1 and not os.environ.get("RS_BENCH_SAME_DEVICE"):
+        xfer_one_gpu(args)
     else:
         ours(args)
 
