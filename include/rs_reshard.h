@@ -108,6 +108,8 @@ typedef struct {
 #define RS_COPY_LDG16 6    /* warp engine, 16 loads in flight per lane */
 #define RS_COPY_CTA8 7     /* CTA-cooperative items (rows dealt to the CTA's warps), 8 loads/lane */
 #define RS_COPY_BULK_MW 8  /* TMA bulk rings, 4 independent issuer warps per SM */
+#define RS_COPY_CE 16      /* comparator: copy engines (one cudaMemcpy2DAsync per descriptor row
+                              plane), no kernel of ours -- DIRECT mode only */
 
 typedef struct {
   int32_t ok;

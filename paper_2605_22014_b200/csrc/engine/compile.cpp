@@ -58,7 +58,7 @@ std::uint64_t bytes_of(const rs_copy_desc& d) { return d.rows * d.row_bytes; }
 void append_copy(std::vector<rs_copy_desc>& out, std::uint64_t src_base,
                  const reshard::ShardView& src_owner, std::uint64_t dst_base,
                  const reshard::ShardView& dst_owner, const reshard::ShardView& region,
-                 std::int64_t elem_bytes, std::uint32_t tag) {
+                 std::int64_t elem_bytes, std::uint32_t tag, bool cut_runs) {
   const std::size_t nd = region.ndims();
   // element strides of both owners and the region origin offsets
   std::vector<std::int64_t> ss(nd), ds(nd);
@@ -106,7 +106,7 @@ void append_copy(std::vector<rs_copy_desc>& out, std::uint64_t src_base,
   }
 
   // cut long runs into sub-rows (one extra innermost outer axis) + tail
-  if (run > 2 * kSubRowBytes && outer.size() < RS_MAX_OUTER) {
+  if (cut_runs && run > 2 * kSubRowBytes && outer.size() < RS_MAX_OUTER) {
     const std::uint64_t nsub = run / kSubRowBytes;
     const std::uint64_t tail = run - nsub * kSubRowBytes;
     std::vector<Dim> o2;

@@ -19,7 +19,7 @@ constexpr std::uint64_t kSubRowBytes = 8192;
 void append_copy(std::vector<rs_copy_desc>& out, std::uint64_t src_base,
                  const reshard::ShardView& src_owner, std::uint64_t dst_base,
                  const reshard::ShardView& dst_owner, const reshard::ShardView& region,
-                 std::int64_t elem_bytes, std::uint32_t tag);
+                 std::int64_t elem_bytes, std::uint32_t tag, bool cut_runs = true);
 
 // Assign work items (rows_per_item from item_bytes) and return item0 prefix
 // sums for descs[first..]; returns the total item count after the range.

@@ -644,7 +644,7 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
     const int l = local_of(se->slot);
     if (l < 0) return;  // the source's process pushes it
     append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
-                addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
+                addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
   };
 
   for (int layer : plan_layers_) {
@@ -1063,6 +1063,42 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   }
 }
 
+// RS_COPY_CE comparator: every descriptor whose items fall in [b, e) as
+// cudaMemcpy2DAsync planes (innermost outer dim = rows; further outer dims
+// loop on the host).  Returns the number of copy calls.
+int Engine::ce_copies(const std::vector<rs_copy_desc>& descs, std::uint64_t b, std::uint64_t e,
+                      cudaStream_t stream) {
+  int calls = 0;
+  for (const auto& D : descs) {
+    if (D.item0 < b || D.item0 >= e) continue;
+    if (D.nouter == 0) {
+      cuda_check(cudaMemcpyAsync(reinterpret_cast<void*>(D.dst), reinterpret_cast<const void*>(D.src), D.row_bytes,
+                                 cudaMemcpyDefault, stream),
+                 "ce copy");
+      ++calls;
+      continue;
+    }
+    std::uint64_t planes = 1;
+    for (std::uint32_t k = 1; k < D.nouter; ++k) planes *= D.ext[k];
+    for (std::uint64_t pl = 0; pl < planes; ++pl) {
+      std::int64_t so = 0, dof = 0;
+      std::uint64_t r = pl;
+      for (std::uint32_t k = 1; k < D.nouter; ++k) {
+        const std::uint64_t i = r % D.ext[k];
+        r /= D.ext[k];
+        so += static_cast<std::int64_t>(i) * D.sstr[k];
+        dof += static_cast<std::int64_t>(i) * D.dstr[k];
+      }
+      cuda_check(cudaMemcpy2DAsync(reinterpret_cast<void*>(D.dst + dof), static_cast<std::size_t>(D.dstr[0]),
+                                   reinterpret_cast<const void*>(D.src + so), static_cast<std::size_t>(D.sstr[0]),
+                                   D.row_bytes, D.ext[0], cudaMemcpyDefault, stream),
+                 "ce copy 2d");
+      ++calls;
+    }
+  }
+  return calls;
+}
+
 void Engine::upload_programs() {
   for (std::size_t d = 0; d < devices_.size(); ++d) {
     DeviceProgram& p = programs_[d];
@@ -1137,6 +1173,10 @@ rs_exec_report Engine::run() {
     DeviceProgram& p = programs_[d];
     if (e <= b) return;
     DeviceGuard g(devices_[d].ordinal);
+    if (opts_.copy_kernel == RS_COPY_CE) {  // comparator: the DMA copy engines, one call per 2-D plane
+      launches += ce_copies(p.local, b, e, devices_[d].stream);
+      return;
+    }
     cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                               reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
                               static_cast<std::uint32_t>(p.local.size()), b, e, copy_grid(static_cast<int>(d)),

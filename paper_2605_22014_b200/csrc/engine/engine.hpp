@@ -200,6 +200,7 @@ class Engine {
   };
   CommLayout make_comm_layout(const std::map<int, std::uint64_t>* ring_bytes) const;
   void alloc_comm_arenas();
+  int ce_copies(const std::vector<rs_copy_desc>& descs, std::uint64_t b, std::uint64_t e, cudaStream_t stream);
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
   int copy_variant(int dev) const;

@@ -1,5 +1,6 @@
 """Every copy-engine variant is bit-exact (GPU): LDG x4/x8/x16, CTA-cooperative,
-evict-first stores, TMA bulk single-issuer and multi-issuer rings."""
+evict-first stores, TMA bulk single-issuer and multi-issuer rings, and the
+copy-engine comparator (RS_COPY_CE, cudaMemcpy2DAsync planes)."""
 import pytest
 
 from paper_2605_22014_b200 import reshard as R
@@ -16,7 +17,7 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("copy_kernel", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+@pytest.mark.parametrize("copy_kernel", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 16])
 @pytest.mark.parametrize("case", ["c1", "mini"])
 def test_copy_variant_bitexact(copy_kernel, case):
     if case == "c1":
