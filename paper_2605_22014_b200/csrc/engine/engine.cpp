@@ -463,8 +463,12 @@ int Engine::copy_grid(int dev) const {
   switch (copy_variant(dev)) {
     case 2:
     case 5: {
+      // 3 CTAs (24 warps) per SM at full size; a launch of a few GB is
+      // ramp-dominated and runs faster with 4 (profiles/r1/item_sweep*.jsonl)
+      const std::uint64_t lb = programs_.empty() ? 0 : programs_[static_cast<std::size_t>(dev)].launch_bytes;
+      const int dflt = lb && lb < (4ull << 30) ? 4 : 3;
       int per_sm = std::max(1, rs_kernel_max_blocks_per_sm(3));
-      per_sm = std::min(per_sm, opts_.blocks_per_sm > 0 ? opts_.blocks_per_sm : 3);
+      per_sm = std::min(per_sm, opts_.blocks_per_sm > 0 ? opts_.blocks_per_sm : dflt);
       return d.sms * per_sm;
     }
     case 3:
@@ -1110,6 +1114,18 @@ void Engine::upload_programs() {
       p.all_aligned = p.all_aligned && c.vec_log2 == 4;
     }
     p.local_bytes = bytes;
+    // bytes one launch moves: everything (fused), or the largest layer (strict
+    // per-layer launches, where the last items of every layer form a tail)
+    p.launch_bytes = bytes;
+    if (opts_.strict_layers) {
+      p.launch_bytes = 0;
+      for (const auto& lr : p.layers) {
+        std::uint64_t lb = 0;
+        for (std::size_t i = static_cast<std::size_t>(lr.item_begin); i < static_cast<std::size_t>(lr.item_end); ++i)
+          lb += bytes_of(p.local[i]);
+        p.launch_bytes = std::max(p.launch_bytes, lb);
+      }
+    }
     std::uint64_t item_bytes = static_cast<std::uint64_t>(opts_.item_bytes);
     if (item_bytes == 0) {
       const int variant = copy_variant(static_cast<int>(d));
@@ -1118,10 +1134,12 @@ void Engine::upload_programs() {
       } else if (variant >= 8) {  // 4..16 bulk issuers per SM
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 32 + 1), 32768, 1u << 20);
       } else {
-        // 256 KB items (full-size sweep optimum); smaller when the work is small so
-        // every warp still gets ~8 items
+        // 64-256 KB items are equivalent at full size (item_sweep_c2.jsonl);
+        // smaller when a launch is small so every warp still gets ~64 items
+        // and the last items do not form a tail (C1 0.80 -> 0.67 ms, strict
+        // per-layer C2 34.6 -> 30.9 ms, item_sweep_c1_strict.jsonl)
         const std::uint64_t warps = static_cast<std::uint64_t>(copy_grid(static_cast<int>(d))) * 8;
-        item_bytes = std::clamp<std::uint64_t>(bytes / (warps * 8 + 1), 16384, 256u << 10);
+        item_bytes = std::clamp<std::uint64_t>(p.launch_bytes / (warps * 64 + 1), 16384, 256u << 10);
       }
     }
     std::uint64_t item = 0;

@@ -108,6 +108,7 @@ struct DeviceProgram {
   DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error;
   std::uint64_t local_bytes = 0;
   bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
+  std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)
 };
 
 struct Device {
