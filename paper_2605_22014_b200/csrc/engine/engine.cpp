@@ -158,6 +158,13 @@ std::int64_t Store::total_bytes() const {
 Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.num_devices < 1 || !opts.device_ids) throw DomainError("engine: no devices");
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
+  for (int i = 0; i < opts.num_devices; ++i)
+    for (int j = 0; j < i; ++j)
+      if (opts.device_ids[i] == opts.device_ids[j])
+        // two slots of one process on one GPU would run two launches whose ring
+        // lanes wait on each other without being co-resident
+        throw DomainError("engine: device " + std::to_string(opts.device_ids[i]) +
+                          " listed twice; one slot per GPU per process (several processes may share a GPU)");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
     throw DomainError("engine: unknown mode");
   if (opts_.slots_per_link == 0) opts_.slots_per_link = 2;  // ring depth default (profiles/r1/ring_sweep_v3.jsonl)

@@ -52,3 +52,12 @@ def test_include_dir_has_only_boundary_headers():
     r = subprocess.run(["gcc", "-std=c99", "-fsyntax-only", "-x", "c", os.path.join(inc, "rs_reshard.h")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_engine_rejects_duplicate_devices_before_touching_cuda():
+    """Two slots of one process on one GPU could deadlock STAGED rings; the
+    engine refuses the option struct (checked before any CUDA call)."""
+    from paper_2605_22014_b200 import reshard as R
+    import pytest
+    with pytest.raises(N.DomainError, match="listed twice"):
+        R.Engine([0, 0])
