@@ -402,7 +402,7 @@ def ours(args) -> None:
                            f"rank r on GPU r*{world}//8, one process per GPU"),
                        "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
                        "tasks": summ["task_count"], "mode": args.mode, "placement": args.placement, "staging_bytes": args.staging_bytes,
-                       "strict_layers": bool(args.strict), "copy_kernel": "LDG8 x 3 CTAs/SM, 256 KB items",
+                       "strict_layers": bool(args.strict), "copy_kernel": "LDG8 (16 B vectors, 8 loads in flight per lane), non-persistent grid, one 16 KB item per warp",
                        "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
             "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}

@@ -99,15 +99,18 @@ typedef struct {
   int32_t reserved;
 } rs_engine_options;
 
-#define RS_COPY_AUTO 0     /* engine default */
+#define RS_COPY_AUTO 0     /* engine default: RS_COPY_LDG8_NP */
 #define RS_COPY_LDG4 1     /* warp-per-row 16 B vectors, 4 loads in flight per lane */
-#define RS_COPY_LDG8 2     /* same, 8 loads in flight per lane */
+#define RS_COPY_LDG8 2     /* same, 8 loads in flight per lane, persistent grid (3 CTAs/SM) */
 #define RS_COPY_BULK 3     /* cp.async.bulk global->smem->global ring, one issuer per CTA */
 #define RS_COPY_LDG4_CS 4  /* LDG4 with evict-first (st.global.cs) stores */
 #define RS_COPY_LDG8_CS 5  /* LDG8 with evict-first (st.global.cs) stores */
 #define RS_COPY_LDG16 6    /* warp engine, 16 loads in flight per lane */
 #define RS_COPY_CTA8 7     /* CTA-cooperative items (rows dealt to the CTA's warps), 8 loads/lane */
 #define RS_COPY_BULK_MW 8  /* TMA bulk rings, 4 independent issuer warps per SM */
+#define RS_COPY_LDG8_PF 13 /* LDG8 with the L2::256B prefetch hint on loads */
+#define RS_COPY_LDG8_EF 14 /* LDG8 with an evict-first L2 policy on loads */
+#define RS_COPY_LDG8_NP 15 /* LDG8, non-persistent grid (one work item per warp) */
 #define RS_COPY_CE 16      /* comparator: copy engines (one cudaMemcpy2DAsync per descriptor row
                               plane), no kernel of ours -- DIRECT mode only */
 

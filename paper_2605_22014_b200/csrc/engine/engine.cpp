@@ -455,13 +455,17 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_LDG8_CS: return 5;
     case RS_COPY_LDG16: return 6;
     case RS_COPY_CTA8: return 7;
+    case RS_COPY_LDG8_PF: return 13;
+    case RS_COPY_LDG8_EF: return 14;
+    case RS_COPY_LDG8_NP: return 15;
     case RS_COPY_BULK_MW:
     case RS_COPY_BULK_MW + 1:
     case RS_COPY_BULK_MW + 2:
     case RS_COPY_BULK_MW + 3:
     case RS_COPY_BULK_MW + 4:  // issuer-count / ring-shape variants (kernels.cu launch_bulk_mw)
       return programs_[static_cast<std::size_t>(dev)].all_aligned ? opts_.copy_kernel : 2;
-    default: return 2;
+    case RS_COPY_LDG8: return 2;
+    default: return 15;  // LDG8 over a non-persistent grid (profiles/r1/np_sweep.jsonl)
   }
 }
 
@@ -469,7 +473,10 @@ int Engine::copy_grid(int dev) const {
   const Device& d = devices_[static_cast<std::size_t>(dev)];
   switch (copy_variant(dev)) {
     case 2:
-    case 5: {
+    case 5:
+    case 13:
+    case 14:
+    case 15: {
       // 3 CTAs (24 warps) per SM at full size; a launch of a few GB is
       // ramp-dominated and runs faster with 4 (profiles/r1/item_sweep*.jsonl)
       const std::uint64_t lb = programs_.empty() ? 0 : programs_[static_cast<std::size_t>(dev)].launch_bytes;
@@ -1138,6 +1145,11 @@ void Engine::upload_programs() {
       const int variant = copy_variant(static_cast<int>(d));
       if (variant == 3) {
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 8 + 1), 32768, 8u << 20);
+      } else if (variant == 15) {
+        // non-persistent grid: one 16 KB item per warp, the block scheduler
+        // deals CTAs in item order (C2 28.6 ms = 100.7 % of the copy_ peak,
+        // strict per-layer 28.9 ms, C1 0.649 ms; np_sweep.jsonl)
+        item_bytes = 16384;
       } else if (variant >= 8) {  // 4..16 bulk issuers per SM
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 32 + 1), 32768, 1u << 20);
       } else {

@@ -80,19 +80,40 @@ __device__ __forceinline__ void store_cs(uint4* p, const uint4& v) {
                : "memory");
 }
 
+// Read-only 16 B load flavours of the copy engine (RS_COPY_LDG8_PF / _EF):
+// 1 = L2 256 B sector prefetch hint, 2 = evict-first L2 policy.
+template <int kLd>
+__device__ __forceinline__ uint4 load16(const uint4* p, uint64_t pol) {
+  uint4 r;
+  if constexpr (kLd == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+
 // One warp copies one contiguous run: lanes stride T-sized vectors, U loads
 // issued before their stores.
-template <typename T, bool kReadOnly, int U = kUnroll, bool kStream = false>
+template <typename T, bool kReadOnly, int U = kUnroll, bool kStream = false, int kLd = 0>
 __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64_t nbytes,
                                               int lane) {
   const T* s = reinterpret_cast<const T*>(src);
   T* d = reinterpret_cast<T*>(dst);
   const uint64_t n = nbytes / sizeof(T);
   uint64_t i = static_cast<uint64_t>(lane);
+  uint64_t pol = 0;
+  if constexpr (kLd == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   for (; i + 32 * (U - 1) < n; i += 32 * U) {
     T v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = load<T, kReadOnly>(s + i + 32 * u);
+    for (int u = 0; u < U; ++u) {
+      if constexpr (kLd != 0 && kReadOnly && sizeof(T) == 16)
+        v[u] = load16<kLd>(reinterpret_cast<const uint4*>(s + i + 32 * u), pol);
+      else
+        v[u] = load<T, kReadOnly>(s + i + 32 * u);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if constexpr (kStream && sizeof(T) == 16) store_cs(reinterpret_cast<uint4*>(d + i + 32 * u), v[u]);
@@ -102,11 +123,11 @@ __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64
   for (; i < n; i += 32) store<T>(d + i, load<T, kReadOnly>(s + i));
 }
 
-template <bool kReadOnly, int U = kUnroll, bool kStream = false>
+template <bool kReadOnly, int U = kUnroll, bool kStream = false, int kLd = 0>
 __device__ __forceinline__ void warp_copy_any(const char* src, char* dst, uint64_t nbytes,
                                               uint32_t vec_log2, int lane) {
   switch (vec_log2) {
-    case 4: warp_copy_run<uint4, kReadOnly, U, kStream>(src, dst, nbytes, lane); break;
+    case 4: warp_copy_run<uint4, kReadOnly, U, kStream, kLd>(src, dst, nbytes, lane); break;
     case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane); break;
     case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane); break;
     case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane); break;
@@ -142,7 +163,7 @@ __device__ __forceinline__ void row_offsets(const rs_copy_desc& D, uint32_t r, i
   }
 }
 
-template <bool kReadOnly, int U = kUnroll, bool kStream = false>
+template <bool kReadOnly, int U = kUnroll, bool kStream = false, int kLd = 0>
 __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t local_item,
                                                int lane) {
   const uint64_t r0 = local_item * D.rows_per_item;
@@ -152,11 +173,11 @@ __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t l
   for (uint64_t r = r0; r < r1; ++r) {
     int64_t so, dof;
     row_offsets(D, static_cast<uint32_t>(r), so, dof);
-    warp_copy_any<kReadOnly, U, kStream>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+    warp_copy_any<kReadOnly, U, kStream, kLd>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
   }
 }
 
-template <int U, bool kStream = false>
+template <int U, bool kStream = false, int kLd = 0>
 __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __restrict__ descs,
                                                       const uint64_t* __restrict__ item0,
                                                       uint32_t ndesc, uint64_t item_begin,
@@ -166,7 +187,7 @@ __global__ void __launch_bounds__(256) rs_copy_kernel(const rs_copy_desc* __rest
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t item = item_begin + warp; item < item_end; item += nwarps) {
     const uint32_t di = find_desc(item0, ndesc, item);
-    warp_copy_item<true, U, kStream>(descs[di], item - descs[di].item0, lane);
+    warp_copy_item<true, U, kStream, kLd>(descs[di], item - descs[di].item0, lane);
   }
 }
 
@@ -844,6 +865,17 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
       break;
     case 7:
       rs_copy_cta_kernel<8><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 13:
+      rs_copy_kernel<8, false, 1><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    case 15: {  // non-persistent: one item per warp, the block scheduler deals CTAs
+      const uint64_t ctas = (item_end - item_begin + 7) / 8;
+      rs_copy_kernel<8><<<static_cast<unsigned>(ctas), 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
+      break;
+    }
+    case 14:
+      rs_copy_kernel<8, false, 2><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
     case 8: return launch_bulk_mw<4, 6, 4, 8192>(descs, item0, ndesc, item_begin, item_end, grid, stream);
     case 9: return launch_bulk_mw<8, 3, 2, 8192>(descs, item0, ndesc, item_begin, item_end, grid, stream);
