@@ -63,38 +63,38 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        nvml = None
-        try:  # NVML: a sample costs microseconds, so short timed regions still get many
+        self._nvml = None
+        try:  # NVML (initialised before the timed region): a sample costs microseconds
             import pynvml as nvml
             nvml.nvmlInit()
-            h = nvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = nvml.nvmlDeviceGetMaxClockInfo(h, nvml.NVML_CLOCK_SM)
-            bits = [(0x8, "Active"), (0x40, "Active"), (0x20, "Active"), (0x4, "Active")]
+            self._h = nvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = nvml.nvmlDeviceGetMaxClockInfo(self._h, nvml.NVML_CLOCK_SM)
+            self._nvml = nvml
         except Exception:
-            nvml = None
+            self._nvml = None
+
+    def _sample(self):
+        nvml = self._nvml
+        if nvml is not None:
+            sm = nvml.nvmlDeviceGetClockInfo(self._h, nvml.NVML_CLOCK_SM)
+            r = nvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            # hw_slowdown 0x8, hw_thermal 0x40, sw_thermal 0x20, sw_power_cap 0x4
+            self.rows.append([str(self.index), str(sm), str(self._max)] +
+                             ["Active" if r & b else "Not Active" for b in (0x8, 0x40, 0x20, 0x4)])
+            return
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        if out:
+            self.rows.append([x.strip() for x in out.split(",")])
+
+    def _run(self):
         while not self._stop.is_set():
             try:
-                if nvml is not None:
-                    sm = nvml.nvmlDeviceGetClockInfo(h, nvml.NVML_CLOCK_SM)
-                    r = nvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.rows.append([str(self.index), str(sm), str(mx)] +
-                                     ["Active" if r & b else "Not Active" for b, _ in bits])
-                else:
-                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.02 if nvml is not None else 0.2)
-        if nvml is not None:
-            try:
-                nvml.nvmlShutdown()
-            except Exception:
-                pass
+            self._stop.wait(0.01 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -103,6 +103,11 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nvml is not None:
+            try:
+                self._nvml.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self) -> dict:
         if not self.rows:
