@@ -96,7 +96,7 @@ typedef struct {
                                flags 1 = receivers drop drained slot lines (discard.global.L2,
                                no write-back), 4 = L2 policies (shards evict-first, slots
                                evict-last); 2 = neither */
-  int32_t reserved;
+  int32_t ring_cta_threads; /* STAGED: threads per ring-lane CTA, 256 / 512 / 1024 (0: default) */
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default: RS_COPY_LDG8_NP */

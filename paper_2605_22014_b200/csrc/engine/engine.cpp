@@ -167,6 +167,9 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
                           " listed twice; one slot per GPU per process (several processes may share a GPU)");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
     throw DomainError("engine: unknown mode");
+  if (opts_.ring_cta_threads == 0) opts_.ring_cta_threads = 256;
+  if (opts_.ring_cta_threads != 256 && opts_.ring_cta_threads != 512 && opts_.ring_cta_threads != 1024)
+    throw DomainError("engine: ring_cta_threads must be 256, 512 or 1024");
   if (opts_.slots_per_link == 0) opts_.slots_per_link = 2;  // ring depth default (profiles/r1/ring_sweep_v3.jsonl)
   if (opts_.slots_per_link < 2) opts_.slots_per_link = 2;
   if (opts_.lanes_per_link < 0) opts_.lanes_per_link = 0;  // 0: automatic (compile_staged)
@@ -759,7 +762,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
       slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
     }
-    const int capacity = grid_for(0, 2) * 3 / 4;
+    const int capacity = grid_for(0, exchange_kernel_id()) * 3 / 4;
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
     const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
     std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
@@ -1243,7 +1246,7 @@ rs_exec_report Engine::run() {
     epoch_ += 1ull << 32;
     for (std::size_t d = 0; d < devices_.size(); ++d) {
       DeviceProgram& p = programs_[d];
-      const int cap = grid_for(static_cast<int>(d), 2);
+      const int cap = grid_for(static_cast<int>(d), exchange_kernel_id());
       if (p.ntx + p.nrx >= cap)
         throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) +
                           " ring lanes exceed the co-resident CTA capacity " + std::to_string(cap) +
@@ -1264,7 +1267,7 @@ rs_exec_report Engine::run() {
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
                                     (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0),
-                                    cap - p.ntx - p.nrx, devices_[d].stream),
+                                    cap - p.ntx - p.nrx, opts_.ring_cta_threads, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }

@@ -204,6 +204,7 @@ class Engine {
   int ce_copies(const std::vector<rs_copy_desc>& descs, std::uint64_t b, std::uint64_t e, cudaStream_t stream);
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
+  int exchange_kernel_id() const { return opts_.ring_cta_threads == 1024 ? 8 : opts_.ring_cta_threads == 512 ? 7 : 2; }
   int copy_variant(int dev) const;
   int copy_grid(int dev) const;
   void check_laid_out() const;

@@ -750,7 +750,8 @@ constexpr int kExHints = 4;     // L2 policies: shards evict-first, ring slots e
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
 // never exceeds the co-resident CTA capacity, so every waiting role has its
 // counterpart running (same device) or launched on its own device (peers).
-__global__ void __launch_bounds__(256) rs_exchange_kernel(
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
     const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
@@ -916,12 +917,17 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
                                unsigned int* error_flag, uint64_t spin_limit, int flags,
-                               int local_blocks, cudaStream_t stream) {
+                               int local_blocks, int threads, cudaStream_t stream) {
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
-  rs_exchange_kernel<<<grid, 256, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,
-                                               local_item0, nlocal, local_items, epoch, error_flag, spin_limit,
-                                               flags);
+#define RS_EXCHANGE_LAUNCH(T)                                                                              \
+  rs_exchange_kernel<T><<<grid, T, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
+                                                local_item0, nlocal, local_items, epoch, error_flag, spin_limit, \
+                                                flags)
+  if (threads == 1024) RS_EXCHANGE_LAUNCH(1024);
+  else if (threads == 512) RS_EXCHANGE_LAUNCH(512);
+  else RS_EXCHANGE_LAUNCH(256);
+#undef RS_EXCHANGE_LAUNCH
   return cudaGetLastError();
 }
 
@@ -933,7 +939,9 @@ int rs_kernel_max_blocks_per_sm(int which) {
   else if (which == 6) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_cta_kernel<8>, 256, 0);
   else if (which == 4) n = 1;  // bulk ring: one CTA (one issuer, ~200 KB smem) per SM
   else if (which == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_pattern_kernel<false>, 256, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel, 256, 0);
+  else if (which == 7) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512>, 512, 0);
+  else if (which == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<1024>, 1024, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256>, 256, 0);
   return n;
 }
 

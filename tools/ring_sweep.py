@@ -24,16 +24,17 @@ def main():
     caps = [int(c) for c in os.environ.get("RS_SWEEP_CAPS", "32,64,128,256,512,1024,-1").split(",")]
     depths = [int(k) for k in os.environ.get("RS_SWEEP_K", "2,4").split(",")]
     lanes_list = [int(x) for x in os.environ.get("RS_SWEEP_LANES", "0").split(",")]
+    threads_list = [int(x) for x in os.environ.get("RS_SWEEP_THREADS", "256").split(",")]
     sp, co, cn = specs.sliced_case(case, layers)
     plan = R.compute_transfer_plan(co, cn, sp)
     s = plan.summary()
     modes = [int(x) for x in os.environ.get("RS_SWEEP_L2MODES", "0,1,4,5").split(",")]
-    for l2mode in modes:
+    for l2mode, threads in [(m, t) for m in modes for t in threads_list]:
         for lanes in lanes_list:
             for K in depths:
                 for cap in caps:
                     eng = R.Engine([0], staging_bytes=B, mode="staged", slots_per_link=K, lanes_per_link=lanes,
-                                   ring_slot_kib=cap, ring_discard=l2mode)
+                                   ring_slot_kib=cap, ring_discard=l2mode, ring_cta_threads=threads)
                     eng.layout(RS_SRC, sp, co)
                     eng.layout(RS_DST, sp, cn)
                     eng.alloc(RS_SRC)
@@ -42,7 +43,7 @@ def main():
                     eng.fill_pattern(RS_SRC, 42)
                     eng.fill_pattern(RS_DST, 7)
                     row = {"case": case, "layers": layers, "B_MiB": B >> 20, "l2_discard": bool(l2mode & 1), "l2_hints": bool(l2mode & 4),
-                           "lanes": lanes, "K": K, "slot_cap_KiB": cap}
+                           "lanes": lanes, "K": K, "cta_threads": threads, "slot_cap_KiB": cap}
                     try:
                         eng.prepare(plan)
                         eng.run()
