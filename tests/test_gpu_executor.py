@@ -335,3 +335,17 @@ def test_plan_sized_staging_arena():
     rep = R.execute_plan(plan, eng)
     assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("threads", [512, 1024])
+def test_wide_ring_lanes_bitexact(threads, golden, oracle_c):
+    """512 / 1024-thread ring-lane CTAs (fewer, wider lanes): same bytes as the
+    reference's execute_plan on 30 random pairs."""
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(30, golden["random_pairs"]["base_seed"]):
+        eng = make_engine(sp, co, cn, "staged", 1 << 16, lanes_per_link=1, ring_cta_threads=threads)
+        rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+        assert rep["ok"], (seed, rep)
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            rows[seed]["exec"]["4096"]["dst_sha"], seed
+        eng.close()
