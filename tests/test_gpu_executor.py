@@ -349,3 +349,20 @@ def test_wide_ring_lanes_bitexact(threads, golden, oracle_c):
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
             rows[seed]["exec"]["4096"]["dst_sha"], seed
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_identity_resize_is_all_carryover(mode, oracle_c):
+    """Same layout, new generation: the plan is carryovers only (no tasks,
+    no rings); the destination store still receives every byte."""
+    sp = mini_llama(2)
+    co, cn = specs.iota_config(1, 2, 2, 1), specs.iota_config(2, 2, 2, 1)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    s = plan.summary()
+    assert s["task_count"] == 0 and s["carryover_bytes"] > 0
+    eng = make_engine(sp, co, cn, mode, 1 << 20)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["bytes_moved"] == 0 and rep["carryover_bytes"] == s["carryover_bytes"]
+    assert rep["peak_staging_bytes"] == 0
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
