@@ -111,6 +111,8 @@ typedef struct {
 #define RS_COPY_LDG8_PF 13 /* LDG8 with the L2::256B prefetch hint on loads */
 #define RS_COPY_LDG8_EF 14 /* LDG8 with an evict-first L2 policy on loads */
 #define RS_COPY_LDG8_NP 15 /* LDG8, non-persistent grid (one work item per warp) */
+#define RS_COPY_TMA_NP 17  /* TMA bulk copy (cp.async.bulk), one 1-warp CTA per 16 KB item, non-persistent */
+#define RS_COPY_TMA_NP32 18 /* same with 32 KB items */
 #define RS_COPY_CE 16      /* comparator: copy engines (one cudaMemcpy2DAsync per descriptor row
                               plane), no kernel of ours -- DIRECT mode only */
 

@@ -461,6 +461,10 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_LDG8_PF: return 13;
     case RS_COPY_LDG8_EF: return 14;
     case RS_COPY_LDG8_NP: return 15;
+    case RS_COPY_TMA_NP: return programs_[static_cast<std::size_t>(dev)].max_row_bytes <= 16384 &&
+                                        programs_[static_cast<std::size_t>(dev)].all_aligned ? 17 : 15;
+    case RS_COPY_TMA_NP32: return programs_[static_cast<std::size_t>(dev)].max_row_bytes <= 32768 &&
+                                          programs_[static_cast<std::size_t>(dev)].all_aligned ? 18 : 15;
     case RS_COPY_BULK_MW:
     case RS_COPY_BULK_MW + 1:
     case RS_COPY_BULK_MW + 2:
@@ -468,7 +472,13 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_BULK_MW + 4:  // issuer-count / ring-shape variants (kernels.cu launch_bulk_mw)
       return programs_[static_cast<std::size_t>(dev)].all_aligned ? opts_.copy_kernel : 2;
     case RS_COPY_LDG8: return 2;
-    default: return 15;  // LDG8 over a non-persistent grid (profiles/r1/np_sweep.jsonl)
+    // default: TMA bulk copy over a non-persistent grid when every descriptor is
+    // 16 B aligned with rows <= 16 KB (all BASELINE plans), else LDG8 over a
+    // non-persistent grid (profiles/r1/tma_np_sweep.jsonl, np_sweep.jsonl)
+    default: {
+      const DeviceProgram& p = programs_[static_cast<std::size_t>(dev)];
+      return p.all_aligned && p.max_row_bytes <= 16384 ? 17 : 15;
+    }
   }
 }
 
@@ -1126,9 +1136,11 @@ void Engine::upload_programs() {
     const Device& dv = devices_[d];
     std::uint64_t bytes = 0;
     p.all_aligned = true;
+    p.max_row_bytes = 0;
     for (const auto& c : p.local) {
       bytes += bytes_of(c);
       p.all_aligned = p.all_aligned && c.vec_log2 == 4;
+      p.max_row_bytes = std::max<std::uint64_t>(p.max_row_bytes, c.row_bytes);
     }
     p.local_bytes = bytes;
     // bytes one launch moves: everything (fused), or the largest layer (strict
@@ -1148,7 +1160,9 @@ void Engine::upload_programs() {
       const int variant = copy_variant(static_cast<int>(d));
       if (variant == 3) {
         item_bytes = std::clamp<std::uint64_t>(bytes / (static_cast<std::uint64_t>(dv.sms) * 8 + 1), 32768, 8u << 20);
-      } else if (variant == 15) {
+      } else if (variant == 18) {
+        item_bytes = 32768;
+      } else if (variant == 15 || variant == 17) {
         // non-persistent grid: one 16 KB item per warp, the block scheduler
         // deals CTAs in item order (C2 28.6 ms = 100.7 % of the copy_ peak,
         // strict per-layer 28.9 ms, C1 0.649 ms; np_sweep.jsonl)

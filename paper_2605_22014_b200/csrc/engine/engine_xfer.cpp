@@ -267,11 +267,12 @@ void Engine::xfer_step(int what, int round) {
   } else {
     if (round < 0 || round >= xfer_rounds_) throw DomainError("xfer: round out of range");
     const XferRound& r = xfer_round_items_[static_cast<std::size_t>(round)];
+    // link-buffer frames: 256 KB items, any alignment -> the LDG8 non-persistent kernel
     const std::uint64_t b = what == 1 ? r.pack_begin : r.unpack_begin;
     const std::uint64_t e = what == 1 ? r.pack_end : r.unpack_end;
     cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(d_xfer_descs_.data()),
                               reinterpret_cast<const std::uint64_t*>(d_xfer_item0_.data()),
-                              static_cast<std::uint32_t>(xfer_descs_.size()), b, e, copy_grid(0), copy_variant(0),
+                              static_cast<std::uint32_t>(xfer_descs_.size()), b, e, copy_grid(0), 15,
                               dv.stream),
                what == 1 ? "xfer pack" : "xfer unpack");
   }

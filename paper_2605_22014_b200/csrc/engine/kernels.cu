@@ -439,6 +439,50 @@ __global__ void __launch_bounds__(kMwWarps * 32, 1) rs_copy_bulk_mw_kernel(const
   bulk_wait_all();
 }
 
+// Non-persistent TMA bulk copy: one 1-warp CTA per work item (<= the dynamic
+// shared memory of the launch: 16 or 32 KB of 16 B aligned rows).  The elected lane bulk-loads every row piece of the
+// item into shared memory on one mbarrier (complete_tx), waits, bulk-stores
+// them back out and waits for the stores to have read shared memory before the
+// CTA retires.  ~14 such CTAs fit an SM (16 KB of smem each), so an SM keeps
+// ~14 items of loads in flight with one issuing thread per item.
+constexpr uint32_t kNpTmaBytes = 16384;
+
+__global__ void __launch_bounds__(32) rs_copy_tma_np_kernel(const rs_copy_desc* __restrict__ descs,
+                                                            const uint64_t* __restrict__ item0,
+                                                            uint32_t ndesc, uint64_t item_begin,
+                                                            uint64_t item_end) {
+  extern __shared__ __align__(128) unsigned char buf[];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x != 0) return;
+  const uint64_t item = item_begin + blockIdx.x;
+  if (item >= item_end) return;
+  const uint32_t di = find_desc(item0, ndesc, item);
+  const rs_copy_desc& D = descs[di];
+  const uint64_t r0 = (item - D.item0) * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  mbar_init(&bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint32_t total = static_cast<uint32_t>((r1 - r0) * D.row_bytes);
+  mbar_expect_tx(&bar, total);
+  uint32_t off = 0;
+  for (uint64_t r = r0; r < r1; ++r) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    bulk_load(buf + off, reinterpret_cast<const void*>(D.src + so), static_cast<uint32_t>(D.row_bytes), &bar);
+    off += static_cast<uint32_t>(D.row_bytes);
+  }
+  mbar_wait(&bar, 0);
+  off = 0;
+  for (uint64_t r = r0; r < r1; ++r) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    bulk_store(reinterpret_cast<void*>(D.dst + dof), buf + off, static_cast<uint32_t>(D.row_bytes));
+    off += static_cast<uint32_t>(D.row_bytes);
+  }
+  bulk_commit();
+  bulk_wait_all();
+}
+
 // ------------------------------------------------------------- pattern
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -870,6 +914,14 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
     case 13:
       rs_copy_kernel<8, false, 1><<<grid, 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
+    case 17:    // non-persistent TMA bulk copy: one 1-warp CTA per <= 16 KB item
+    case 18: {  // same with <= 32 KB items
+      const uint64_t ctas = item_end - item_begin;
+      const uint32_t smem = variant == 18 ? 2 * kNpTmaBytes : kNpTmaBytes;
+      rs_copy_tma_np_kernel<<<static_cast<unsigned>(ctas), 32, smem, stream>>>(descs, item0, ndesc, item_begin,
+                                                                              item_end);
+      break;
+    }
     case 15: {  // non-persistent: one item per warp, the block scheduler deals CTAs
       const uint64_t ctas = (item_end - item_begin + 7) / 8;
       rs_copy_kernel<8><<<static_cast<unsigned>(ctas), 256, 0, stream>>>(descs, item0, ndesc, item_begin, item_end);

@@ -25,8 +25,8 @@ def main():
         co, cn = ParallelConfig(1, 1, 1, 1, [0]), ParallelConfig(2, 1, 1, 1, [1])
         plan = R.compute_transfer_plan(co, cn, sp)
         row = {"GiB": gib}
-        for bps, ck in ((3, 0), (3, 15)):
-            for item in (0, 16 << 10, 64 << 10):
+        for bps, ck in ((3, 0), (3, 17), (3, 18)):
+            for item in (0,):
                 eng = R.Engine([0], staging_bytes=1 << 30, blocks_per_sm=bps, copy_kernel=ck, item_bytes=item)
                 eng.layout(RS_SRC, sp, co)
                 eng.layout(RS_DST, sp, cn)
@@ -59,7 +59,7 @@ def c2_variants():
     sp, co, cn = specs.baseline_case("c2")
     plan = R.compute_transfer_plan(co, cn, sp)
     s = plan.summary()
-    for ck in (0, 15, 0):
+    for ck in (0, 17, 18, 17, 18):
         eng = R.Engine([0], staging_bytes=1 << 30, copy_kernel=ck)
         eng.layout(RS_SRC, sp, co)
         eng.layout(RS_DST, sp, cn)

@@ -14,7 +14,7 @@ for p in $PARTS; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
         python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "$OUT/launch_bench.txt" 2>&1 ;;
     copy)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:rs_copy_kernel -s 3 -c 1 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:rs_copy -s 3 -c 1 \
         -o "$OUT/copy_full" python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --profile-layers 4 \
         > "$OUT/copy_full.txt" 2>&1 ;;
     exchange)
