@@ -476,8 +476,11 @@ int Engine::copy_variant(int dev) const {
     // 16 B aligned with rows <= 16 KB (all BASELINE plans), else LDG8 over a
     // non-persistent grid (profiles/r1/tma_np_sweep.jsonl, np_sweep.jsonl)
     default: {
+      // (TMA bulk stores into another GPU's memory are unmeasured here -- one
+      // GPU per box -- so a program with peer destinations keeps plain
+      // st.global peer stores unless RS_COPY_TMA_NP is asked for explicitly)
       const DeviceProgram& p = programs_[static_cast<std::size_t>(dev)];
-      return p.all_aligned && p.max_row_bytes <= 16384 ? 17 : 15;
+      return p.all_aligned && p.max_row_bytes <= 16384 && !p.peer_stores ? 17 : 15;
     }
   }
 }
@@ -674,6 +677,7 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
   auto push = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb, int layer) {
     const int l = local_of(se->slot);
     if (l < 0) return;  // the source's process pushes it
+    if (de->slot != se->slot) programs_[static_cast<std::size_t>(l)].peer_stores = true;
     append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
                 addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
   };

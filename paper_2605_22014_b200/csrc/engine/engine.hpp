@@ -110,6 +110,7 @@ struct DeviceProgram {
   bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
   std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)
   std::uint64_t max_row_bytes = 0; // longest contiguous run (TMA-NP items must fit shared memory)
+  bool peer_stores = false;        // some descriptor writes another slot's memory (NVLink peer / IPC)
 };
 
 struct Device {
