@@ -416,11 +416,12 @@ def ours(args) -> None:
             "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res = run_reference_cpu(1, 2, 1, 0, args.staging_bytes)
+        cpu_layers = int(os.environ.get("RS_BENCH_CPU_SAMPLE_LAYERS", "4"))  # ~12 s of single-thread work
+        res = run_reference_cpu(1, cpu_layers, 1, 0, args.staging_bytes)
         if res is not None:
             line["cpu_baseline"] = {
                 "value": round(res["value"], 4), "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": (f"reference execute_plan (oracle/_ref) on the C2 resize of a 2-layer Llama-2-7B "
+                "sample": (f"reference execute_plan (oracle/_ref) on the C2 resize of a {cpu_layers}-layer Llama-2-7B "
                            f"slice, both dtype groups, {res['plan_bytes'] / 1e9:.2f} GB, 1 thread "
                            f"(the reference is single-threaded) of {os.cpu_count()} host cores")}
     if not args.no_e2e:
