@@ -374,3 +374,26 @@ def test_identity_resize_is_all_carryover(mode, oracle_c):
     assert rep["peak_staging_bytes"] == 0
     assert eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_bounded_memory_invariant_in_layers(mode, oracle_c):
+    """SPEC.md:562 on the device: resident staging <= B and independent of the
+    number of layers (L in {2, 8, 64}, B = 4096), bytes equal to the C oracle's."""
+    peaks = []
+    for L in (2, 8, 64):
+        ts = [specs.TensorSpec(f"w{l}", l, [32, 16], 0, "param", 4) for l in range(L)]
+        sp = specs.ModelSpec(f"layers{L}", L, ts, 4)
+        co, cn = specs.iota_config(1, 2, 1, 1), specs.iota_config(2, 4, 1, 1)
+        eng = make_engine(sp, co, cn, mode, 4096, lanes_per_link=1)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        rep = R.execute_plan(plan, eng)
+        orep, ostore = oracle_c.execute(sp, co, cn, plan.text(), SEED, 4096)
+        assert rep["ok"] and rep["layers_processed"] == orep["layers_processed"] == L
+        assert rep["peak_staging_bytes"] <= 4096
+        for (ti, rank), want in ostore.entries.items():
+            assert np.array_equal(eng.read(RS_DST, rank, ti), want), (L, ti, rank)
+        peaks.append(rep["peak_staging_bytes"])
+        eng.close()
+    assert len(set(peaks)) == 1
+    assert (peaks[0] == 0) == (mode == "direct")

@@ -138,3 +138,24 @@ def test_distributed_optimizer_execution_is_analytic(oracle_c):
         want = oracle_c.store_pattern(sp, cn, 42)
         for k, arr in want.entries.items():
             assert (store.entries[k] == arr).all(), (seed, k)
+
+
+def _layered(L):
+    ts = [specs.TensorSpec(f"w{l}", l, [32, 16], 0, "param", 4) for l in range(L)]
+    return specs.ModelSpec(f"layers{L}", L, ts, 4)
+
+
+def test_bounded_memory_invariant_in_layers(oracle_c, oracle_ref):
+    """peak staging <= B and invariant in L (L in {2, 8, 64}),
+    on the reference itself and on the restatement, B = 4096."""
+    peaks = []
+    for L in (2, 8, 64):
+        sp = _layered(L)
+        co, cn = specs.iota_config(1, 2, 1, 1), specs.iota_config(2, 4, 1, 1)
+        text = oracle_ref.plan_text(sp, co, cn)[0]
+        rr, _ = oracle_ref.execute(sp, co, cn, text, 7, 4096)
+        rc, _ = oracle_c.execute(sp, co, cn, text, 7, 4096)
+        assert rr["ok"] and rc["ok"] and rr["layers_processed"] == rc["layers_processed"] == L
+        assert rr["peak_staging_bytes"] == rc["peak_staging_bytes"] <= 4096
+        peaks.append(rr["peak_staging_bytes"])
+    assert len(set(peaks)) == 1 and peaks[0] > 0
