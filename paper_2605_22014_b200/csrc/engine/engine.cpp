@@ -1284,7 +1284,8 @@ rs_exec_report Engine::run() {
                                     reinterpret_cast<unsigned int*>(p.d_error.data()),
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
-                                    (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0),
+                                    (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0) |
+                                        (ring_l2 & 8 ? 8 : 0),
                                     cap - p.ntx - p.nrx, opts_.ring_cta_threads, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;

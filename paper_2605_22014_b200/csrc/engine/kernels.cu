@@ -249,6 +249,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -789,6 +805,7 @@ __device__ __forceinline__ uint32_t find_frame(const rs_copy_desc* __restrict__ 
 constexpr int kExFaultRx = 1;   // test hook: ring receivers drop out (peer failure)
 constexpr int kExDiscard = 2;   // receivers discard drained slot lines from L2
 constexpr int kExHints = 4;     // L2 policies: shards evict-first, ring slots evict-last
+constexpr int kExWarpSpec = 8;  // warp-specialised lanes: a control warp runs the handshakes
 
 // Block roles: blocks [0, ntx) send lanes_tx[b], [ntx, ntx + nrx) receive
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
@@ -813,6 +830,113 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
     const bool peer = (L.flags & RS_LANE_PEER) != 0;
     const uint64_t pol_first = (flags & kExHints) ? policy_evict_first() : 0;
     const uint64_t pol_last = (flags & kExHints) ? policy_evict_last() : 0;
+    if (flags & kExWarpSpec) {
+      // Warp-specialised lane: warp 0 polls flags, publishes and discards;
+      // warps 1.. copy.  Two mbarrier pairs hand batches over: go[b % 2]
+      // (control -> copy: slot free / data ready) and done[b % 2] (copy ->
+      // control: batch copied), so the copy warps work on batch b while the
+      // control warp fences and publishes batch b - 1 and polls for b + 1.
+      __shared__ __align__(8) uint64_t go_bar[2], done_bar[2];
+      __shared__ int abort_shared;
+      const int ncopy = warps_per_block - 1;
+      if (threadIdx.x == 0) {
+        mbar_init(&go_bar[0], 1);
+        mbar_init(&go_bar[1], 1);
+        mbar_init(&done_bar[0], static_cast<uint32_t>(ncopy));
+        mbar_init(&done_bar[1], static_cast<uint32_t>(ncopy));
+        abort_shared = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+      if (warp_in_block == 0) {
+        // Event loop, the whole warp in lockstep (lane 0 polls, shuffles the
+        // verdicts): hand batch g to the copy warps as soon as its flag is up
+        // (ready for receivers, the credit of batch g - K for senders) and
+        // publish batch f as soon as its copy is done -- neither waits behind
+        // the other, so no circular wait between the two ends even at K = 2.
+        // go(g) needs done(g - 2) consumed (mbarrier phase reuse): g <= f + 1.
+        uint32_t g = 0, f = 0;
+        uint64_t idle = 0;
+        while (f < L.nbatches) {
+          bool progress = false;
+          if (g < L.nbatches && g <= f + 1) {
+            int up = 0;
+            if (lane_id == 0) {
+              if (sender) {
+                up = g < L.slots ||
+                     (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + g % L.slots)
+                           : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + g % L.slots)) >=
+                         epoch + g - L.slots + 1;
+              } else {
+                up = (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + g % L.slots)
+                           : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + g % L.slots)) >=
+                     epoch + g + 1;
+              }
+              if (up) mbar_arrive(&go_bar[g & 1]);
+            }
+            if (__shfl_sync(0xffffffffu, up, 0)) {
+              ++g;
+              progress = true;
+            }
+          }
+          if (f < g && mbar_test(&done_bar[f & 1], (f >> 1) & 1)) {
+            const rs_batch_desc Bc = batches[L.batch0 + f];
+            const uint32_t sc = f % L.slots;
+            if (!sender && (flags & kExDiscard) && Bc.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
+              const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(sc) * L.slot_bytes;
+              const uint64_t lines = (Bc.extent + 127) >> 7;
+              for (uint64_t i = lane_id; i < lines; i += 32) discard_l2_line(base + (i << 7));
+            }
+            __syncwarp();
+            if (lane_id == 0)
+              publish(reinterpret_cast<uint64_t*>(sender ? L.ready_flags : L.credit_flags) + sc, epoch + f + 1, peer);
+            ++f;
+            progress = true;
+          }
+          if (progress) {
+            idle = 0;
+            continue;
+          }
+          int stop = 0;
+          if (lane_id == 0) {
+            if (*reinterpret_cast<volatile unsigned int*>(error_flag)) stop = 1;
+            else if (++idle > spin_limit) {
+              atomicExch(error_flag, 1u);
+              stop = 1;
+            }
+            if (stop && g < L.nbatches) {  // wake the copy warps waiting for batch g: they see the abort
+              abort_shared = 1;
+              mbar_arrive(&go_bar[g & 1]);
+            }
+            if (!stop) __nanosleep(64);
+          }
+          if (__shfl_sync(0xffffffffu, stop, 0)) return;
+        }
+      } else {
+        const int cw = warp_in_block - 1;
+        for (uint32_t b = 0; b < L.nbatches; ++b) {
+          mbar_wait(&go_bar[b & 1], (b >> 1) & 1);
+          if (*reinterpret_cast<volatile int*>(&abort_shared)) return;
+          const rs_batch_desc B = batches[L.batch0 + b];
+          if (sender) {
+            for (uint32_t it = cw; it < B.pack_items; it += ncopy) {
+              const rs_copy_desc& D = frames[B.pack0 + find_frame(frames + B.pack0, B.npack, it)];
+              if (flags & kExHints) warp_copy_item_hint<true, 8>(D, it - D.item0, lane_id, pol_first, pol_last);
+              else warp_copy_item<true, 8>(D, it - D.item0, lane_id);
+            }
+          } else {
+            for (uint32_t it = cw; it < B.unpack_items; it += ncopy) {
+              const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
+              if (flags & kExHints) warp_copy_item_hint<false, 8>(D, it - D.item0, lane_id, pol_first, pol_first);
+              else warp_copy_item<false, 8>(D, it - D.item0, lane_id);
+            }
+          }
+          __syncwarp();
+          if (lane_id == 0) mbar_arrive(&done_bar[b & 1]);
+        }
+      }
+      return;
+    }
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
       const uint32_t slot = b % L.slots;

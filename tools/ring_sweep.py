@@ -34,7 +34,8 @@ def main():
             for K in depths:
                 for cap in caps:
                     eng = R.Engine([0], staging_bytes=B, mode="staged", slots_per_link=K, lanes_per_link=lanes,
-                                   ring_slot_kib=cap, ring_discard=l2mode, ring_cta_threads=threads)
+                                   ring_slot_kib=cap, ring_discard=l2mode, ring_cta_threads=threads,
+                                   spin_limit=50_000_000)
                     eng.layout(RS_SRC, sp, co)
                     eng.layout(RS_DST, sp, cn)
                     eng.alloc(RS_SRC)
@@ -42,7 +43,7 @@ def main():
                     eng.comm_alloc(plan)
                     eng.fill_pattern(RS_SRC, 42)
                     eng.fill_pattern(RS_DST, 7)
-                    row = {"case": case, "layers": layers, "B_MiB": B >> 20, "l2_discard": bool(l2mode & 1), "l2_hints": bool(l2mode & 4),
+                    row = {"case": case, "layers": layers, "B_MiB": B >> 20, "l2_discard": bool(l2mode & 1), "l2_hints": bool(l2mode & 4), "warp_spec": bool(l2mode & 8),
                            "lanes": lanes, "K": K, "cta_threads": threads, "slot_cap_KiB": cap}
                     try:
                         eng.prepare(plan)
