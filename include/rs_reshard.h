@@ -90,12 +90,13 @@ typedef struct {
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
   int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
-  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 256, -1: no cap,
-                               slot = B / (inbound links x lanes x K)); B stays the upper bound */
-  int32_t ring_discard;     /* STAGED L2 treatment of ring slots: 0 = default (1|4); else bit
-                               flags 1 = receivers drop drained slot lines (discard.global.L2,
-                               no write-back), 4 = L2 policies (shards evict-first, slots
-                               evict-last); 2 = neither */
+  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 128, -1: no cap,
+                               slot = B / (inbound lanes x K)); B stays the upper bound */
+  int32_t ring_discard;     /* STAGED ring mode bit flags (0 = default 1|4; 2 = none):
+                               1 receivers drop drained slot lines (discard.global.L2);
+                               4 L2 policies (shards evict-first, slots evict-last);
+                               8 warp-specialised lanes (control-warp event loop);
+                               16 (with 8, 256-thread lanes) TMA bulk copies in the copy warps */
   int32_t ring_cta_threads; /* STAGED: threads per ring-lane CTA, 256 / 512 / 1024 (0: default) */
 } rs_engine_options;
 

@@ -42,7 +42,7 @@ namespace {
 
 constexpr std::size_t kAlign = 256;
 constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
-constexpr std::uint64_t kRingSlotDefault = 256u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
+constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
 constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 std::uint64_t key(int rank, std::uint32_t ti) {
@@ -804,7 +804,9 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       }
   }
   // Ring slot size per dst rank: B split over its inbound lanes, capped at
-  // 256 KiB by default -- B is the budget, not the target footprint.  With
+  // 128 KiB by default -- B is the budget, not the target footprint.  At
+  // 64-128 KiB the rings stay (almost) entirely in L2: DRAM traffic of the
+  // exchange kernel = the 2x floor (profiles/r1/ring_traffic/).  With
   // GPU-scope handshakes for same-device lanes, 128-256 KiB slots x K = 2
   // keep the rings small enough to stay largely L2-resident (less HBM
   // traffic than the 4x of a DRAM-resident ring) while a batch is still long
@@ -1285,7 +1287,8 @@ rs_exec_report Engine::run() {
                                     opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit)
                                                          : kSpinLimit,
                                     (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0) |
-                                        (ring_l2 & 8 ? 8 : 0),
+                                        (ring_l2 & 8 ? 8 : 0) |
+                                        ((ring_l2 & 24) == 24 && opts_.ring_cta_threads == 256 ? 16 : 0),
                                     cap - p.ntx - p.nrx, opts_.ring_cta_threads, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;

@@ -296,6 +296,26 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* smem_src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+// Order generic-proxy global accesses against async-proxy (TMA) ones.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(32, 1) rs_copy_bulk_kernel(const rs_copy_desc* __restrict__ descs,
@@ -801,11 +821,52 @@ __device__ __forceinline__ uint32_t find_frame(const rs_copy_desc* __restrict__ 
   return lo;
 }
 
+// One work item through the copy warp's shared-memory buffer with TMA (the
+// elected lane issues everything): bulk-load the item's rows on the warp's
+// mbarrier, wait, bulk-store them, and wait until the stores have read the
+// buffer.  Returns false (nothing done) when the item does not fit the buffer
+// or is not 16 B aligned -- the caller copies it with the warp instead.
+constexpr uint32_t kLaneTmaBytes = 16384;
+
+__device__ __forceinline__ bool tma_copy_item(const rs_copy_desc& D, uint64_t local_item, unsigned char* buf,
+                                              uint64_t* bar, uint32_t& phase, uint64_t lpol, uint64_t spol,
+                                              int lane) {
+  const uint64_t r0 = local_item * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  const uint64_t total = (r1 - r0) * D.row_bytes;
+  if (D.vec_log2 != 4 || total > kLaneTmaBytes) return false;
+  if (lane == 0) {
+    mbar_expect_tx(bar, static_cast<uint32_t>(total));
+    uint32_t off = 0;
+    for (uint64_t r = r0; r < r1; ++r) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      bulk_load_hint(buf + off, reinterpret_cast<const void*>(D.src + so), static_cast<uint32_t>(D.row_bytes), bar,
+                     lpol);
+      off += static_cast<uint32_t>(D.row_bytes);
+    }
+    mbar_wait(bar, phase);
+    off = 0;
+    for (uint64_t r = r0; r < r1; ++r) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      bulk_store_hint(reinterpret_cast<void*>(D.dst + dof), buf + off, static_cast<uint32_t>(D.row_bytes), spol);
+      off += static_cast<uint32_t>(D.row_bytes);
+    }
+    bulk_commit();
+    bulk_wait_read<0>();
+  }
+  phase ^= 1;
+  __syncwarp();
+  return true;
+}
+
 // flags of rs_launch_exchange
 constexpr int kExFaultRx = 1;   // test hook: ring receivers drop out (peer failure)
 constexpr int kExDiscard = 2;   // receivers discard drained slot lines from L2
 constexpr int kExHints = 4;     // L2 policies: shards evict-first, ring slots evict-last
 constexpr int kExWarpSpec = 8;  // warp-specialised lanes: a control warp runs the handshakes
+constexpr int kExLaneTma = 16;  // (with kExWarpSpec) copy warps move items with TMA bulk copies
 
 // Block roles: blocks [0, ntx) send lanes_tx[b], [ntx, ntx + nrx) receive
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
@@ -914,22 +975,46 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
         }
       } else {
         const int cw = warp_in_block - 1;
+        extern __shared__ __align__(128) unsigned char lane_smem[];
+        const bool tma = (flags & kExLaneTma) != 0;
+        __shared__ __align__(8) uint64_t tma_bar[32];
+        unsigned char* buf = lane_smem + static_cast<size_t>(cw) * kLaneTmaBytes;
+        uint32_t phase = 0;
+        if (tma && lane_id == 0) {
+          mbar_init(&tma_bar[cw], 1);
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        const uint64_t tpol_first = policy_evict_first(), tpol_last = policy_evict_last();
         for (uint32_t b = 0; b < L.nbatches; ++b) {
           mbar_wait(&go_bar[b & 1], (b >> 1) & 1);
           if (*reinterpret_cast<volatile int*>(&abort_shared)) return;
           const rs_batch_desc B = batches[L.batch0 + b];
+          // receivers: the slot bytes were published through the generic proxy
+          if (tma && !sender && lane_id == 0) fence_proxy_async_global();
+          __syncwarp();
           if (sender) {
             for (uint32_t it = cw; it < B.pack_items; it += ncopy) {
               const rs_copy_desc& D = frames[B.pack0 + find_frame(frames + B.pack0, B.npack, it)];
+              if (tma && tma_copy_item(D, it - D.item0, buf, &tma_bar[cw], phase, tpol_first, tpol_last, lane_id))
+                continue;
               if (flags & kExHints) warp_copy_item_hint<true, 8>(D, it - D.item0, lane_id, pol_first, pol_last);
               else warp_copy_item<true, 8>(D, it - D.item0, lane_id);
             }
           } else {
             for (uint32_t it = cw; it < B.unpack_items; it += ncopy) {
               const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
+              if (tma && tma_copy_item(D, it - D.item0, buf, &tma_bar[cw], phase, tpol_first, tpol_first, lane_id))
+                continue;
               if (flags & kExHints) warp_copy_item_hint<false, 8>(D, it - D.item0, lane_id, pol_first, pol_first);
               else warp_copy_item<false, 8>(D, it - D.item0, lane_id);
             }
+          }
+          // senders: the slot writes of the async proxy complete and become
+          // ordered before the control warp's release
+          if (tma && lane_id == 0) {
+            bulk_wait_all();
+            fence_proxy_async_global();
           }
           __syncwarp();
           if (lane_id == 0) mbar_arrive(&done_bar[b & 1]);
@@ -1096,10 +1181,18 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                int local_blocks, int threads, cudaStream_t stream) {
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
-#define RS_EXCHANGE_LAUNCH(T)                                                                              \
-  rs_exchange_kernel<T><<<grid, T, 0, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
-                                                local_item0, nlocal, local_items, epoch, error_flag, spin_limit, \
-                                                flags)
+  const int smem = (flags & kExLaneTma) ? (threads / 32 - 1) * static_cast<int>(kLaneTmaBytes) : 0;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaSuccess;
+    if (threads == 1024) e = cudaFuncSetAttribute(rs_exchange_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    else if (threads == 512) e = cudaFuncSetAttribute(rs_exchange_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    else e = cudaFuncSetAttribute(rs_exchange_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+#define RS_EXCHANGE_LAUNCH(T)                                                                                 \
+  rs_exchange_kernel<T><<<grid, T, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
+                                                   local_item0, nlocal, local_items, epoch, error_flag, spin_limit, \
+                                                   flags)
   if (threads == 1024) RS_EXCHANGE_LAUNCH(1024);
   else if (threads == 512) RS_EXCHANGE_LAUNCH(512);
   else RS_EXCHANGE_LAUNCH(256);
@@ -1115,7 +1208,11 @@ int rs_kernel_max_blocks_per_sm(int which) {
   else if (which == 6) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_copy_cta_kernel<8>, 256, 0);
   else if (which == 4) n = 1;  // bulk ring: one CTA (one issuer, ~200 KB smem) per SM
   else if (which == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_pattern_kernel<false>, 256, 0);
-  else if (which == 7) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512>, 512, 0);
+  else if (which == 9) {
+    const int smem = 7 * static_cast<int>(kLaneTmaBytes);
+    cudaFuncSetAttribute(rs_exchange_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256>, 256, smem);
+  } else if (which == 7) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512>, 512, 0);
   else if (which == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<1024>, 1024, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256>, 256, 0);
   return n;
