@@ -29,6 +29,7 @@
 #include <set>
 
 #include "compile.hpp"
+#include "engine_internal.hpp"
 #include "kernels.h"
 
 namespace rsb {
@@ -38,39 +39,8 @@ void cuda_check(cudaError_t e, const char* what) {
     throw SystemError(std::string(what) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
 }
 
-namespace {
+using namespace detail;
 
-constexpr std::size_t kAlign = 256;
-constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
-constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
-constexpr std::uint64_t kSpinLimit = 200000000ull;
-
-std::uint64_t key(int rank, std::uint32_t ti) {
-  return (static_cast<std::uint64_t>(ti) << 32) | static_cast<std::uint32_t>(rank);
-}
-
-std::size_t align_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
-
-struct DeviceGuard {
-  int prev = 0;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-  }
-  ~DeviceGuard() { cudaSetDevice(prev); }
-};
-
-std::string escape_msg(const char* who, const reshard::ShardView& b, const reshard::ShardView& owner) {
-  return std::string(who) + ": bounds " + b.to_string() + " escape owner view " + owner.to_string();
-}
-
-std::string no_buffer(int rank, std::uint32_t ti) {
-  return "shard store: no buffer for rank " + std::to_string(rank) + " tensor " + std::to_string(ti);
-}
-
-std::uint64_t addr(const char* p) { return reinterpret_cast<std::uint64_t>(p); }
-
-}  // namespace
 
 // ------------------------------------------------------------ DeviceBuffer
 
@@ -351,46 +321,6 @@ void Engine::bind(int which, int rank, std::uint32_t ti, void* ptr, std::int64_t
 
 // ------------------------------------------------------ comm arenas and IPC
 
-std::size_t Engine::comm_bytes(int slot) const {
-  if (comm_layout_valid_) return comm_layout_.slot_bytes.at(static_cast<std::size_t>(slot));
-  return make_comm_layout(nullptr).slot_bytes.at(static_cast<std::size_t>(slot));
-}
-
-void Engine::comm_alloc() {
-  if (!stores_[RS_DST].laid_out) throw DomainError("comm: lay out the dst store first");
-  comm_layout_ = make_comm_layout(nullptr);
-  comm_layout_valid_ = true;
-  alloc_comm_arenas();
-}
-
-// Plan-sized rings: each dst rank's region holds exactly its rings (<= B),
-// so resident staging is what the rings use, not B per rank.
-void Engine::comm_alloc_plan(const reshard::TransferPlan& plan) {
-  if (!stores_[RS_DST].laid_out || !stores_[RS_SRC].laid_out) throw DomainError("comm: lay out both stores first");
-  const RingGeometry geo = ring_geometry(plan);
-  comm_layout_ = make_comm_layout(&geo.ring_bytes_of);
-  comm_layout_valid_ = true;
-  alloc_comm_arenas();
-}
-
-void Engine::alloc_comm_arenas() {
-  comm_.clear();
-  for (const auto& dv : devices_) {
-    const std::size_t n = comm_bytes(dv.slot);
-    comm_.emplace_back(dv.ordinal, n);
-    DeviceGuard g(dv.ordinal);
-    cuda_check(cudaMemset(comm_.back().data(), 0, n), "comm memset");
-  }
-  prepared_ = false;
-}
-
-char* Engine::comm_base(int slot) const {
-  const int l = local_of(slot);
-  if (l >= 0) return static_cast<std::size_t>(l) < comm_.size() ? comm_[static_cast<std::size_t>(l)].data() : nullptr;
-  const auto& imp = comm_imported_[static_cast<std::size_t>(slot)];
-  return imp ? imp->data() : nullptr;
-}
-
 std::int64_t Engine::export_arena(int which, int slot, void* handle) const {
   const int l = local_of(slot);
   if (l < 0) throw DomainError("export: slot " + std::to_string(slot) + " is not local");
@@ -654,18 +584,6 @@ void Engine::prepare(const reshard::TransferPlan& plan, std::uint64_t plan_id) {
   prepared_id_ = plan_id;
 }
 
-namespace {
-
-// Pointer of an entry that local work must touch.
-char* need_ptr(const Entry* e, const char* what) {
-  if (!e->ptr)
-    throw DomainError(std::string(what) + " shard rank " + std::to_string(e->rank) + " tensor " +
-                      std::to_string(e->ti) + " on slot " + std::to_string(e->slot) +
-                      " is not mapped in this process (rs_arena_import)");
-  return e->ptr;
-}
-
-}  // namespace
 
 void Engine::compile_direct(const reshard::TransferPlan& plan) {
   const Store& src = stores_[RS_SRC];
@@ -730,374 +648,6 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
       programs_[d].layers.push_back({layer, mark[d], programs_[d].local.size()});
   }
   planned_.ok = 1;
-}
-
-// Ring geometry of a plan (STAGED): lanes per link, slot size and ring bytes
-// per destination rank.  Deterministic from the plan and the layouts, so
-// every process computes the same rings for every slot.
-Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) const {
-  const Store& src = stores_[RS_SRC];
-  const Store& dst = stores_[RS_DST];
-  const std::int64_t B = opts_.staging_bytes;
-  const int K = opts_.slots_per_link;
-  RingGeometry geo;
-  // inbound links per destination rank (remote tasks only)
-  std::map<int, std::set<int>> inbound;
-  for (const auto& kv : plan.tasks_by_layer)
-    for (const auto& t : kv.second)
-      if (!t.is_local()) inbound[t.dst_rank].insert(t.src_rank);
-
-  // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
-  // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
-  // the sender + receiver CTAs of the busiest slot stop being co-resident.
-  // Automatic choice: lanes proportional to each link's bytes (a link's
-  // lanes finish together, so the launch ends when the heaviest link does),
-  // scaled so every slot's sender + receiver lanes fit 3/4 of one device's
-  // CTA capacity, at least one and at most 32 per link (same answer on every
-  // process: the plan and the placement are global).
-  std::map<std::pair<int, int>, std::uint64_t> link_bytes;
-  for (const auto& kv : plan.tasks_by_layer)
-    for (const auto& t : kv.second)
-      if (!t.is_local()) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
-  auto& lanes_of = geo.lanes_of;
-  if (opts_.lanes_per_link > 0) {
-    for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
-  } else if (!link_bytes.empty()) {
-    auto slot_of = [&](const Store& s, int rank) {
-      for (const auto& e : s.entries)
-        if (e.rank == rank) return e.slot;
-      return 0;
-    };
-    std::map<int, int> src_slot, dst_slot;
-    std::vector<std::uint64_t> slot_bytes(static_cast<std::size_t>(nslots_), 0);
-    for (const auto& [lk, b] : link_bytes) {
-      if (!src_slot.count(lk.first)) src_slot[lk.first] = slot_of(src, lk.first);
-      if (!dst_slot.count(lk.second)) dst_slot[lk.second] = slot_of(dst, lk.second);
-      slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
-      slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
-    }
-    const int capacity = grid_for(0, exchange_kernel_id()) * 3 / 4;
-    const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
-    const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
-    std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
-    for (const auto& [lk, b] : link_bytes) {
-      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, 32);
-      lanes_of[lk] = n;
-      slot_lanes[static_cast<std::size_t>(src_slot[lk.first])] += n;
-      slot_lanes[static_cast<std::size_t>(dst_slot[lk.second])] += n;
-    }
-    // the max(1, .) floor can overshoot a slot with many light links: trim
-    // the widest links touching it
-    for (int sl = 0; sl < nslots_; ++sl)
-      while (slot_lanes[static_cast<std::size_t>(sl)] > capacity) {
-        std::pair<int, int> widest{-1, -1};
-        int w = 1;
-        for (const auto& [lk, n] : lanes_of)
-          if ((src_slot[lk.first] == sl || dst_slot[lk.second] == sl) && n > w) {
-            w = n;
-            widest = lk;
-          }
-        if (widest.first < 0) break;  // every link at one lane: the launch check reports it
-        --lanes_of[widest];
-        --slot_lanes[static_cast<std::size_t>(src_slot[widest.first])];
-        --slot_lanes[static_cast<std::size_t>(dst_slot[widest.second])];
-      }
-  }
-  // Ring slot size per dst rank: B split over its inbound lanes, capped at
-  // 128 KiB by default -- B is the budget, not the target footprint.  At
-  // 64-128 KiB the rings stay (almost) entirely in L2: DRAM traffic of the
-  // exchange kernel = the 2x floor (profiles/r1/ring_traffic/).  With
-  // GPU-scope handshakes for same-device lanes, 128-256 KiB slots x K = 2
-  // keep the rings small enough to stay largely L2-resident (less HBM
-  // traffic than the 4x of a DRAM-resident ring) while a batch is still long
-  // against its handshake; 32 KiB slots pay the handshake, >= 1 MiB slots
-  // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).  The kernel adds
-  // evict-first / evict-last L2 policies and discards drained slots by
-  // default (ring_sweep_v4.jsonl: 15.4 -> 13.1 ms on the C5 slice).
-  const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
-                                 : opts_.ring_slot_kib == 0 ? kRingSlotDefault
-                                                            : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
-  auto& inbound_lanes = geo.inbound_lanes;
-  for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
-  auto& slot_bytes_of = geo.slot_bytes_of;
-  for (const auto& [d, srcs] : inbound) {
-    std::uint64_t sb = static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(K));
-    sb = std::min(sb, slot_cap);
-    slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
-    geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(K);
-  }
-
-  return geo;
-}
-
-// Comm arena layout over every slot: the dst ranks of a slot in ascending
-// order, each with `ring_bytes[rank]` (plan-sized) or B bytes, then the flags.
-Engine::CommLayout Engine::make_comm_layout(const std::map<int, std::uint64_t>* ring_bytes) const {
-  CommLayout L;
-  L.regions.resize(static_cast<std::size_t>(nslots_));
-  L.slot_bytes.assign(static_cast<std::size_t>(nslots_), kFlagBytes);
-  std::map<int, std::set<int>> ranks_on_slot;
-  for (const auto& e : stores_[RS_DST].entries) ranks_on_slot[e.slot].insert(e.rank);
-  for (const auto& [slot, ranks] : ranks_on_slot) {
-    std::size_t off = 0;
-    for (int r : ranks) {
-      std::size_t b = static_cast<std::size_t>(opts_.staging_bytes);
-      if (ring_bytes) {
-        auto it = ring_bytes->find(r);
-        b = it == ring_bytes->end() ? 0 : align_up(static_cast<std::size_t>(it->second), kAlign);
-      }
-      L.regions[static_cast<std::size_t>(slot)][r] = {off, b};
-      off += b;
-    }
-    L.slot_bytes[static_cast<std::size_t>(slot)] = off + kFlagBytes;
-  }
-  return L;
-}
-
-void Engine::compile_staged(const reshard::TransferPlan& plan) {
-  const Store& src = stores_[RS_SRC];
-  const Store& dst = stores_[RS_DST];
-  const auto& m = src.model;
-  const std::int64_t B = opts_.staging_bytes;
-  const int K = opts_.slots_per_link;
-
-  const RingGeometry geo = ring_geometry(plan);
-  const auto& lanes_of = geo.lanes_of;
-  const auto& slot_bytes_of = geo.slot_bytes_of;
-  const auto& inbound_lanes = geo.inbound_lanes;
-  // each destination rank's region in its slot's comm arena (the layout the
-  // arena was allocated with: B per rank, or plan-sized, rs_comm_alloc_plan)
-  std::map<int, std::size_t> region_of, region_bytes;
-  for (std::size_t sl = 0; sl < comm_layout_.regions.size(); ++sl)
-    for (const auto& [r, ob] : comm_layout_.regions[sl]) {
-      region_of[r] = ob.first;
-      region_bytes[r] = ob.second;
-    }
-
-  struct Frame {
-    const Entry* se;
-    const Entry* de;
-    reshard::ShardView region;
-    std::int64_t eb;
-    std::uint64_t off;
-    int layer;
-  };
-  struct LaneBuild {
-    int src_rank, dst_rank, sslot, dslot;
-    std::uint64_t slot_bytes;
-    std::vector<std::vector<Frame>> batches;
-    std::uint64_t fill = 0;
-  };
-  std::vector<LaneBuild> lanes;
-  std::map<std::pair<int, int>, int> link_first_lane, link_cursor;
-
-  std::vector<std::size_t> mark(devices_.size());
-  for (int layer : plan_layers_) {
-    for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
-    std::vector<std::size_t> lane_mark_batches(lanes.size()), lane_mark_frames(lanes.size());
-    std::vector<std::uint64_t> lane_mark_fill(lanes.size());
-    for (std::size_t i = 0; i < lanes.size(); ++i) {
-      lane_mark_batches[i] = lanes[i].batches.size();
-      lane_mark_fill[i] = lanes[i].fill;
-      lane_mark_frames[i] = lanes[i].batches.empty() ? 0 : lanes[i].batches.back().size();
-    }
-    const std::size_t lanes_before = lanes.size();
-    rs_exec_report delta{};
-    auto local_copy = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb) {
-      const int l = local_of(se->slot);
-      if (l < 0) return;
-      append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
-                  addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
-    };
-    try {
-      if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end()) {
-        for (const auto& k : it->second) {
-          const Entry* se = src.find(k.rank, k.tensor_index);
-          const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
-          if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
-          if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
-          if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
-          const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
-          local_copy(se, de, k.bounds, eb);
-          delta.carryover_bytes += k.bounds.element_count() * eb;
-        }
-      }
-      if (auto it = plan.tasks_by_layer.find(layer); it != plan.tasks_by_layer.end()) {
-        for (const auto& t : it->second) {
-          const Entry* se = src.find(t.src_rank, t.tensor_index);
-          if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
-          if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
-          const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
-          if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
-          const Entry* de = dst.find(t.dst_rank, t.tensor_index);
-          if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
-          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
-          if (t.is_local()) {
-            local_copy(se, de, t.bounds, eb);
-            delta.local_copy_bytes += t.bounds.element_count() * eb;
-            continue;
-          }
-          const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);
-          if (static_cast<std::uint64_t>(eb) > sb)
-            throw IntegrityError("staging: ring slot of " + std::to_string(sb) + " bytes cannot hold one element (B=" +
-                                 std::to_string(B) + " over " + std::to_string(inbound_lanes.at(t.dst_rank)) +
-                                 " inbound links)");
-          const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
-          const auto lk = std::make_pair(t.src_rank, t.dst_rank);
-          const int P = lanes_of.at(lk);
-          if (!link_first_lane.count(lk)) {
-            link_first_lane[lk] = static_cast<int>(lanes.size());
-            for (int p = 0; p < P; ++p) lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, {}, 0});
-          }
-          for (const auto& c : chunks) {
-            int& cur = link_cursor[lk];
-            LaneBuild& lb = lanes[static_cast<std::size_t>(link_first_lane[lk] + cur)];
-            cur = (cur + 1) % P;
-            const std::uint64_t n = static_cast<std::uint64_t>(c.element_count() * eb);
-            std::uint64_t off = align_up(lb.fill, 16);
-            if (lb.batches.empty() || off + n > lb.slot_bytes) {
-              lb.batches.emplace_back();
-              off = 0;
-            }
-            lb.batches.back().push_back({se, de, c, eb, off, layer});
-            lb.fill = off + n;
-          }
-          delta.bytes_moved += t.bounds.element_count() * eb;
-        }
-      }
-    } catch (const std::exception& e) {
-      if (dynamic_cast<const DomainError*>(&e)) throw;  // mapping errors are not plan integrity
-      for (std::size_t d = 0; d < devices_.size(); ++d) programs_[d].local.resize(mark[d]);
-      lanes.resize(lanes_before);
-      for (std::size_t i = 0; i < lanes_before; ++i) {
-        lanes[i].batches.resize(lane_mark_batches[i]);
-        if (!lanes[i].batches.empty()) lanes[i].batches.back().resize(lane_mark_frames[i]);
-        lanes[i].fill = lane_mark_fill[i];
-      }
-      for (auto it = link_first_lane.begin(); it != link_first_lane.end();)
-        it = it->second >= static_cast<int>(lanes_before) ? link_first_lane.erase(it) : std::next(it);
-      planned_.ok = 0;
-      planned_.failed_layer = layer;
-      std::snprintf(planned_.error, sizeof planned_.error, "%s", e.what());
-      break;
-    }
-    planned_.carryover_bytes += delta.carryover_bytes;
-    planned_.local_copy_bytes += delta.local_copy_bytes;
-    planned_.bytes_moved += delta.bytes_moved;
-    planned_.layers_processed++;
-    for (std::size_t d = 0; d < devices_.size(); ++d)
-      programs_[d].layers.push_back({layer, mark[d], programs_[d].local.size()});
-  }
-  if (planned_.failed_layer < 0) planned_.ok = 1;
-
-  // Ring memory inside the comm arenas (deterministic on every process):
-  // a destination rank's lanes take consecutive K-slot rings in its B region;
-  // ready flags in the destination slot's flag area, credit flags in the
-  // source slot's.
-  std::map<int, std::uint64_t> ring_used;  // dst rank -> bytes used in its region
-  std::vector<std::size_t> flag_used(static_cast<std::size_t>(nslots_), 0);
-  const std::size_t flags_per_lane = align_up(sizeof(std::uint64_t) * static_cast<std::size_t>(K), 64);
-  struct LaneAddr {
-    std::uint64_t ring_off, ready_off, credit_off;
-  };
-  std::vector<LaneAddr> where(lanes.size());
-  for (std::size_t i = 0; i < lanes.size(); ++i) {
-    const auto& lb = lanes[i];
-    std::uint64_t& used = ring_used[lb.dst_rank];
-    auto reg = region_of.find(lb.dst_rank);
-    if (reg == region_of.end())
-      throw DomainError("staged: comm arena has no ring region for dst rank " + std::to_string(lb.dst_rank) +
-                        "; re-run rs_comm_alloc for this dst layout");
-    where[i].ring_off = reg->second + used;
-    used += lb.slot_bytes * static_cast<std::uint64_t>(K);
-    if (used > region_bytes.at(lb.dst_rank))
-      throw DomainError("staged: ring region of dst rank " + std::to_string(lb.dst_rank) + " (" +
-                        std::to_string(region_bytes.at(lb.dst_rank)) + " bytes) is smaller than this plan's rings; " +
-                        "re-run rs_comm_alloc_plan with this plan");
-    auto& fr = flag_used[static_cast<std::size_t>(lb.dslot)];
-    auto& fc = flag_used[static_cast<std::size_t>(lb.sslot)];
-    if (fr + flags_per_lane > kFlagBytes || fc + flags_per_lane > kFlagBytes)
-      throw DomainError("staged: too many ring lanes for the flag area; lower lanes_per_link");
-    where[i].ready_off = fr;
-    fr += flags_per_lane;
-    where[i].credit_off = fc;
-    fc += flags_per_lane;
-    planned_.peak_staging_bytes = std::max<std::int64_t>(planned_.peak_staging_bytes, static_cast<std::int64_t>(used));
-  }
-  auto flag_base = [&](int slot) -> char* {
-    char* b = comm_base(slot);
-    const std::size_t ring_area = comm_bytes(slot) - kFlagBytes;
-    return b ? b + ring_area : nullptr;
-  };
-
-  // serialise lanes / batches / frames (global tables, uploaded to every local device)
-  std::vector<rs_lane_desc> all_lanes;
-  std::vector<rs_batch_desc> batches;
-  std::vector<rs_copy_desc> frames;
-  for (std::size_t i = 0; i < lanes.size(); ++i) {
-    const auto& lb = lanes[i];
-    const bool tx_local = local_of(lb.sslot) >= 0, rx_local = local_of(lb.dslot) >= 0;
-    char* ring = comm_base(lb.dslot);
-    char* ready = flag_base(lb.dslot);
-    char* credit = flag_base(lb.sslot);
-    if ((tx_local || rx_local) && (!ring || !ready || !credit))
-      throw DomainError("staged: comm arena of slot " + std::to_string(tx_local ? lb.dslot : lb.sslot) +
-                        " not mapped in this process (rs_arena_import RS_COMM)");
-    const std::uint64_t ring_addr = ring ? addr(ring) + where[i].ring_off : 0;
-    rs_lane_desc L{};
-    L.slot_base = L.slot_base_rx = ring_addr;
-    L.slot_bytes = lb.slot_bytes;
-    L.ready_flags = L.ready_flags_rx = ready ? addr(ready) + where[i].ready_off : 0;
-    L.credit_flags = L.credit_flags_tx = credit ? addr(credit) + where[i].credit_off : 0;
-    L.slots = static_cast<std::uint32_t>(K);
-    // GPU-scope synchronisation only when both ends are this process's same
-    // slot; every cross-slot lane (another GPU, or another process sharing a
-    // GPU through IPC) synchronises at system scope
-    L.flags = lb.sslot == lb.dslot ? 0u : RS_LANE_PEER;
-    L.batch0 = static_cast<std::uint32_t>(batches.size());
-    L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
-    // work items inside a batch: ~32 per slot so all 8 warps of the lane's
-    // CTA share even a small (L2-resident) slot
-    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / 32, 4096, 65536);
-    for (std::size_t b = 0; b < lb.batches.size(); ++b) {
-      const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
-      rs_batch_desc Bd{};
-      Bd.pack0 = static_cast<std::uint32_t>(frames.size());
-      if (tx_local)
-        for (const auto& f : lb.batches[b])
-          append_copy(frames, addr(f.se->ptr), f.se->view, slot_addr + f.off, f.region, f.region, f.eb,
-                      static_cast<std::uint32_t>(f.layer));
-      for (const auto& f : lb.batches[b]) {
-        const std::uint64_t n = static_cast<std::uint64_t>(f.region.element_count() * f.eb);
-        Bd.bytes += n;
-        Bd.extent = std::max(Bd.extent, f.off + n);
-      }
-      Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
-      Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
-      Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
-      if (rx_local)
-        for (const auto& f : lb.batches[b])
-          append_copy(frames, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
-                      f.eb, static_cast<std::uint32_t>(f.layer));
-      Bd.nunpack = static_cast<std::uint32_t>(frames.size()) - Bd.unpack0;
-      Bd.unpack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.unpack0, 0, frame_item));
-      batches.push_back(Bd);
-    }
-    all_lanes.push_back(L);
-  }
-  for (std::size_t d = 0; d < devices_.size(); ++d) {
-    DeviceProgram& p = programs_[d];
-    const int slot = devices_[d].slot;
-    p.batches = batches;
-    p.frames = frames;
-    p.lanes.clear();
-    for (std::size_t i = 0; i < lanes.size(); ++i)
-      if (lanes[i].sslot == slot) p.lanes.push_back(all_lanes[i]);
-    p.ntx = static_cast<int>(p.lanes.size());
-    for (std::size_t i = 0; i < lanes.size(); ++i)
-      if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);
-    p.nrx = static_cast<int>(p.lanes.size()) - p.ntx;
-  }
 }
 
 // RS_COPY_CE comparator: every descriptor whose items fall in [b, e) as
@@ -1323,233 +873,5 @@ rs_exec_report Engine::run() {
 }
 
 // ------------------------------------------------------------ live handoff
-
-// Drain -> transfer -> swap, the Switch phase of generation.cpp:239-290 with
-// each piece executed instead of priced.  The drain is a stream-order wait on
-// the caller's iteration-boundary events, so no host thread blocks on the
-// training stream and the transfer starts the instant the last one fires.
-rs_switch_stats Engine::switch_step(void* const* drain_events, bool swap) {
-  if (!prepared_) throw DomainError("switch: prepare the handoff plan first (Prepare phase)");
-  rs_switch_stats st{};
-  for (std::size_t d = 0; d < devices_.size(); ++d) {
-    DeviceGuard g(devices_[d].ordinal);
-    cuda_check(cudaEventRecord(devices_[d].ev_call, devices_[d].stream), "event");
-    if (drain_events && drain_events[d])
-      cuda_check(cudaStreamWaitEvent(devices_[d].stream, static_cast<cudaEvent_t>(drain_events[d]), 0),
-                 "drain wait");
-  }
-  st.exec = run();  // records ev_begin behind the drain waits
-  for (auto& dv : devices_) {
-    DeviceGuard g(dv.ordinal);
-    float ms = 0;
-    cuda_check(cudaEventElapsedTime(&ms, dv.ev_call, dv.ev_begin), "elapsed");
-    st.drain_ms = std::max(st.drain_ms, static_cast<double>(ms));
-  }
-  st.transfer_ms = st.exec.device_ms;
-  st.transfer_bytes = planned_total_bytes_;
-  if (st.exec.ok && swap) {
-    const auto t0 = std::chrono::steady_clock::now();
-    swap_stores();
-    st.swap_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    st.swapped = 1;
-  }
-  st.pause_ms = st.drain_ms + st.transfer_ms + st.swap_ms;
-  return st;
-}
-
-void Engine::swap_stores() {
-  std::swap(stores_[RS_SRC], stores_[RS_DST]);
-  prepared_ = false;  // compiled descriptors point into the old roles
-  prepared_id_ = 0;
-}
-
-// Host<->device copies of a set of store entries, merged into runs: entries
-// that are back to back in the device arena AND in the caller's host buffers
-// become one copy (never touching a byte outside the entries), cut into
-// <= 256 MiB pieces.  Thousands of per-shard copies cap concurrent H2D + D2H
-// at 65 GB/s on a B200 host; merged runs reach 96 GB/s
-// (profiles/r1/e2e_probe2.json).
-void Engine::copy_runs(const Store& s, const std::vector<std::size_t>& idx, void* const* host, bool to_device) {
-  struct Piece {
-    char* dev;
-    char* hst;
-    std::size_t n;
-    int local;
-  };
-  std::vector<Piece> ps;
-  ps.reserve(idx.size());
-  for (std::size_t k : idx) {
-    const Entry& e = s.entries[k];
-    if (!e.nbytes) continue;
-    ps.push_back({e.ptr, static_cast<char*>(host[k]), static_cast<std::size_t>(e.nbytes), local_of(e.slot)});
-  }
-  std::sort(ps.begin(), ps.end(), [](const Piece& a, const Piece& b) {
-    return a.local != b.local ? a.local < b.local : a.dev < b.dev;
-  });
-  std::vector<Piece> runs;
-  for (const Piece& p : ps) {
-    if (!runs.empty()) {
-      Piece& r = runs.back();
-      if (r.local == p.local && p.dev == r.dev + r.n && p.hst == r.hst + r.n) {
-        r.n += p.n;
-        continue;
-      }
-    }
-    runs.push_back(p);
-  }
-  constexpr std::size_t kPiece = 256u << 20;
-  for (const Piece& r : runs) {
-    const Device& dv = devices_[static_cast<std::size_t>(r.local)];
-    DeviceGuard g(dv.ordinal);
-    for (std::size_t off = 0; off < r.n; off += kPiece) {
-      const std::size_t n = std::min(kPiece, r.n - off);
-      if (to_device)
-        cuda_check(cudaMemcpyAsync(r.dev + off, r.hst + off, n, cudaMemcpyHostToDevice, dv.h2d), "H2D");
-      else
-        cuda_check(cudaMemcpyAsync(r.hst + off, r.dev + off, n, cudaMemcpyDeviceToHost, dv.d2h), "D2H");
-    }
-  }
-}
-
-rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, int window_layers) {
-  (void)window_layers;
-  if (!prepared_) throw DomainError("engine: prepare a plan first");
-  const auto t0 = std::chrono::steady_clock::now();
-  const Store& S = stores_[RS_SRC];
-  const Store& D = stores_[RS_DST];
-  if (window_layers_ > 0 && opts_.mode != RS_MODE_DIRECT)
-    throw DomainError("windowed host-store execution runs in RS_MODE_DIRECT");
-  if (opts_.mode != RS_MODE_DIRECT) {
-    // staged transfers run as one launch: stage everything in, run, stage out
-    for (std::size_t k = 0; k < S.entries.size(); ++k) {
-      const Entry& e = S.entries[k];
-      const int l = local_of(e.slot);
-      if (l < 0) continue;
-      const Device& dv = devices_[static_cast<std::size_t>(l)];
-      DeviceGuard g(dv.ordinal);
-      cuda_check(cudaMemcpyAsync(e.ptr, host_src[k], static_cast<std::size_t>(e.nbytes), cudaMemcpyHostToDevice,
-                                 dv.stream), "H2D");
-    }
-    rs_exec_report rep = run();
-    for (std::size_t k = 0; k < D.entries.size(); ++k) {
-      const Entry& e = D.entries[k];
-      const int l = local_of(e.slot);
-      if (l < 0) continue;
-      const Device& dv = devices_[static_cast<std::size_t>(l)];
-      DeviceGuard g(dv.ordinal);
-      cuda_check(cudaMemcpyAsync(host_dst[k], e.ptr, static_cast<std::size_t>(e.nbytes), cudaMemcpyDeviceToHost,
-                                 dv.stream), "D2H");
-    }
-    for (auto& dv : devices_) {
-      DeviceGuard g(dv.ordinal);
-      cuda_check(cudaStreamSynchronize(dv.stream), "D2H");
-    }
-    rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return rep;
-  }
-
-  // DIRECT: layer pipeline over three streams per device.  Layer l's source
-  // shards go H2D (h2d stream), its copy kernel waits for them (compute
-  // stream), its destination shards go D2H once every local device finished
-  // layer l (d2h stream) -- H2D of l+1, the kernel of l and D2H of l-1
-  // overlap and PCIe runs full duplex.  Layers are the plan's
-  // (executor.cpp:134-138).
-  rs_exec_report rep = planned_;
-  const std::size_t nlayers = programs_.empty() ? 0 : programs_[0].layers.size();
-  const std::size_t ndev = devices_.size();
-  std::map<int, std::size_t> slot_of_layer;
-  for (std::size_t li = 0; li < nlayers; ++li) slot_of_layer[programs_[0].layers[li].layer] = li;
-  std::vector<std::vector<std::size_t>> src_by_layer(nlayers), dst_by_layer(nlayers);
-  for (std::size_t k = 0; k < S.entries.size(); ++k) {
-    auto it = slot_of_layer.find(S.model.tensors[S.entries[k].ti].layer);
-    if (it != slot_of_layer.end() && local_of(S.entries[k].slot) >= 0) src_by_layer[it->second].push_back(k);
-  }
-  for (std::size_t k = 0; k < D.entries.size(); ++k) {
-    auto it = slot_of_layer.find(D.model.tensors[D.entries[k].ti].layer);
-    if (it != slot_of_layer.end() && local_of(D.entries[k].slot) >= 0) dst_by_layer[it->second].push_back(k);
-  }
-  std::vector<cudaEvent_t> ev_in(nlayers * ndev), ev_done(nlayers * ndev), ev_out(nlayers * ndev);
-  for (std::size_t d = 0; d < ndev; ++d) {
-    DeviceGuard g(devices_[d].ordinal);
-    for (std::size_t li = 0; li < nlayers; ++li) {
-      cuda_check(cudaEventCreateWithFlags(&ev_in[li * ndev + d], cudaEventDisableTiming), "event");
-      cuda_check(cudaEventCreateWithFlags(&ev_done[li * ndev + d], cudaEventDisableTiming), "event");
-      cuda_check(cudaEventCreateWithFlags(&ev_out[li * ndev + d], cudaEventDisableTiming), "event");
-    }
-    cuda_check(cudaEventRecord(devices_[d].ev_begin, devices_[d].h2d), "event");
-  }
-  // Windowed stores: layer l reuses the device slot of the last earlier plan
-  // layer with the same (l % window); its H2D waits for that layer's D2H.
-  std::vector<long> reuse_of(nlayers, -1);
-  if (window_layers_ > 0) {
-    std::map<int, std::size_t> last_in_slot;
-    for (std::size_t li = 0; li < nlayers; ++li) {
-      const int w = programs_[0].layers[li].layer % window_layers_;
-      if (auto it = last_in_slot.find(w); it != last_in_slot.end()) reuse_of[li] = static_cast<long>(it->second);
-      last_in_slot[w] = li;
-    }
-  }
-  // One interleaved enqueue loop (an event must be recorded before a stream
-  // waits on it): H2D(l) -> kernel(l) -> D2H(l), three streams per device.
-  int launches = 0;
-  for (std::size_t li = 0; li < nlayers; ++li) {
-    if (reuse_of[li] >= 0)
-      for (std::size_t d = 0; d < ndev; ++d) {
-        DeviceGuard g(devices_[d].ordinal);
-        cuda_check(cudaStreamWaitEvent(devices_[d].h2d, ev_out[static_cast<std::size_t>(reuse_of[li]) * ndev + d], 0),
-                   "wait");
-      }
-    copy_runs(S, src_by_layer[li], host_src, true);
-    for (std::size_t d = 0; d < ndev; ++d) {
-      DeviceGuard g(devices_[d].ordinal);
-      cuda_check(cudaEventRecord(ev_in[li * ndev + d], devices_[d].h2d), "event");
-    }
-    for (std::size_t d = 0; d < ndev; ++d) {
-      DeviceProgram& p = programs_[d];
-      const LayerRange& lr = p.layers[li];
-      DeviceGuard g(devices_[d].ordinal);
-      for (std::size_t o = 0; o < ndev; ++o)
-        cuda_check(cudaStreamWaitEvent(devices_[d].stream, ev_in[li * ndev + o], 0), "wait");
-      if (lr.item_end > lr.item_begin) {
-        cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
-                                  reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
-                                  static_cast<std::uint32_t>(p.local.size()), lr.item_begin, lr.item_end,
-                                  copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)),
-                                  devices_[d].stream),
-                   "copy kernel launch");
-        ++launches;
-      }
-      cuda_check(cudaEventRecord(ev_done[li * ndev + d], devices_[d].stream), "event");
-    }
-    for (std::size_t d = 0; d < ndev; ++d) {
-      DeviceGuard g(devices_[d].ordinal);
-      for (std::size_t o = 0; o < ndev; ++o)
-        cuda_check(cudaStreamWaitEvent(devices_[d].d2h, ev_done[li * ndev + o], 0), "wait");
-    }
-    copy_runs(D, dst_by_layer[li], host_dst, false);
-    for (std::size_t d = 0; d < ndev; ++d) {
-      DeviceGuard g(devices_[d].ordinal);
-      cuda_check(cudaEventRecord(ev_out[li * ndev + d], devices_[d].d2h), "event");
-    }
-  }
-  double worst = 0;
-  for (auto& dv : devices_) {
-    DeviceGuard g(dv.ordinal);
-    cuda_check(cudaEventRecord(dv.ev_end, dv.d2h), "event");
-    cuda_check(cudaEventSynchronize(dv.ev_end), "host-store reshard");
-    float ms = 0;
-    cuda_check(cudaEventElapsedTime(&ms, dv.ev_begin, dv.ev_end), "elapsed");
-    worst = std::max(worst, static_cast<double>(ms));
-  }
-  for (std::size_t i = 0; i < ev_in.size(); ++i) {
-    cudaEventDestroy(ev_in[i]);
-    cudaEventDestroy(ev_done[i]);
-    cudaEventDestroy(ev_out[i]);
-  }
-  rep.device_ms = worst;
-  rep.kernel_launches = launches;
-  rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return rep;
-}
 
 }  // namespace rsb

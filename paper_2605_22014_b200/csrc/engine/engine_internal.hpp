@@ -1,0 +1,55 @@
+// Internal helpers shared by the engine's translation units (engine.cpp,
+// engine_staged.cpp, engine_host.cpp).  Not part of any public interface.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "engine.hpp"
+
+namespace rsb {
+namespace detail {
+
+constexpr std::size_t kAlign = 256;
+constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
+constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
+constexpr std::uint64_t kSpinLimit = 200000000ull;
+
+inline std::uint64_t key(int rank, std::uint32_t ti) {
+  return (static_cast<std::uint64_t>(ti) << 32) | static_cast<std::uint32_t>(rank);
+}
+
+inline std::size_t align_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+inline std::string escape_msg(const char* who, const reshard::ShardView& b, const reshard::ShardView& owner) {
+  return std::string(who) + ": bounds " + b.to_string() + " escape owner view " + owner.to_string();
+}
+
+inline std::string no_buffer(int rank, std::uint32_t ti) {
+  return "shard store: no buffer for rank " + std::to_string(rank) + " tensor " + std::to_string(ti);
+}
+
+inline std::uint64_t addr(const char* p) { return reinterpret_cast<std::uint64_t>(p); }
+
+
+// Pointer of an entry that local work must touch.
+inline char* need_ptr(const Entry* e, const char* what) {
+  if (!e->ptr)
+    throw DomainError(std::string(what) + " shard rank " + std::to_string(e->rank) + " tensor " +
+                      std::to_string(e->ti) + " on slot " + std::to_string(e->slot) +
+                      " is not mapped in this process (rs_arena_import)");
+  return e->ptr;
+}
+
+}  // namespace detail
+}  // namespace rsb

@@ -1,0 +1,427 @@
+// STAGED mode: ring geometry, the staging (comm) arena and the compilation
+// of a plan into ring lanes / batches / frames for rs_exchange_kernel.
+// Bounded staging like the reference's executor (proj/src/executor.cpp:183-206):
+// chunk_bounds cuts tasks to the ring slot size, a destination rank's rings
+// live in its budget B.
+#include <algorithm>
+#include <map>
+#include <set>
+
+#include "engine.hpp"
+#include "compile.hpp"
+#include "engine_internal.hpp"
+#include "kernels.h"
+
+namespace rsb {
+
+using namespace detail;
+
+std::size_t Engine::comm_bytes(int slot) const {
+  if (comm_layout_valid_) return comm_layout_.slot_bytes.at(static_cast<std::size_t>(slot));
+  return make_comm_layout(nullptr).slot_bytes.at(static_cast<std::size_t>(slot));
+}
+
+void Engine::comm_alloc() {
+  if (!stores_[RS_DST].laid_out) throw DomainError("comm: lay out the dst store first");
+  comm_layout_ = make_comm_layout(nullptr);
+  comm_layout_valid_ = true;
+  alloc_comm_arenas();
+}
+
+// Plan-sized rings: each dst rank's region holds exactly its rings (<= B),
+// so resident staging is what the rings use, not B per rank.
+void Engine::comm_alloc_plan(const reshard::TransferPlan& plan) {
+  if (!stores_[RS_DST].laid_out || !stores_[RS_SRC].laid_out) throw DomainError("comm: lay out both stores first");
+  const RingGeometry geo = ring_geometry(plan);
+  comm_layout_ = make_comm_layout(&geo.ring_bytes_of);
+  comm_layout_valid_ = true;
+  alloc_comm_arenas();
+}
+
+void Engine::alloc_comm_arenas() {
+  comm_.clear();
+  for (const auto& dv : devices_) {
+    const std::size_t n = comm_bytes(dv.slot);
+    comm_.emplace_back(dv.ordinal, n);
+    DeviceGuard g(dv.ordinal);
+    cuda_check(cudaMemset(comm_.back().data(), 0, n), "comm memset");
+  }
+  prepared_ = false;
+}
+
+char* Engine::comm_base(int slot) const {
+  const int l = local_of(slot);
+  if (l >= 0) return static_cast<std::size_t>(l) < comm_.size() ? comm_[static_cast<std::size_t>(l)].data() : nullptr;
+  const auto& imp = comm_imported_[static_cast<std::size_t>(slot)];
+  return imp ? imp->data() : nullptr;
+}
+
+// Ring geometry of a plan (STAGED): lanes per link, slot size and ring bytes
+// per destination rank.  Deterministic from the plan and the layouts, so
+// every process computes the same rings for every slot.
+Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) const {
+  const Store& src = stores_[RS_SRC];
+  const Store& dst = stores_[RS_DST];
+  const std::int64_t B = opts_.staging_bytes;
+  const int K = opts_.slots_per_link;
+  RingGeometry geo;
+  // inbound links per destination rank (remote tasks only)
+  std::map<int, std::set<int>> inbound;
+  for (const auto& kv : plan.tasks_by_layer)
+    for (const auto& t : kv.second)
+      if (!t.is_local()) inbound[t.dst_rank].insert(t.src_rank);
+
+  // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
+  // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
+  // the sender + receiver CTAs of the busiest slot stop being co-resident.
+  // Automatic choice: lanes proportional to each link's bytes (a link's
+  // lanes finish together, so the launch ends when the heaviest link does),
+  // scaled so every slot's sender + receiver lanes fit 3/4 of one device's
+  // CTA capacity, at least one and at most 32 per link (same answer on every
+  // process: the plan and the placement are global).
+  std::map<std::pair<int, int>, std::uint64_t> link_bytes;
+  for (const auto& kv : plan.tasks_by_layer)
+    for (const auto& t : kv.second)
+      if (!t.is_local()) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
+  auto& lanes_of = geo.lanes_of;
+  if (opts_.lanes_per_link > 0) {
+    for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
+  } else if (!link_bytes.empty()) {
+    auto slot_of = [&](const Store& s, int rank) {
+      for (const auto& e : s.entries)
+        if (e.rank == rank) return e.slot;
+      return 0;
+    };
+    std::map<int, int> src_slot, dst_slot;
+    std::vector<std::uint64_t> slot_bytes(static_cast<std::size_t>(nslots_), 0);
+    for (const auto& [lk, b] : link_bytes) {
+      if (!src_slot.count(lk.first)) src_slot[lk.first] = slot_of(src, lk.first);
+      if (!dst_slot.count(lk.second)) dst_slot[lk.second] = slot_of(dst, lk.second);
+      slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
+      slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
+    }
+    const int capacity = grid_for(0, exchange_kernel_id()) * 3 / 4;
+    const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
+    const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
+    std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
+    for (const auto& [lk, b] : link_bytes) {
+      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, 32);
+      lanes_of[lk] = n;
+      slot_lanes[static_cast<std::size_t>(src_slot[lk.first])] += n;
+      slot_lanes[static_cast<std::size_t>(dst_slot[lk.second])] += n;
+    }
+    // the max(1, .) floor can overshoot a slot with many light links: trim
+    // the widest links touching it
+    for (int sl = 0; sl < nslots_; ++sl)
+      while (slot_lanes[static_cast<std::size_t>(sl)] > capacity) {
+        std::pair<int, int> widest{-1, -1};
+        int w = 1;
+        for (const auto& [lk, n] : lanes_of)
+          if ((src_slot[lk.first] == sl || dst_slot[lk.second] == sl) && n > w) {
+            w = n;
+            widest = lk;
+          }
+        if (widest.first < 0) break;  // every link at one lane: the launch check reports it
+        --lanes_of[widest];
+        --slot_lanes[static_cast<std::size_t>(src_slot[widest.first])];
+        --slot_lanes[static_cast<std::size_t>(dst_slot[widest.second])];
+      }
+  }
+  // Ring slot size per dst rank: B split over its inbound lanes, capped at
+  // 128 KiB by default -- B is the budget, not the target footprint.  At
+  // 64-128 KiB the rings stay (almost) entirely in L2: DRAM traffic of the
+  // exchange kernel = the 2x floor (profiles/r1/ring_traffic/).  With
+  // GPU-scope handshakes for same-device lanes, 128-256 KiB slots x K = 2
+  // keep the rings small enough to stay largely L2-resident (less HBM
+  // traffic than the 4x of a DRAM-resident ring) while a batch is still long
+  // against its handshake; 32 KiB slots pay the handshake, >= 1 MiB slots
+  // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).  The kernel adds
+  // evict-first / evict-last L2 policies and discards drained slots by
+  // default (ring_sweep_v4.jsonl: 15.4 -> 13.1 ms on the C5 slice).
+  const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
+                                 : opts_.ring_slot_kib == 0 ? kRingSlotDefault
+                                                            : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
+  auto& inbound_lanes = geo.inbound_lanes;
+  for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
+  auto& slot_bytes_of = geo.slot_bytes_of;
+  for (const auto& [d, srcs] : inbound) {
+    std::uint64_t sb = static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(K));
+    sb = std::min(sb, slot_cap);
+    slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
+    geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(K);
+  }
+
+  return geo;
+}
+
+// Comm arena layout over every slot: the dst ranks of a slot in ascending
+// order, each with `ring_bytes[rank]` (plan-sized) or B bytes, then the flags.
+Engine::CommLayout Engine::make_comm_layout(const std::map<int, std::uint64_t>* ring_bytes) const {
+  CommLayout L;
+  L.regions.resize(static_cast<std::size_t>(nslots_));
+  L.slot_bytes.assign(static_cast<std::size_t>(nslots_), kFlagBytes);
+  std::map<int, std::set<int>> ranks_on_slot;
+  for (const auto& e : stores_[RS_DST].entries) ranks_on_slot[e.slot].insert(e.rank);
+  for (const auto& [slot, ranks] : ranks_on_slot) {
+    std::size_t off = 0;
+    for (int r : ranks) {
+      std::size_t b = static_cast<std::size_t>(opts_.staging_bytes);
+      if (ring_bytes) {
+        auto it = ring_bytes->find(r);
+        b = it == ring_bytes->end() ? 0 : align_up(static_cast<std::size_t>(it->second), kAlign);
+      }
+      L.regions[static_cast<std::size_t>(slot)][r] = {off, b};
+      off += b;
+    }
+    L.slot_bytes[static_cast<std::size_t>(slot)] = off + kFlagBytes;
+  }
+  return L;
+}
+
+void Engine::compile_staged(const reshard::TransferPlan& plan) {
+  const Store& src = stores_[RS_SRC];
+  const Store& dst = stores_[RS_DST];
+  const auto& m = src.model;
+  const std::int64_t B = opts_.staging_bytes;
+  const int K = opts_.slots_per_link;
+
+  const RingGeometry geo = ring_geometry(plan);
+  const auto& lanes_of = geo.lanes_of;
+  const auto& slot_bytes_of = geo.slot_bytes_of;
+  const auto& inbound_lanes = geo.inbound_lanes;
+  // each destination rank's region in its slot's comm arena (the layout the
+  // arena was allocated with: B per rank, or plan-sized, rs_comm_alloc_plan)
+  std::map<int, std::size_t> region_of, region_bytes;
+  for (std::size_t sl = 0; sl < comm_layout_.regions.size(); ++sl)
+    for (const auto& [r, ob] : comm_layout_.regions[sl]) {
+      region_of[r] = ob.first;
+      region_bytes[r] = ob.second;
+    }
+
+  struct Frame {
+    const Entry* se;
+    const Entry* de;
+    reshard::ShardView region;
+    std::int64_t eb;
+    std::uint64_t off;
+    int layer;
+  };
+  struct LaneBuild {
+    int src_rank, dst_rank, sslot, dslot;
+    std::uint64_t slot_bytes;
+    std::vector<std::vector<Frame>> batches;
+    std::uint64_t fill = 0;
+  };
+  std::vector<LaneBuild> lanes;
+  std::map<std::pair<int, int>, int> link_first_lane, link_cursor;
+
+  std::vector<std::size_t> mark(devices_.size());
+  for (int layer : plan_layers_) {
+    for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
+    std::vector<std::size_t> lane_mark_batches(lanes.size()), lane_mark_frames(lanes.size());
+    std::vector<std::uint64_t> lane_mark_fill(lanes.size());
+    for (std::size_t i = 0; i < lanes.size(); ++i) {
+      lane_mark_batches[i] = lanes[i].batches.size();
+      lane_mark_fill[i] = lanes[i].fill;
+      lane_mark_frames[i] = lanes[i].batches.empty() ? 0 : lanes[i].batches.back().size();
+    }
+    const std::size_t lanes_before = lanes.size();
+    rs_exec_report delta{};
+    auto local_copy = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb) {
+      const int l = local_of(se->slot);
+      if (l < 0) return;
+      append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
+                  addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
+    };
+    try {
+      if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end()) {
+        for (const auto& k : it->second) {
+          const Entry* se = src.find(k.rank, k.tensor_index);
+          const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
+          if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
+          if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
+          if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
+          const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
+          local_copy(se, de, k.bounds, eb);
+          delta.carryover_bytes += k.bounds.element_count() * eb;
+        }
+      }
+      if (auto it = plan.tasks_by_layer.find(layer); it != plan.tasks_by_layer.end()) {
+        for (const auto& t : it->second) {
+          const Entry* se = src.find(t.src_rank, t.tensor_index);
+          if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
+          if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
+          const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
+          if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
+          const Entry* de = dst.find(t.dst_rank, t.tensor_index);
+          if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
+          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
+          if (t.is_local()) {
+            local_copy(se, de, t.bounds, eb);
+            delta.local_copy_bytes += t.bounds.element_count() * eb;
+            continue;
+          }
+          const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);
+          if (static_cast<std::uint64_t>(eb) > sb)
+            throw IntegrityError("staging: ring slot of " + std::to_string(sb) + " bytes cannot hold one element (B=" +
+                                 std::to_string(B) + " over " + std::to_string(inbound_lanes.at(t.dst_rank)) +
+                                 " inbound links)");
+          const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
+          const auto lk = std::make_pair(t.src_rank, t.dst_rank);
+          const int P = lanes_of.at(lk);
+          if (!link_first_lane.count(lk)) {
+            link_first_lane[lk] = static_cast<int>(lanes.size());
+            for (int p = 0; p < P; ++p) lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, {}, 0});
+          }
+          for (const auto& c : chunks) {
+            int& cur = link_cursor[lk];
+            LaneBuild& lb = lanes[static_cast<std::size_t>(link_first_lane[lk] + cur)];
+            cur = (cur + 1) % P;
+            const std::uint64_t n = static_cast<std::uint64_t>(c.element_count() * eb);
+            std::uint64_t off = align_up(lb.fill, 16);
+            if (lb.batches.empty() || off + n > lb.slot_bytes) {
+              lb.batches.emplace_back();
+              off = 0;
+            }
+            lb.batches.back().push_back({se, de, c, eb, off, layer});
+            lb.fill = off + n;
+          }
+          delta.bytes_moved += t.bounds.element_count() * eb;
+        }
+      }
+    } catch (const std::exception& e) {
+      if (dynamic_cast<const DomainError*>(&e)) throw;  // mapping errors are not plan integrity
+      for (std::size_t d = 0; d < devices_.size(); ++d) programs_[d].local.resize(mark[d]);
+      lanes.resize(lanes_before);
+      for (std::size_t i = 0; i < lanes_before; ++i) {
+        lanes[i].batches.resize(lane_mark_batches[i]);
+        if (!lanes[i].batches.empty()) lanes[i].batches.back().resize(lane_mark_frames[i]);
+        lanes[i].fill = lane_mark_fill[i];
+      }
+      for (auto it = link_first_lane.begin(); it != link_first_lane.end();)
+        it = it->second >= static_cast<int>(lanes_before) ? link_first_lane.erase(it) : std::next(it);
+      planned_.ok = 0;
+      planned_.failed_layer = layer;
+      std::snprintf(planned_.error, sizeof planned_.error, "%s", e.what());
+      break;
+    }
+    planned_.carryover_bytes += delta.carryover_bytes;
+    planned_.local_copy_bytes += delta.local_copy_bytes;
+    planned_.bytes_moved += delta.bytes_moved;
+    planned_.layers_processed++;
+    for (std::size_t d = 0; d < devices_.size(); ++d)
+      programs_[d].layers.push_back({layer, mark[d], programs_[d].local.size()});
+  }
+  if (planned_.failed_layer < 0) planned_.ok = 1;
+
+  // Ring memory inside the comm arenas (deterministic on every process):
+  // a destination rank's lanes take consecutive K-slot rings in its B region;
+  // ready flags in the destination slot's flag area, credit flags in the
+  // source slot's.
+  std::map<int, std::uint64_t> ring_used;  // dst rank -> bytes used in its region
+  std::vector<std::size_t> flag_used(static_cast<std::size_t>(nslots_), 0);
+  const std::size_t flags_per_lane = align_up(sizeof(std::uint64_t) * static_cast<std::size_t>(K), 64);
+  struct LaneAddr {
+    std::uint64_t ring_off, ready_off, credit_off;
+  };
+  std::vector<LaneAddr> where(lanes.size());
+  for (std::size_t i = 0; i < lanes.size(); ++i) {
+    const auto& lb = lanes[i];
+    std::uint64_t& used = ring_used[lb.dst_rank];
+    auto reg = region_of.find(lb.dst_rank);
+    if (reg == region_of.end())
+      throw DomainError("staged: comm arena has no ring region for dst rank " + std::to_string(lb.dst_rank) +
+                        "; re-run rs_comm_alloc for this dst layout");
+    where[i].ring_off = reg->second + used;
+    used += lb.slot_bytes * static_cast<std::uint64_t>(K);
+    if (used > region_bytes.at(lb.dst_rank))
+      throw DomainError("staged: ring region of dst rank " + std::to_string(lb.dst_rank) + " (" +
+                        std::to_string(region_bytes.at(lb.dst_rank)) + " bytes) is smaller than this plan's rings; " +
+                        "re-run rs_comm_alloc_plan with this plan");
+    auto& fr = flag_used[static_cast<std::size_t>(lb.dslot)];
+    auto& fc = flag_used[static_cast<std::size_t>(lb.sslot)];
+    if (fr + flags_per_lane > kFlagBytes || fc + flags_per_lane > kFlagBytes)
+      throw DomainError("staged: too many ring lanes for the flag area; lower lanes_per_link");
+    where[i].ready_off = fr;
+    fr += flags_per_lane;
+    where[i].credit_off = fc;
+    fc += flags_per_lane;
+    planned_.peak_staging_bytes = std::max<std::int64_t>(planned_.peak_staging_bytes, static_cast<std::int64_t>(used));
+  }
+  auto flag_base = [&](int slot) -> char* {
+    char* b = comm_base(slot);
+    const std::size_t ring_area = comm_bytes(slot) - kFlagBytes;
+    return b ? b + ring_area : nullptr;
+  };
+
+  // serialise lanes / batches / frames (global tables, uploaded to every local device)
+  std::vector<rs_lane_desc> all_lanes;
+  std::vector<rs_batch_desc> batches;
+  std::vector<rs_copy_desc> frames;
+  for (std::size_t i = 0; i < lanes.size(); ++i) {
+    const auto& lb = lanes[i];
+    const bool tx_local = local_of(lb.sslot) >= 0, rx_local = local_of(lb.dslot) >= 0;
+    char* ring = comm_base(lb.dslot);
+    char* ready = flag_base(lb.dslot);
+    char* credit = flag_base(lb.sslot);
+    if ((tx_local || rx_local) && (!ring || !ready || !credit))
+      throw DomainError("staged: comm arena of slot " + std::to_string(tx_local ? lb.dslot : lb.sslot) +
+                        " not mapped in this process (rs_arena_import RS_COMM)");
+    const std::uint64_t ring_addr = ring ? addr(ring) + where[i].ring_off : 0;
+    rs_lane_desc L{};
+    L.slot_base = L.slot_base_rx = ring_addr;
+    L.slot_bytes = lb.slot_bytes;
+    L.ready_flags = L.ready_flags_rx = ready ? addr(ready) + where[i].ready_off : 0;
+    L.credit_flags = L.credit_flags_tx = credit ? addr(credit) + where[i].credit_off : 0;
+    L.slots = static_cast<std::uint32_t>(K);
+    // GPU-scope synchronisation only when both ends are this process's same
+    // slot; every cross-slot lane (another GPU, or another process sharing a
+    // GPU through IPC) synchronises at system scope
+    L.flags = lb.sslot == lb.dslot ? 0u : RS_LANE_PEER;
+    L.batch0 = static_cast<std::uint32_t>(batches.size());
+    L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
+    // work items inside a batch: ~32 per slot so all 8 warps of the lane's
+    // CTA share even a small (L2-resident) slot
+    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / 32, 4096, 65536);
+    for (std::size_t b = 0; b < lb.batches.size(); ++b) {
+      const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
+      rs_batch_desc Bd{};
+      Bd.pack0 = static_cast<std::uint32_t>(frames.size());
+      if (tx_local)
+        for (const auto& f : lb.batches[b])
+          append_copy(frames, addr(f.se->ptr), f.se->view, slot_addr + f.off, f.region, f.region, f.eb,
+                      static_cast<std::uint32_t>(f.layer));
+      for (const auto& f : lb.batches[b]) {
+        const std::uint64_t n = static_cast<std::uint64_t>(f.region.element_count() * f.eb);
+        Bd.bytes += n;
+        Bd.extent = std::max(Bd.extent, f.off + n);
+      }
+      Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
+      Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
+      Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
+      if (rx_local)
+        for (const auto& f : lb.batches[b])
+          append_copy(frames, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
+                      f.eb, static_cast<std::uint32_t>(f.layer));
+      Bd.nunpack = static_cast<std::uint32_t>(frames.size()) - Bd.unpack0;
+      Bd.unpack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.unpack0, 0, frame_item));
+      batches.push_back(Bd);
+    }
+    all_lanes.push_back(L);
+  }
+  for (std::size_t d = 0; d < devices_.size(); ++d) {
+    DeviceProgram& p = programs_[d];
+    const int slot = devices_[d].slot;
+    p.batches = batches;
+    p.frames = frames;
+    p.lanes.clear();
+    for (std::size_t i = 0; i < lanes.size(); ++i)
+      if (lanes[i].sslot == slot) p.lanes.push_back(all_lanes[i]);
+    p.ntx = static_cast<int>(p.lanes.size());
+    for (std::size_t i = 0; i < lanes.size(); ++i)
+      if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);
+    p.nrx = static_cast<int>(p.lanes.size()) - p.ntx;
+  }
+}
+
+}  // namespace rsb
