@@ -1,5 +1,6 @@
 // Device work descriptors shared by the host descriptor compiler
-// (compile.cpp) and the sm_100a kernels (kernels.cu).  Plain C layout.
+// (compile.cpp) and the sm_100a kernels (copy_kernels.cu, exchange_kernel.cu,
+// pattern_kernel.cu).  Plain C layout.
 //
 // A CopyDesc is one strided->strided byte copy of a sub-box between two
 // row-major shard buffers, after dimension coalescing: `rows` contiguous runs

@@ -399,7 +399,7 @@ int Engine::copy_variant(int dev) const {
     case RS_COPY_BULK_MW + 1:
     case RS_COPY_BULK_MW + 2:
     case RS_COPY_BULK_MW + 3:
-    case RS_COPY_BULK_MW + 4:  // issuer-count / ring-shape variants (kernels.cu launch_bulk_mw)
+    case RS_COPY_BULK_MW + 4:  // issuer-count / ring-shape variants (copy_kernels.cu launch_bulk_mw)
       return programs_[static_cast<std::size_t>(dev)].all_aligned ? opts_.copy_kernel : 2;
     case RS_COPY_LDG8: return 2;
     // default: TMA bulk copy over a non-persistent grid when every descriptor is

@@ -1,4 +1,5 @@
-// Host-callable launchers for kernels.cu (C linkage, no templates exposed).
+// Host-callable launchers of copy_kernels.cu, pattern_kernel.cu and
+// exchange_kernel.cu (C linkage, no templates exposed).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -30,6 +31,10 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
 
 // which: 0 LDG4, 3 LDG8, 5 LDG16, 6 CTA8, 4 bulk, 1 pattern, 2/7/8 exchange 256/512/1024 threads
 int rs_kernel_max_blocks_per_sm(int which);
+// per-file occupancy helpers behind rs_kernel_max_blocks_per_sm
+int copy_max_blocks_per_sm(int which);
+int pattern_max_blocks_per_sm(void);
+int exchange_max_blocks_per_sm(int which);
 
 #ifdef __cplusplus
 }
