@@ -40,10 +40,10 @@ def run(case, mode, layers=None):
     eng.layout(RS_SRC, sp, co)
     eng.layout(RS_DST, sp, cn)
     need = eng.store_bytes(RS_SRC) + eng.store_bytes(RS_DST)
-    if mode == "staged":  # B per destination rank of comm arena
-        need += (256 << 20) * len(set(cn.ranks))
+    if mode == "staged":  # plan-sized rings (rs_comm_alloc_plan): tens of MiB per destination rank
+        need += (64 << 20) * len(set(cn.ranks))
     free, _ = torch.cuda.mem_get_info()
-    if need + (2 << 30) > free:
+    if need + (1 << 30) > free:
         eng.close()
         return None
     eng.alloc(RS_SRC)
