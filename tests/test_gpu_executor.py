@@ -434,3 +434,26 @@ def test_warp_specialised_lanes_bitexact(K, cap_kib, mode, golden, oracle_c):
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
             golden["c1_exec"]["1073741824"]["dst_sha"]
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_balanced_sources_same_bytes(mode, golden, oracle_c):
+    """balance_sources (planner.hpp:18, round-robin over DP replicas) changes
+    which replica sends, never the destination bytes: balanced plans execute
+    to the reference's default-plan digests (replicas hold identical state)."""
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    n = 0
+    for seed, sp, co, cn in specs.iter_random_cases(200, golden["random_pairs"]["base_seed"]):
+        if co.dp < 2:
+            continue
+        plan = R.compute_transfer_plan(co, cn, sp, R.PlanOptions(True))
+        eng = make_engine(sp, co, cn, mode, 1 << 16, lanes_per_link=1)
+        rep = R.execute_plan(plan, eng)
+        assert rep["ok"], (seed, rep)
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            rows[seed]["exec"]["4096"]["dst_sha"], seed
+        eng.close()
+        n += 1
+        if n == 30:
+            break
+    assert n >= 10
