@@ -457,3 +457,24 @@ def test_balanced_sources_same_bytes(mode, golden, oracle_c):
         if n == 30:
             break
     assert n >= 10
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_shuffled_plan_text_same_bytes(mode, golden, oracle_c):
+    """SURVEY §4 property: any order of a layer's tasks gives the same bytes.
+    write_plan -> shuffle every task / keep line -> read_plan (re-indexed by
+    tensor name, unlike the reference's first-appearance interning,
+    transfer_plan.cpp:94-101) -> execute: the reference's digest."""
+    import random
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(25, golden["random_pairs"]["base_seed"]):
+        lines = R.compute_transfer_plan(co, cn, sp).text().splitlines()
+        head, body = lines[:1], lines[1:]
+        random.Random(seed).shuffle(body)
+        plan = R.read_plan("\n".join(head + body) + "\n", sp)
+        eng = make_engine(sp, co, cn, mode, 1 << 16, lanes_per_link=1)
+        rep = R.execute_plan(plan, eng)
+        assert rep["ok"], (seed, rep)
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            rows[seed]["exec"]["4096"]["dst_sha"], seed
+        eng.close()
