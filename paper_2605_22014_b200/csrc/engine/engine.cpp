@@ -35,8 +35,12 @@
 namespace rsb {
 
 void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess)
+  if (e != cudaSuccess) {
+    // clear a non-sticky error (e.g. a failed cudaMalloc) so the next launch's
+    // cudaGetLastError does not report it again; sticky faults stay sticky
+    cudaGetLastError();
     throw SystemError(std::string(what) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
+  }
 }
 
 using namespace detail;
