@@ -478,3 +478,21 @@ def test_shuffled_plan_text_same_bytes(mode, golden, oracle_c):
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
             rows[seed]["exec"]["4096"]["dst_sha"], seed
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_tensor_beyond_2_32_elements(mode):
+    """Maximum-size edge: one bf16 tensor of 70001 x 70003 = 4.9 G elements
+    (> 2^32, 9.8 GB) split on axis 1, TP3 -> TP4 (ragged ceil blocks on both
+    sides, every row strided): 64-bit element / byte offsets in the
+    descriptors and the pattern check; every destination byte verified."""
+    ts = [specs.TensorSpec("huge", 0, [70001, 70003], 1, "param", 2)]
+    sp = specs.ModelSpec("huge", 1, ts, 2)
+    co, cn = specs.iota_config(1, 3, 1, 1), specs.iota_config(2, 4, 1, 1)
+    eng = make_engine(sp, co, cn, mode, 1 << 30)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    assert R.verify_plan(plan, co, cn) == []
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["bytes_moved"] + rep["local_copy_bytes"] == plan.total_bytes()
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
