@@ -380,7 +380,12 @@ def ours(args) -> None:
                 "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"],
                 "note": ("the peak is torch copy_ of 2 GiB (MEASURED_PEAKS.json); the TMA bulk copy kernel "
                          "sustains 6.82-6.95 TB/s on a plain contiguous 2-32 GiB copy where copy_ gets "
-                         "6.50-6.69 (profiles/r1/contig_probe.jsonl), so frac can exceed 1")}
+                         "6.50-6.69 (profiles/r1/contig_probe.jsonl), so frac can exceed 1; "
+                         "frac_vs_contiguous_copy compares with the kernel's own contiguous 32 GiB copy")}
+        if args.mode == "direct":
+            contiguous = 6954.0  # profiles/r1/contig_probe.jsonl, TMA-NP, 32 GiB
+            roof["contiguous_copy_gbs"] = contiguous
+            roof["frac_vs_contiguous_copy"] = round(achieved / contiguous, 4)
         if args.mode == "staged":  # with DRAM-resident rings each remote byte costs 2 more
             ring = algo_bytes + 2 * summ["remote_bytes"]
             roof["ring_staged_bytes_per_launch"] = ring
