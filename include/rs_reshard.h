@@ -98,6 +98,8 @@ typedef struct {
                                8 warp-specialised lanes (control-warp event loop);
                                16 (with 8, 256-thread lanes) TMA bulk copies in the copy warps */
   int32_t ring_cta_threads; /* STAGED: threads per ring-lane CTA, 256 / 512 / 1024 (0: default) */
+  int32_t trace;            /* STAGED: 1 = record a per-batch transport trace (rs_trace_read) */
+  int32_t reserved2;
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default: RS_COPY_LDG8_NP */
@@ -289,6 +291,21 @@ int rs_xfer_info(rs_engine* e, int32_t* rounds, int32_t* ntx, int32_t* nrx);
 int rs_xfer_link(rs_engine* e, int32_t dir, int32_t index, int32_t* peer_slot, int32_t* src_rank,
                  int32_t* dst_rank, void** buffer, int64_t* buffer_bytes, int64_t* round_bytes);
 int rs_xfer_step(rs_engine* e, int32_t what, int32_t round);
+
+/* Transport trace of the last STAGED run on local device `device` (engine
+ * created with trace = 1): the RecordingTransport of the reference
+ * (proj/include/reshard/transport.hpp:50-75) on the device -- one record per
+ * (batch, role) this device ran, globaltimer nanoseconds. */
+typedef struct {
+  uint32_t lane;    /* the lane's first batch index */
+  uint32_t batch;   /* batch index within the lane */
+  uint32_t layer;
+  uint32_t role;    /* 0 sender, 1 receiver */
+  uint64_t bytes;
+  uint64_t t_begin; /* flag acquired */
+  uint64_t t_end;   /* flag published */
+} rs_trace_record_t;
+int rs_trace_read(rs_engine* e, int32_t device, rs_trace_record_t* out, int64_t cap, int64_t* count);
 
 /* Page-locked host memory for host shard stores (full-bandwidth H2D/D2H). */
 int rs_host_alloc(size_t bytes, void** out);

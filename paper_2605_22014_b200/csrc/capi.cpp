@@ -481,6 +481,17 @@ int rs_plan_placement(const char* model_spec, const rs_config* c_old, const rs_c
 
 extern "C" {
 
+int rs_trace_read(rs_engine* e, int32_t device, rs_trace_record_t* out, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (!e || !count || cap < 0 || (cap > 0 && !out)) throw std::invalid_argument("bad argument");
+    static_assert(sizeof(rs_trace_record_t) == sizeof(rs_trace_record), "trace record layout");
+    const auto recs = e->impl.trace(device);
+    *count = static_cast<int64_t>(recs.size());
+    const std::size_t n = std::min<std::size_t>(recs.size(), static_cast<std::size_t>(cap));
+    if (n) std::memcpy(out, recs.data(), n * sizeof(rs_trace_record));
+  });
+}
+
 int rs_xfer_info(rs_engine* e, int32_t* rounds, int32_t* ntx, int32_t* nrx) {
   return guarded([&] {
     *rounds = e->impl.xfer_rounds();

@@ -77,4 +77,19 @@ typedef struct {
   uint32_t unpack_items;     // work items over the unpack frames
   uint64_t bytes;            // payload bytes in this batch
   uint64_t extent;           // slot bytes in use (last frame end), for the L2 discard
+  uint32_t layer;            // layer of the batch's frames (trace)
+  uint32_t pad;
 } rs_batch_desc;
+
+// Transport trace (the RecordingTransport of proj/include/reshard/transport.hpp:50-75
+// on the device): one record per (batch, role) of the last STAGED run;
+// globaltimer nanoseconds.  t_end == 0: not recorded (role ran elsewhere).
+typedef struct {
+  uint32_t lane;             // the lane's first batch index (a lane identifier)
+  uint32_t batch;            // batch index within the lane
+  uint32_t layer;
+  uint32_t role;             // 0 sender (pack + publish), 1 receiver (unpack + credit)
+  uint64_t bytes;
+  uint64_t t_begin;          // flag acquired (slot free / data ready)
+  uint64_t t_end;            // flag published
+} rs_trace_record;

@@ -690,6 +690,19 @@ int Engine::ce_copies(const std::vector<rs_copy_desc>& descs, std::uint64_t b, s
   return calls;
 }
 
+std::vector<rs_trace_record> Engine::trace(int dev) const {
+  if (dev < 0 || dev >= num_devices()) throw DomainError("trace: bad local device index");
+  const DeviceProgram& p = programs_.at(static_cast<std::size_t>(dev));
+  if (!opts_.trace || opts_.mode != RS_MODE_STAGED) throw DomainError("trace: create the engine with trace = 1 in STAGED mode");
+  std::vector<rs_trace_record> all(p.d_trace.size() / sizeof(rs_trace_record)), out;
+  if (all.empty()) return out;
+  DeviceGuard g(devices_[static_cast<std::size_t>(dev)].ordinal);
+  cuda_check(cudaMemcpy(all.data(), p.d_trace.data(), p.d_trace.size(), cudaMemcpyDeviceToHost), "trace read");
+  for (const auto& r : all)
+    if (r.t_end) out.push_back(r);
+  return out;
+}
+
 void Engine::upload_programs() {
   for (std::size_t d = 0; d < devices_.size(); ++d) {
     DeviceProgram& p = programs_[d];
@@ -760,6 +773,7 @@ void Engine::upload_programs() {
     if (opts_.mode == RS_MODE_STAGED) {
       p.d_lanes = DeviceBuffer(dv.ordinal, p.lanes.size() * sizeof(rs_lane_desc));
       p.d_batches = DeviceBuffer(dv.ordinal, p.batches.size() * sizeof(rs_batch_desc));
+      if (opts_.trace) p.d_trace = DeviceBuffer(dv.ordinal, 2 * std::max<std::size_t>(1, p.batches.size()) * sizeof(rs_trace_record));
       p.d_frames = DeviceBuffer(dv.ordinal, p.frames.size() * sizeof(rs_copy_desc));
       p.d_error = DeviceBuffer(dv.ordinal, sizeof(unsigned int));
       p.d_lanes.upload(p.lanes.data(), p.lanes.size() * sizeof(rs_lane_desc), dv.stream);
@@ -827,6 +841,8 @@ rs_exec_report Engine::run() {
                           "; lower lanes_per_link");
       if (!p.ntx && !p.nrx && !p.local_items) continue;
       DeviceGuard g(devices_[d].ordinal);
+      if (opts_.trace && p.d_trace.size())
+        cuda_check(cudaMemsetAsync(p.d_trace.data(), 0, p.d_trace.size(), devices_[d].stream), "trace reset");
       const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
       // ring slots in L2: 0 = default (discard + policies), else bit flags (2 = neither)
       const int ring_l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;
@@ -843,7 +859,9 @@ rs_exec_report Engine::run() {
                                     (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | (ring_l2 & 4 ? 4 : 0) |
                                         (ring_l2 & 8 ? 8 : 0) |
                                         ((ring_l2 & 24) == 24 && opts_.ring_cta_threads == 256 ? 16 : 0),
-                                    cap - p.ntx - p.nrx, opts_.ring_cta_threads, devices_[d].stream),
+                                    cap - p.ntx - p.nrx, opts_.ring_cta_threads,
+                                    opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
+                                    devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }

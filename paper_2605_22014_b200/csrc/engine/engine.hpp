@@ -105,7 +105,7 @@ struct DeviceProgram {
   int ntx = 0, nrx = 0;
   std::vector<rs_batch_desc> batches;
   std::vector<rs_copy_desc> frames;
-  DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error;
+  DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error, d_trace;
   std::uint64_t local_bytes = 0;
   bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
   std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)
@@ -156,6 +156,7 @@ class Engine {
   // Live-handoff Switch step (rs_switch): drain -> transfer -> swap.
   rs_switch_stats switch_step(void* const* drain_events, bool swap);
   void swap_stores();
+  std::vector<rs_trace_record> trace(int dev) const;  // STAGED transport trace of the last run
 
   int num_devices() const { return static_cast<int>(devices_.size()); }
   int num_slots() const { return nslots_; }

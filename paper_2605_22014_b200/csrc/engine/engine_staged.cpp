@@ -396,6 +396,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         Bd.bytes += n;
         Bd.extent = std::max(Bd.extent, f.off + n);
       }
+      Bd.layer = lb.batches[b].empty() ? 0u : static_cast<std::uint32_t>(lb.batches[b].front().layer);
       Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
       Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
       Bd.unpack0 = static_cast<std::uint32_t>(frames.size());

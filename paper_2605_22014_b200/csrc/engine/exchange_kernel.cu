@@ -122,6 +122,21 @@ __device__ __forceinline__ bool tma_copy_item(const rs_copy_desc& D, uint64_t lo
   return true;
 }
 
+__device__ __forceinline__ void record_batch(rs_trace_record* trace, const rs_lane_desc& L, const rs_batch_desc& B,
+                                             uint32_t b, uint32_t role, uint64_t t_begin) {
+  uint64_t t_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+  rs_trace_record r;
+  r.lane = L.batch0;
+  r.batch = b;
+  r.layer = B.layer;
+  r.role = role;
+  r.bytes = B.bytes;
+  r.t_begin = t_begin;
+  r.t_end = t_end;
+  trace[2ull * (L.batch0 + b) + role] = r;
+}
+
 // flags of rs_launch_exchange
 constexpr int kExFaultRx = 1;   // test hook: ring receivers drop out (peer failure)
 constexpr int kExDiscard = 2;   // receivers discard drained slot lines from L2
@@ -139,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
     const uint64_t* __restrict__ local_item0, uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-    unsigned int* error_flag, uint64_t spin_limit, int flags) {
+    unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace) {
   const int lane_id = threadIdx.x & 31;
   const int warp_in_block = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
@@ -302,6 +317,8 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
       }
       __syncthreads();
       if (!ok_shared) return;
+      uint64_t t_begin = 0;
+      if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
       if (sender) {
         // pack: the batch's frames copy their source boxes into the slot
         // (remote stores); one flat item space over the frames, dealt to warps
@@ -311,7 +328,10 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
           else warp_copy_item<true, 8>(D, it - D.item0, lane_id);
         }
         __syncthreads();
-        if (threadIdx.x == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq, peer);
+        if (threadIdx.x == 0) {
+          publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, seq, peer);
+          if (trace) record_batch(trace, L, B, b, 0, t_begin);
+        }
       } else {
         for (uint32_t it = warp_in_block; it < B.unpack_items; it += warps_per_block) {
           const rs_copy_desc& D = frames[B.unpack0 + find_frame(frames + B.unpack0, B.nunpack, it)];
@@ -327,7 +347,10 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
           for (uint64_t i = threadIdx.x; i < lines; i += blockDim.x) discard_l2_line(base + (i << 7));
         }
         __syncthreads();
-        if (threadIdx.x == 0) publish(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, seq, peer);
+        if (threadIdx.x == 0) {
+          publish(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, seq, peer);
+          if (trace) record_batch(trace, L, B, b, 1, t_begin);
+        }
       }
     }
     return;
@@ -351,7 +374,7 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
                                unsigned int* error_flag, uint64_t spin_limit, int flags,
-                               int local_blocks, int threads, cudaStream_t stream) {
+                               int local_blocks, int threads, rs_trace_record* trace, cudaStream_t stream) {
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
   const int smem = (flags & kExLaneTma) ? (threads / 32 - 1) * static_cast<int>(kLaneTmaBytes) : 0;
@@ -365,7 +388,7 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
 #define RS_EXCHANGE_LAUNCH(T)                                                                                 \
   rs_exchange_kernel<T><<<grid, T, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
                                                    local_item0, nlocal, local_items, epoch, error_flag, spin_limit, \
-                                                   flags)
+                                                   flags, trace)
   if (threads == 1024) RS_EXCHANGE_LAUNCH(1024);
   else if (threads == 512) RS_EXCHANGE_LAUNCH(512);
   else RS_EXCHANGE_LAUNCH(256);

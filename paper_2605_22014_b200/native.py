@@ -27,7 +27,7 @@ EXPORTS = [
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
     "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
-    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan",
+    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan", "rs_trace_read",
 ]
 
 
@@ -80,7 +80,12 @@ class EngineOptions(C.Structure):
                 ("world_slots", C.c_int32), ("first_local_slot", C.c_int32),
                 ("spin_limit", C.c_int64), ("fault_inject", C.c_int32),
                 ("ring_slot_kib", C.c_int32), ("ring_discard", C.c_int32),
-                ("ring_cta_threads", C.c_int32)]
+                ("ring_cta_threads", C.c_int32), ("trace", C.c_int32), ("reserved2", C.c_int32)]
+
+
+class TraceRecord(C.Structure):
+    _fields_ = [("lane", C.c_uint32), ("batch", C.c_uint32), ("layer", C.c_uint32), ("role", C.c_uint32),
+                ("bytes", C.c_uint64), ("t_begin", C.c_uint64), ("t_end", C.c_uint64)]
 
 
 class PlacementOptions(C.Structure):
@@ -175,6 +180,7 @@ def lib() -> C.CDLL:
         L.rs_host_free.argtypes = [VP]
         L.rs_comm_alloc.argtypes = [VP]
         L.rs_comm_alloc_plan.argtypes = [VP, VP]
+        L.rs_trace_read.argtypes = [VP, I32, P(TraceRecord), I64, P(I64)]
         L.rs_arena_export.argtypes = [VP, I32, I32, VP, P(I64)]
         L.rs_arena_import.argtypes = [VP, I32, I32, VP, I64]
         L.rs_plan_traffic.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, P(I64)]

@@ -160,14 +160,15 @@ class Engine:
                  strict_layers: bool = False, item_bytes: int = 0, blocks_per_sm: int = 0,
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
                  spin_limit: int = 0, fault_inject: int = 0, ring_slot_kib: int = 0,
-                 ring_discard: int = 0, ring_cta_threads: int = 0):
+                 ring_discard: int = 0, ring_cta_threads: int = 0, trace: bool = False):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
         o = N.EngineOptions(len(devs), self._devs, staging_bytes, modes[mode],
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
                             blocks_per_sm, copy_kernel, world_slots, first_local_slot,
-                            spin_limit, fault_inject, ring_slot_kib, ring_discard, ring_cta_threads)
+                            spin_limit, fault_inject, ring_slot_kib, ring_discard, ring_cta_threads,
+                            int(trace), 0)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -273,6 +274,15 @@ class Engine:
 
     def xfer_step(self, what: int, rnd: int = 0):
         N.check(N.lib().rs_xfer_step(self._h, what, rnd))
+
+    def trace(self, device: int = 0):
+        """STAGED transport trace of the last run (engine built with trace=True):
+        [{lane, batch, layer, role, bytes, t_begin, t_end}] (ns, globaltimer)."""
+        cnt = C.c_int64()
+        N.check(N.lib().rs_trace_read(self._h, device, None, 0, C.byref(cnt)))
+        arr = (N.TraceRecord * max(1, cnt.value))()
+        N.check(N.lib().rs_trace_read(self._h, device, arr, cnt.value, C.byref(cnt)))
+        return [{f: getattr(arr[i], f) for f, _ in N.TraceRecord._fields_} for i in range(cnt.value)]
 
     def export_arena(self, which: int, slot: int):
         """(64-byte CUDA IPC handle, arena bytes) of a local slot's arena."""

@@ -496,3 +496,32 @@ def test_tensor_beyond_2_32_elements(mode):
     assert rep["ok"] and rep["bytes_moved"] + rep["local_copy_bytes"] == plan.total_bytes()
     assert eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+def test_transport_trace_layer_order_and_causality():
+    """STAGED transport trace (rs_trace_read, the reference's RecordingTransport
+    on the device): every remote byte appears once per role; each lane
+    streams its batches in layer order (SPEC.md:256 layer-ordering property);
+    a receiver starts a batch only after its sender published it."""
+    sp = mini_llama(4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 1)
+    eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=2, ring_slot_kib=4, trace=True)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    tr = eng.trace(0)
+    tx = {(r["lane"], r["batch"]): r for r in tr if r["role"] == 0}
+    rx = {(r["lane"], r["batch"]): r for r in tr if r["role"] == 1}
+    assert tx.keys() == rx.keys() and len(tx) > 8
+    assert sum(r["bytes"] for r in tx.values()) == rep["bytes_moved"]
+    lanes = {}
+    for (lane, b), r in sorted(tx.items()):
+        lanes.setdefault(lane, []).append(r)
+    for recs in lanes.values():
+        layers = [r["layer"] for r in recs]
+        assert layers == sorted(layers)
+        assert all(a["t_end"] <= b["t_end"] for a, b in zip(recs, recs[1:]))
+    for k, s in tx.items():
+        assert rx[k]["t_begin"] >= s["t_end"] - 1000, (k, s, rx[k])  # globaltimer granularity
+        assert rx[k]["t_end"] >= rx[k]["t_begin"] and s["t_end"] >= s["t_begin"]
+    eng.close()
