@@ -4,6 +4,7 @@
 // chunk_bounds cuts tasks to the ring slot size, a destination rank's rings
 // live in its budget B.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <set>
 
@@ -76,9 +77,9 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   // the sender + receiver CTAs of the busiest slot stop being co-resident.
   // Automatic choice: lanes proportional to each link's bytes (a link's
   // lanes finish together, so the launch ends when the heaviest link does),
-  // scaled so every slot's sender + receiver lanes fit 3/4 of one device's
-  // CTA capacity, at least one and at most 32 per link (same answer on every
-  // process: the plan and the placement are global).
+  // scaled so every slot's sender + receiver lanes fit a share of one
+  // device's CTA capacity (below), at least one and at most 32 per link (same
+  // answer on every process: the plan and the placement are global).
   std::map<std::pair<int, int>, std::uint64_t> link_bytes;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
@@ -100,12 +101,27 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
       slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
     }
-    const int capacity = grid_for(0, exchange_kernel_id()) * 3 / 4;
+    // Share of the co-resident CTAs given to ring lanes; the rest run the
+    // local copies (local tasks + carryovers) in the same launch.  Balanced so
+    // both finish together: a lane pair (2 CTAs) streams ~10 GB/s of payload,
+    // a local-copy CTA ~20 GB/s (profiles/r1/trace_capacity.jsonl), so with
+    // r = local / remote bytes the lane CTAs take 1.94 / (2 + r / 2) of 97 %.
+    std::uint64_t remote_total = 0, local_total = 0;
+    for (const auto& kv : plan.tasks_by_layer)
+      for (const auto& t : kv.second) (t.is_local() ? local_total : remote_total) += static_cast<std::uint64_t>(t.byte_size);
+    for (const auto& kv : plan.carryover_by_layer)
+      for (const auto& k : kv.second) local_total += static_cast<std::uint64_t>(k.byte_size);
+    const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
+    double frac = std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
+    if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
+    const int capacity = static_cast<int>(grid_for(0, exchange_kernel_id()) * frac);
+    int max_lanes = 32;  // per link
+    if (const char* env = std::getenv("RS_RING_MAX_LANES")) max_lanes = std::atoi(env);
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
     const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
     std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
     for (const auto& [lk, b] : link_bytes) {
-      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, 32);
+      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, max_lanes);
       lanes_of[lk] = n;
       slot_lanes[static_cast<std::size_t>(src_slot[lk.first])] += n;
       slot_lanes[static_cast<std::size_t>(dst_slot[lk.second])] += n;
