@@ -366,7 +366,7 @@ int copy_max_blocks_per_sm(int which) {
 
 int rs_kernel_max_blocks_per_sm(int which) {
   if (which == 1) return pattern_max_blocks_per_sm();
-  if (which == 2 || which >= 7) return exchange_max_blocks_per_sm(which);
+  if (which == 2 || (which >= 7 && which <= 12)) return exchange_max_blocks_per_sm(which);
   return copy_max_blocks_per_sm(which);
 }
 

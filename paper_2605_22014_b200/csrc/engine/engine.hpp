@@ -207,10 +207,12 @@ class Engine {
   int ce_copies(const std::vector<rs_copy_desc>& descs, std::uint64_t b, std::uint64_t e, cudaStream_t stream);
   void upload_programs();
   int grid_for(int dev, int which_kernel) const;
-  int exchange_kernel_id() const {
+  int exchange_kernel_id() const {  // occupancy query id (exchange_max_blocks_per_sm)
     const int l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;
     if ((l2 & 24) == 24 && opts_.ring_cta_threads == 256) return 9;  // TMA lanes: shared memory bounds residency
-    return opts_.ring_cta_threads == 1024 ? 8 : opts_.ring_cta_threads == 512 ? 7 : 2;
+    const int base = opts_.ring_cta_threads == 1024 ? 2 : opts_.ring_cta_threads == 512 ? 1 : 0;
+    if (l2 & 8) return 10 + base;
+    return base == 2 ? 8 : base == 1 ? 7 : 2;
   }
   int copy_variant(int dev) const;
   int copy_grid(int dev) const;

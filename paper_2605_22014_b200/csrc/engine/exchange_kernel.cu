@@ -148,8 +148,11 @@ constexpr int kExLaneTma = 16;  // (with kExWarpSpec) copy warps move items with
 // lanes_rx[b - ntx], the rest run the local (DIRECT) copy list.  The launch
 // never exceeds the co-resident CTA capacity, so every waiting role has its
 // counterpart running (same device) or launched on its own device (peers).
-template <int kThreads>
-__global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
+// 3 x 256-thread CTAs per SM: up to 85 registers, so the lane copy loops do
+// not spill (the 64-register build spilled and ran STAGED 8-16 % slower,
+// profiles/r1/lane_share_sweep.jsonl)
+template <int kThreads, bool kWs>
+__global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
     const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
     const bool peer = (L.flags & RS_LANE_PEER) != 0;
     const uint64_t pol_first = (flags & kExHints) ? policy_evict_first() : 0;
     const uint64_t pol_last = (flags & kExHints) ? policy_evict_last() : 0;
-    if (flags & kExWarpSpec) {
+    if constexpr (kWs) {
       // Warp-specialised lane: warp 0 polls flags, publishes and discards;
       // warps 1.. copy.  Two mbarrier pairs hand batches over: go[b % 2]
       // (control -> copy: slot free / data ready) and done[b % 2] (copy ->
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
         }
       }
       return;
-    }
+    } else {
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
       const uint32_t slot = b % L.slots;
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(kThreads) rs_exchange_kernel(
       }
     }
     return;
+    }  // classic lanes
   }
 
   // local copy role
@@ -378,33 +382,41 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
   const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
   if (grid == 0) return cudaSuccess;
   const int smem = (flags & kExLaneTma) ? (threads / 32 - 1) * static_cast<int>(kLaneTmaBytes) : 0;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaSuccess;
-    if (threads == 1024) e = cudaFuncSetAttribute(rs_exchange_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    else if (threads == 512) e = cudaFuncSetAttribute(rs_exchange_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    else e = cudaFuncSetAttribute(rs_exchange_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const bool ws = (flags & kExWarpSpec) != 0;
+  if (smem > 48 * 1024) {  // TMA lanes: 256-thread warp-specialised kernel only
+    cudaError_t e = cudaFuncSetAttribute(rs_exchange_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-#define RS_EXCHANGE_LAUNCH(T)                                                                                 \
-  rs_exchange_kernel<T><<<grid, T, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
-                                                   local_item0, nlocal, local_items, epoch, error_flag, spin_limit, \
-                                                   flags, trace)
-  if (threads == 1024) RS_EXCHANGE_LAUNCH(1024);
-  else if (threads == 512) RS_EXCHANGE_LAUNCH(512);
-  else RS_EXCHANGE_LAUNCH(256);
+#define RS_EXCHANGE_LAUNCH(T, W)                                                                                 \
+  rs_exchange_kernel<T, W><<<grid, T, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
+                                                      local_item0, nlocal, local_items, epoch, error_flag,         \
+                                                      spin_limit, flags, trace)
+  if (threads == 1024) {
+    if (ws) RS_EXCHANGE_LAUNCH(1024, true); else RS_EXCHANGE_LAUNCH(1024, false);
+  } else if (threads == 512) {
+    if (ws) RS_EXCHANGE_LAUNCH(512, true); else RS_EXCHANGE_LAUNCH(512, false);
+  } else {
+    if (ws) RS_EXCHANGE_LAUNCH(256, true); else RS_EXCHANGE_LAUNCH(256, false);
+  }
 #undef RS_EXCHANGE_LAUNCH
   return cudaGetLastError();
 }
 
 int exchange_max_blocks_per_sm(int which) {
+  // 2 / 7 / 8: classic lanes, 256 / 512 / 1024 threads; 9: warp-specialised
+  // 256-thread lanes with TMA copy warps (112 KB of shared memory); 10 / 11 /
+  // 12: warp-specialised lanes, 256 / 512 / 1024 threads
   int n = 0;
   if (which == 9) {
     const int smem = 7 * static_cast<int>(kLaneTmaBytes);
-    cudaFuncSetAttribute(rs_exchange_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256>, 256, smem);
-  } else if (which == 7) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512>, 512, 0);
-  else if (which == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<1024>, 1024, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256>, 256, 0);
+    cudaFuncSetAttribute(rs_exchange_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256, true>, 256, smem);
+  } else if (which == 7) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512, false>, 512, 0);
+  else if (which == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<1024, false>, 1024, 0);
+  else if (which == 10) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256, true>, 256, 0);
+  else if (which == 11) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<512, true>, 512, 0);
+  else if (which == 12) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<1024, true>, 1024, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_exchange_kernel<256, false>, 256, 0);
   return n;
 }
 
