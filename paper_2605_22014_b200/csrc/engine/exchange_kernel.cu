@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t find_frame(const rs_copy_desc* __restrict__ 
 // mbarrier, wait, bulk-store them, and wait until the stores have read the
 // buffer.  Returns false (nothing done) when the item does not fit the buffer
 // or is not 16 B aligned -- the caller copies it with the warp instead.
-constexpr uint32_t kLaneTmaBytes = 16384;
+constexpr uint32_t kLaneTmaBytes = 8192;
 
 __device__ __forceinline__ bool tma_copy_item(const rs_copy_desc& D, uint64_t local_item, unsigned char* buf,
                                               uint64_t* bar, uint32_t& phase, uint64_t lpol, uint64_t spol,
