@@ -115,7 +115,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     double frac = std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
     if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
     const int capacity = static_cast<int>(grid_for(0, exchange_kernel_id()) * frac);
-    int max_lanes = 32;  // per link
+    int max_lanes = 64;  // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than 32)
     if (const char* env = std::getenv("RS_RING_MAX_LANES")) max_lanes = std::atoi(env);
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
     const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
