@@ -272,6 +272,18 @@ def xfer_one_gpu(args) -> None:
     nccl.close()
 
 
+def copy_kernel_label(mode: str, world: int) -> str:
+    if mode == "staged":
+        return ("rs_exchange_kernel: ring lanes (one 256-thread CTA per lane end, 128 KiB slots x 2, "
+                "L2-resident), spare CTAs copy local tasks")
+    if mode == "xfer":
+        return "pack/unpack LDG8 non-persistent kernels around ncclSend/ncclRecv"
+    if world > 1:
+        return "LDG8 non-persistent grid (peer stores over NVLink), one 16 KB item per warp"
+    return ("TMA bulk copy (cp.async.bulk global->smem->global, mbarrier complete_tx), one 1-warp CTA per "
+            "16 KB item, non-persistent grid")
+
+
 def ours(args) -> None:
     """N=1: every logical rank on cuda:0.  N>1 (torchrun, one process per GPU):
     rank id r of both configs lives on GPU r*N//8 (iota placement at N=8);
@@ -400,7 +412,8 @@ def ours(args) -> None:
         achieved = link / (step_ms / 1e3) / 1e9
         nvl = 770.0
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": nvl, "unit": "GB/s",
-                "frac": round(achieved / nvl, 4), "traffic": None, "kernel": "rs_copy_kernel (peer stores)",
+                "frac": round(achieved / nvl, 4), "traffic": None, "kernel": ("rs_exchange_kernel (ring lanes over peer memory)" if args.mode == "staged"
+                                                                 else "rs_copy_kernel<8> non-persistent (peer stores)"),
                 "algorithmic_bytes_per_launch": link,
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
                 "per_gpu_egress_ingress_GB": [[round(t[0] / 1e9, 2), round(t[1] / 1e9, 2)] for t in traffic]}
@@ -415,7 +428,7 @@ def ours(args) -> None:
                            f"rank r on GPU r*{world}//8, one process per GPU"),
                        "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
                        "tasks": summ["task_count"], "mode": args.mode, "placement": args.placement, "staging_bytes": args.staging_bytes,
-                       "strict_layers": bool(args.strict), "copy_kernel": "TMA bulk copy (cp.async.bulk global->smem->global, mbarrier complete_tx), one 1-warp CTA per 16 KB item, non-persistent grid",
+                       "strict_layers": bool(args.strict), "copy_kernel": copy_kernel_label(args.mode, world),
                        "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
             "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}
