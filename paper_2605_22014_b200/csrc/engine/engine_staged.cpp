@@ -406,6 +406,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
     nbatch_total += lb.batches.size();
   }
+  std::uint64_t item_div = 32;  // work items per slot (RS_FRAME_ITEMS overrides; diagnostic)
+  if (const char* env = std::getenv("RS_FRAME_ITEMS")) item_div = std::max(1, std::atoi(env));
   std::vector<std::vector<rs_copy_desc>> lane_frames(lanes.size());
   std::vector<std::vector<rs_batch_desc>> lane_batches(lanes.size());
   auto build_lane = [&](std::size_t i) {
@@ -416,7 +418,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     batches.reserve(lb.batches.size());
     // work items inside a batch: ~32 per slot so all 8 warps of the lane's
     // CTA share even a small (L2-resident) slot
-    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / 32, 4096, 65536);
+    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / item_div, 2048, 65536);
     for (std::size_t b = 0; b < lb.batches.size(); ++b) {
       const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
       rs_batch_desc Bd{};
