@@ -182,7 +182,8 @@ def reference_arm(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    layers = int(os.environ.get("RS_BENCH_CPU_LAYERS", str(min(os.cpu_count() or 1, 16))))
+    # >= 2 layers: the resize is PP2 -> PP2, every stage needs a layer
+    layers = max(2, int(os.environ.get("RS_BENCH_CPU_LAYERS", str(min(os.cpu_count() or 1, 16)))))
     threads = min(os.cpu_count() or 1, layers)  # execute_plan is per-layer; one thread per layer
     res = run_reference_cpu(threads, layers, max(1, args.steps), args.warmup, args.staging_bytes)
     _, _, _, desc = workload(args.gpus)
