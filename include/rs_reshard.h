@@ -22,6 +22,13 @@
  *   rs_verify_pattern  gather-reslice oracle compare (SPEC.md cmd_verify)
  *   rs_execute         execute_plan            proj/include/reshard/executor.hpp:50-53
  *   rs_execute_host    execute_plan on host ShardStore buffers (H2D/D2H inside)
+ *   rs_switch          GenerationMachine::run_switch + atomic_switch, executed
+ *                      (proj/src/generation.cpp:239-290) instead of priced
+ *   rs_trace_read      RecordingTransport          proj/include/reshard/transport.hpp:50-75
+ *   rs_comm_alloc*, rs_arena_*  the staging buffers + NCCL/TCPStore bootstrap of the
+ *                      paper's executor, as CUDA-IPC peer arenas
+ *   rs_xfer_*          the paper's NCCL isend/irecv executor,
+ *                      kept as a measured comparator
  */
 #ifndef RS_RESHARD_H
 #define RS_RESHARD_H
