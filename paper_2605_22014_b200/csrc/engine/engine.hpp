@@ -196,6 +196,7 @@ class Engine {
     std::map<int, std::uint64_t> inbound_lanes;      // dst rank -> lanes into it
     std::map<int, std::uint64_t> slot_bytes_of;      // dst rank -> ring slot bytes
     std::map<int, std::uint64_t> ring_bytes_of;      // dst rank -> bytes of all its rings
+    std::map<int, int> k_of;                         // dst rank -> ring depth (K, or 1 for a tiny B)
   };
   RingGeometry ring_geometry(const reshard::TransferPlan& plan) const;
   struct CommLayout {

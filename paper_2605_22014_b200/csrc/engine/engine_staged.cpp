@@ -161,12 +161,39 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
   auto& inbound_lanes = geo.inbound_lanes;
   for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
+  // largest element a destination rank receives over rings
+  std::map<int, std::uint64_t> need_eb;
+  for (const auto& kv : plan.tasks_by_layer)
+    for (const auto& t : kv.second)
+      if (!t.is_local()) {
+        const auto& m = src.model;
+        auto& e = need_eb[t.dst_rank];
+        e = std::max<std::uint64_t>(e, static_cast<std::uint64_t>(m.element_bytes(m.tensors[t.tensor_index])));
+      }
   auto& slot_bytes_of = geo.slot_bytes_of;
   for (const auto& [d, srcs] : inbound) {
-    std::uint64_t sb = static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(K));
-    sb = std::min(sb, slot_cap);
-    slot_bytes_of[d] = sb >= 4096 ? sb / kAlign * kAlign : sb / 16 * 16;
-    geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(K);
+    // A tiny budget cannot host K slots on every lane into d: fall back to one
+    // lane per link, then to K = 1 (strictly alternating pack / unpack), so
+    // the ring path accepts every B the reference's executor accepts (a
+    // destination needs room for one element per inbound link).
+    int k = K;
+    const std::uint64_t need = std::max<std::uint64_t>(need_eb[d], 16);
+    auto slot_for = [&]() { return static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(k)); };
+    if (slot_for() < need) {
+      for (auto& [lk, n] : lanes_of)
+        if (lk.second == d && n > 1) {
+          inbound_lanes[d] -= static_cast<std::uint64_t>(n - 1);
+          n = 1;
+        }
+    }
+    if (slot_for() < need) k = 1;
+    geo.k_of[d] = k;
+    std::uint64_t sb = std::min(slot_for(), slot_cap);
+    if (sb >= 4096) sb = sb / kAlign * kAlign;
+    else if (sb >= 16) sb = sb / 16 * 16;
+    else if (need_eb[d]) sb = sb / need_eb[d] * need_eb[d];
+    slot_bytes_of[d] = sb;
+    geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(k);
   }
 
   return geo;
@@ -227,6 +254,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   struct LaneBuild {
     int src_rank, dst_rank, sslot, dslot;
     std::uint64_t slot_bytes;
+    int k;  // ring depth of this lane (geo.k_of: K, or 1 for a tiny budget)
     std::vector<std::vector<Frame>> batches;
     std::uint64_t fill = 0;
   };
@@ -289,7 +317,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           const int P = lanes_of.at(lk);
           if (!link_first_lane.count(lk)) {
             link_first_lane[lk] = static_cast<int>(lanes.size());
-            for (int p = 0; p < P; ++p) lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, {}, 0});
+            for (int p = 0; p < P; ++p)
+              lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, geo.k_of.at(t.dst_rank), {}, 0});
           }
           for (const auto& c : chunks) {
             int& cur = link_cursor[lk];
@@ -351,7 +380,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       throw DomainError("staged: comm arena has no ring region for dst rank " + std::to_string(lb.dst_rank) +
                         "; re-run rs_comm_alloc for this dst layout");
     where[i].ring_off = reg->second + used;
-    used += lb.slot_bytes * static_cast<std::uint64_t>(K);
+    used += lb.slot_bytes * static_cast<std::uint64_t>(lb.k);
     if (used > region_bytes.at(lb.dst_rank))
       throw DomainError("staged: ring region of dst rank " + std::to_string(lb.dst_rank) + " (" +
                         std::to_string(region_bytes.at(lb.dst_rank)) + " bytes) is smaller than this plan's rings; " +
@@ -397,7 +426,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     L.slot_bytes = lb.slot_bytes;
     L.ready_flags = L.ready_flags_rx = ready ? addr(ready) + where[i].ready_off : 0;
     L.credit_flags = L.credit_flags_tx = credit ? addr(credit) + where[i].credit_off : 0;
-    L.slots = static_cast<std::uint32_t>(K);
+    L.slots = static_cast<std::uint32_t>(lb.k);
     // GPU-scope synchronisation only when both ends are this process's same
     // slot; every cross-slot lane (another GPU, or another process sharing a
     // GPU through IPC) synchronises at system scope
@@ -420,7 +449,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     // CTA share even a small (L2-resident) slot
     const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / item_div, 2048, 65536);
     for (std::size_t b = 0; b < lb.batches.size(); ++b) {
-      const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(K)) * lb.slot_bytes;
+      const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(lb.k)) * lb.slot_bytes;
       rs_batch_desc Bd{};
       Bd.pack0 = static_cast<std::uint32_t>(frames.size());
       if (tx_local[i])

@@ -525,3 +525,21 @@ def test_transport_trace_layer_order_and_causality():
         assert rx[k]["t_begin"] >= s["t_end"] - 1000, (k, s, rx[k])  # globaltimer granularity
         assert rx[k]["t_end"] >= rx[k]["t_begin"] and s["t_end"] >= s["t_begin"]
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_tiny_staging_budget_like_reference(mode, golden, oracle_c):
+    """B = 64 bytes per destination rank (the reference's golden B=64 runs all
+    succeed): the ring path falls back to one lane per link and K = 1 where
+    K slots per lane do not fit, and still lands the reference's bytes with
+    resident staging <= B."""
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(60, golden["random_pairs"]["base_seed"]):
+        want = rows[seed]["exec"]["64"]
+        eng = make_engine(sp, co, cn, mode, 64)
+        rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+        assert rep["ok"] == bool(want["ok"]), (seed, rep["error"])
+        assert rep["bytes_moved"] == want["bytes_moved"] and rep["layers_processed"] == want["layers_processed"]
+        assert rep["peak_staging_bytes"] <= 64
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"], seed
+        eng.close()
