@@ -543,3 +543,30 @@ def test_tiny_staging_budget_like_reference(mode, golden, oracle_c):
         assert rep["peak_staging_bytes"] <= 64
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"], seed
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_spec_known_answer_cases_on_device(mode, golden, oracle_ref):
+    """The SPEC's known-answer resizes (TP4->TP8 column / row split, DP2->DP4
+    replicated, identity, PP layer move; tests/golden/kat.json from the
+    reference) executed on the device: the plan is the reference's, and every
+    destination byte equals the reference executor's own output (oracle/_ref)."""
+    from helpers import cfg_from_json, spec_from_text
+    n = 0
+    for case in golden["kat"]:
+        if case.get("error"):
+            continue
+        sp = spec_from_text(case["spec"])
+        co, cn = cfg_from_json(case["old"]), cfg_from_json(case["new"])
+        plan = R.compute_transfer_plan(co, cn, sp)
+        assert plan.text() == case["plan"], case["name"]
+        eng = make_engine(sp, co, cn, mode, 1 << 20)
+        rep = R.execute_plan(plan, eng)
+        orep, ostore = oracle_ref.execute(sp, co, cn, case["plan"], SEED, 1 << 20)
+        assert rep["ok"] and orep["ok"], case["name"]
+        assert (rep["bytes_moved"], rep["local_copy_bytes"]) == (orep["bytes_moved"], orep["local_copy_bytes"])
+        for (ti, rank), want in ostore.entries.items():
+            assert np.array_equal(eng.read(RS_DST, rank, ti), want), (case["name"], ti, rank)
+        eng.close()
+        n += 1
+    assert n == 5
