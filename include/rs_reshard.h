@@ -106,7 +106,9 @@ typedef struct {
                                16 (with 8, 256-thread lanes) TMA bulk copies in the copy warps */
   int32_t ring_cta_threads; /* STAGED: threads per ring-lane CTA, 256 / 512 / 1024 (0: default) */
   int32_t trace;            /* STAGED: 1 = record a per-batch transport trace (rs_trace_read) */
-  int32_t reserved2;
+  int32_t ring_same_slot;   /* STAGED, cross-rank tasks whose ranks share a GPU: 0 = auto (rings
+                               on a one-slot engine -- the transport is what runs -- and direct
+                               copies in a multi-slot job), 1 = always rings, 2 = always direct */
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default: RS_COPY_LDG8_NP */

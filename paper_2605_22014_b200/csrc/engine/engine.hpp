@@ -199,6 +199,8 @@ class Engine {
     std::map<int, int> k_of;                         // dst rank -> ring depth (K, or 1 for a tiny B)
   };
   RingGeometry ring_geometry(const reshard::TransferPlan& plan) const;
+  // STAGED: does this cross-rank task go through a ring (else a direct copy)?
+  bool ringed(const reshard::TransferTask& t) const;
   struct CommLayout {
     std::vector<std::map<int, std::pair<std::size_t, std::size_t>>> regions;  // per slot: rank -> (offset, bytes)
     std::vector<std::size_t> slot_bytes;                                      // per slot, incl. flags

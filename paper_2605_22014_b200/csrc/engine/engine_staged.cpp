@@ -59,6 +59,15 @@ char* Engine::comm_base(int slot) const {
   return imp ? imp->data() : nullptr;
 }
 
+bool Engine::ringed(const reshard::TransferTask& t) const {
+  if (t.is_local()) return false;
+  const int mode = opts_.ring_same_slot == 0 ? (nslots_ > 1 ? 2 : 1) : opts_.ring_same_slot;
+  if (mode == 1) return true;
+  const Entry* se = stores_[RS_SRC].find(t.src_rank, t.tensor_index);
+  const Entry* de = stores_[RS_DST].find(t.dst_rank, t.tensor_index);
+  return !(se && de && se->slot == de->slot);
+}
+
 // Ring geometry of a plan (STAGED): lanes per link, slot size and ring bytes
 // per destination rank.  Deterministic from the plan and the layouts, so
 // every process computes the same rings for every slot.
@@ -72,7 +81,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   std::map<int, std::set<int>> inbound;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
-      if (!t.is_local()) inbound[t.dst_rank].insert(t.src_rank);
+      if (ringed(t)) inbound[t.dst_rank].insert(t.src_rank);
 
   // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
   // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
@@ -85,7 +94,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   std::map<std::pair<int, int>, std::uint64_t> link_bytes;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
-      if (!t.is_local()) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
+      if (ringed(t)) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
   auto& lanes_of = geo.lanes_of;
   if (opts_.lanes_per_link > 0) {
     for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
@@ -110,7 +119,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     // r = local / remote bytes the lane CTAs take 1.94 / (2 + r / 2) of 97 %.
     std::uint64_t remote_total = 0, local_total = 0;
     for (const auto& kv : plan.tasks_by_layer)
-      for (const auto& t : kv.second) (t.is_local() ? local_total : remote_total) += static_cast<std::uint64_t>(t.byte_size);
+      for (const auto& t : kv.second) (ringed(t) ? remote_total : local_total) += static_cast<std::uint64_t>(t.byte_size);
     for (const auto& kv : plan.carryover_by_layer)
       for (const auto& k : kv.second) local_total += static_cast<std::uint64_t>(k.byte_size);
     const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
@@ -165,7 +174,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   std::map<int, std::uint64_t> need_eb;
   for (const auto& kv : plan.tasks_by_layer)
     for (const auto& t : kv.second)
-      if (!t.is_local()) {
+      if (ringed(t)) {
         const auto& m = src.model;
         auto& e = need_eb[t.dst_rank];
         e = std::max<std::uint64_t>(e, static_cast<std::uint64_t>(m.element_bytes(m.tensors[t.tensor_index])));
@@ -305,6 +314,11 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           if (t.is_local()) {
             local_copy(se, de, t.bounds, eb);
             delta.local_copy_bytes += t.bounds.element_count() * eb;
+            continue;
+          }
+          if (!ringed(t)) {  // cross-rank, both ranks on one GPU of a multi-slot job
+            local_copy(se, de, t.bounds, eb);
+            delta.bytes_moved += t.bounds.element_count() * eb;
             continue;
           }
           const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);

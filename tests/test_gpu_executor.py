@@ -570,3 +570,20 @@ def test_spec_known_answer_cases_on_device(mode, golden, oracle_ref):
         eng.close()
         n += 1
     assert n == 5
+
+
+@pytest.mark.parametrize("same_slot", [1, 2])
+def test_ring_same_slot_policy(same_slot, golden, oracle_c):
+    """ring_same_slot: cross-rank tasks whose ranks share a GPU go through the
+    rings (1; the one-slot default) or become direct copies (2; the
+    multi-slot default) -- same bytes either way, no staging when direct."""
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(30, golden["random_pairs"]["base_seed"]):
+        eng = make_engine(sp, co, cn, "staged", 1 << 16, ring_same_slot=same_slot)
+        rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+        want = rows[seed]["exec"]["4096"]
+        assert rep["ok"] and rep["bytes_moved"] == want["bytes_moved"], (seed, rep)
+        if same_slot == 2:
+            assert rep["peak_staging_bytes"] == 0
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"], seed
+        eng.close()
