@@ -132,6 +132,10 @@ std::int64_t Store::total_bytes() const {
 Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.num_devices < 1 || !opts.device_ids) throw DomainError("engine: no devices");
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
+  if (opts.strict_layers && opts.mode != RS_MODE_DIRECT)
+    // one launch per layer is a DIRECT-mode schedule; ring lanes already stream
+    // every link's batches in layer order (verified by rs_trace_read)
+    throw DomainError("engine: strict_layers applies to RS_MODE_DIRECT");
   for (int i = 0; i < opts.num_devices; ++i)
     for (int j = 0; j < i; ++j)
       if (opts.device_ids[i] == opts.device_ids[j])

@@ -61,3 +61,10 @@ def test_engine_rejects_duplicate_devices_before_touching_cuda():
     import pytest
     with pytest.raises(N.DomainError, match="listed twice"):
         R.Engine([0, 0])
+
+
+def test_strict_layers_is_a_direct_mode_option():
+    from paper_2605_22014_b200 import reshard as R
+    import pytest
+    with pytest.raises(N.DomainError, match="strict_layers"):
+        R.Engine([0], mode="staged", strict_layers=True)
