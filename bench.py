@@ -42,13 +42,54 @@ HIGH_IS_GOOD = True
 SEED = 42
 
 
+NVLINK_NOMINAL_GBS = 900.0  # NVLink 5 per direction per GPU (BASELINE.json north_star)
+
+# RS_COPY_* id (rs_exec_report.copy_kernel) -> kernel name as ncu lists it
+COPY_KERNEL_NAMES = {17: "rs_copy_tma_np_kernel", 18: "rs_copy_tma_np_kernel (32 KB items)",
+                     15: "rs_copy_kernel<8> (non-persistent)", 2: "rs_copy_kernel<8> (persistent)",
+                     1: "rs_copy_kernel<4>", 3: "rs_copy_bulk_kernel", 16: "copy engines (cudaMemcpy2DAsync)"}
+
+
 def peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    out = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)",
+           "nvlink_gbs": NVLINK_NOMINAL_GBS, "nvlink_source": "nominal NVLink 5, 900 GB/s per direction (north_star)"}
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        out["hbm_gbs"], out["source"] = float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        for k in ("nvlink_gbs", "nvlink_gbs_per_direction"):
+            if k in d:
+                out["nvlink_gbs"], out["nvlink_source"] = float(d[k]), f"measured (MEASURED_PEAKS.json {k})"
+    return out
+
+
+def roofline(traffic, step_ms: float, hbm_gbs: float, nvlink_gbs: float) -> dict:
+    """BASELINE.md §3 / SURVEY §8(d) per-GPU roofline of one handoff:
+    t_g = max(out_g / NVL, in_g / NVL, (out_g + in_g + 2 local_g + 2 carry_g) / HBM),
+    t_roof = max_g t_g.  ``traffic`` is rs_plan_traffic's per-slot
+    [egress, ingress, intra-GPU, carryover] bytes.  ``achieved`` is the
+    bottleneck term's bytes over the measured step, against that term's peak,
+    so frac = t_roof / t_step."""
+    per, best = [], None
+    for g, (out, inn, intra, carry) in enumerate(traffic):
+        hbm = out + inn + 2 * intra + 2 * carry
+        t_link = max(out, inn) / (nvlink_gbs * 1e9)
+        t_hbm = hbm / (hbm_gbs * 1e9)
+        t = max(t_link, t_hbm)
+        per.append({"gpu": g, "out_GB": round(out / 1e9, 3), "in_GB": round(inn / 1e9, 3),
+                    "hbm_GB": round(hbm / 1e9, 3), "roofline_ms": round(t * 1e3, 4),
+                    "bound": "nvlink" if t_link > t_hbm else "hbm"})
+        if best is None or t > best[0]:
+            best = (t, g, "nvlink" if t_link > t_hbm else "hbm", max(out, inn) if t_link > t_hbm else hbm)
+    t_roof, g, bound, nbytes = best
+    step_s = step_ms / 1e3
+    peak = nvlink_gbs if bound == "nvlink" else hbm_gbs
+    achieved = nbytes / step_s / 1e9
+    return {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "roofline_ms": round(t_roof * 1e3, 4), "bottleneck_gpu": g,
+            "algorithmic_bytes_per_launch": int(nbytes), "per_gpu": per,
+            "formula": "max_g max(out_g/NVL, in_g/NVL, (out_g+in_g+2*local_g+2*carry_g)/HBM)"}
 
 
 class ClockSampler:
@@ -273,16 +314,106 @@ def xfer_one_gpu(args) -> None:
     nccl.close()
 
 
-def copy_kernel_label(mode: str, world: int) -> str:
+def kernel_name(mode: str, rep: dict) -> str:
+    """The kernel that moved the bytes, from the run's own report."""
     if mode == "staged":
-        return ("rs_exchange_kernel: ring lanes (one 256-thread CTA per lane end, 128 KiB slots x 2, "
-                "L2-resident), spare CTAs copy local tasks")
+        return "rs_exchange_kernel"
     if mode == "xfer":
-        return "pack/unpack LDG8 non-persistent kernels around ncclSend/ncclRecv"
+        return "rs_copy_kernel pack/unpack + NCCL"
+    return COPY_KERNEL_NAMES.get(rep.get("copy_kernel", -1), f"RS_COPY variant {rep.get('copy_kernel')}")
+
+
+def kernel_label(name: str) -> str:
+    if name == "rs_exchange_kernel":
+        return ("rs_exchange_kernel: ring lanes (sender CTA packs into the receiver's staging ring, receiver "
+                "CTA unpacks; bounded staging), spare CTAs copy local tasks")
+    if name == "rs_copy_tma_np_kernel":
+        return ("TMA bulk copy (cp.async.bulk global->smem->global, mbarrier complete_tx), one 1-warp CTA per "
+                "16 KB item, non-persistent grid")
+    if name.startswith("rs_copy_kernel<8> (non-persistent)"):
+        return "LDG8 non-persistent grid (plain st.global, peer stores over NVLink), one 16 KB item per warp"
+    return name
+
+
+def timed_steps(one_step, steps: int, world: int, barrier, device: int):
+    """K device-timed steps (CUDA events on the engine stream, max over ranks
+    afterwards), clocks sampled during the timed region."""
+    import torch
+    barrier()
+    launches, dev_ms = 0, []
+    with ClockSampler(device) as clk:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            if world > 1:
+                torch.distributed.barrier()  # every GPU starts the handoff together
+            rep = one_step()
+            assert rep["ok"], rep
+            dev_ms.append(rep["device_ms"])
+            launches += rep["kernel_launches"]
+        barrier()
+        wall = time.perf_counter() - t0
+    return dev_ms, launches, wall, clk.summary(), rep
+
+
+def reduce_ranks(world: int, step_ms: float, counts):
+    """max over ranks of the step time, sum over ranks of the counters."""
+    if world == 1:
+        return step_ms, [int(c) for c in counts]
+    import torch
+    t = torch.tensor([step_ms] + [float(c) for c in counts], dtype=torch.float64)
+    torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
+    tt = t[1:].clone()
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.SUM)
+    return float(t[0]), [int(x) for x in tt]
+
+
+def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank, device, barrier, pk) -> dict:
+    """The STAGED transport (bounded staging rings, the north-star streaming
+    engine) on the same plan and the same device stores as the DIRECT
+    headline: a second engine in RS_MODE_STAGED binds the DIRECT engine's
+    shard buffers, allocates plan-sized rings (resident staging <= B per
+    destination rank), runs K timed handoffs, and pattern-verifies."""
+    from paper_2605_22014_b200 import reshard as R
+    from paper_2605_22014_b200.native import RS_COMM, RS_DST, RS_SRC
+    eng = R.Engine([device], staging_bytes=args.staging_bytes, mode="staged", lanes_per_link=args.lanes,
+                   ring_slot_kib=args.ring_slot_kib, strict_layers=args.strict, world_slots=world,
+                   first_local_slot=rank)
+    eng.layout(RS_SRC, sp, co, so)
+    eng.layout(RS_DST, sp, cn, sn)
+    for which in (RS_SRC, RS_DST):
+        for ti, r, n in eng.entries(which):
+            ptr, nb = eng_direct.ptr(which, r, ti)
+            if ptr:
+                eng.bind(which, r, ti, ptr, nb)
+    eng.comm_alloc(plan)
     if world > 1:
-        return "LDG8 non-persistent grid (peer stores over NVLink), one 16 KB item per warp"
-    return ("TMA bulk copy (cp.async.bulk global->smem->global, mbarrier complete_tx), one 1-warp CTA per "
-            "16 KB item, non-persistent grid")
+        from paper_2605_22014_b200.dist import connect
+        connect(eng, which=(RS_COMM,))
+    eng.prepare(plan)
+    eng_direct.fill_pattern(RS_DST, SEED ^ 0xBEEF)  # poison: the staged run must rewrite every byte
+    for _ in range(args.warmup):
+        barrier()
+        rep = eng.run()
+        assert rep["ok"], rep
+    dev_ms, launches, wall, clocks, rep = timed_steps(eng.run, args.steps, world, barrier, device)
+    bad = eng_direct.verify_pattern(RS_DST, SEED)[0]
+    step_ms, (bad, launches, staging) = reduce_ranks(world, sum(dev_ms) / len(dev_ms),
+                                                     [bad, launches, rep["peak_staging_bytes"]])
+    if world > 1:  # peak staging is a per-destination-rank maximum, not a sum
+        import torch
+        t = torch.tensor([float(rep["peak_staging_bytes"])], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        staging = int(t[0])
+    total = plan.summary()["total_bytes"]
+    roof = roofline(traffic, step_ms, pk["hbm_gbs"], pk["nvlink_gbs"])
+    out = {"ms_per_step": round(step_ms, 4), "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
+           "frac": roof["frac"], "bound": roof["bound"], "roofline_ms": roof["roofline_ms"],
+           "peak_staging_bytes": staging, "staging_budget_bytes": args.staging_bytes,
+           "within_budget": staging <= args.staging_bytes, "kernel": kernel_name("staged", rep),
+           "ring_same_slot": rep["ring_same_slot"], "gpu_launches": launches, "clocks": clocks,
+           "wall_s": round(wall, 3), "dst_pattern_mismatches": int(bad)}
+    eng.close()
+    return out
 
 
 def ours(args) -> None:
@@ -296,7 +427,8 @@ def ours(args) -> None:
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
 
     rank, world, local = dist_env()
-    device = 0 if os.environ.get("RS_BENCH_SAME_DEVICE") else local
+    same_device = bool(os.environ.get("RS_BENCH_SAME_DEVICE"))
+    device = 0 if same_device else local
     torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
@@ -341,12 +473,12 @@ def ours(args) -> None:
         # comparator: our pack/unpack kernels around torch.distributed p2p
         # (NCCL between GPUs; gloo + host staging when processes share a GPU)
         from paper_2605_22014_b200 import xfer
-        same = bool(os.environ.get("RS_BENCH_SAME_DEVICE"))
-        group = None if (world == 1 or same) else torch.distributed.new_group(backend="nccl")
+        group = None if (world == 1 or same_device) else torch.distributed.new_group(backend="nccl")
 
         def one_step():
-            info = xfer.run(eng, device, host_staging=same, group=group)
-            return {"ok": True, "device_ms": info["seconds"] * 1e3, "kernel_launches": 1 + 2 * info["rounds"]}
+            info = xfer.run(eng, device, host_staging=same_device, group=group)
+            return {"ok": True, "device_ms": info["seconds"] * 1e3, "kernel_launches": 1 + 2 * info["rounds"],
+                    "copy_kernel": 15, "peak_staging_bytes": 0}
     else:
         def one_step():
             return eng.run()
@@ -358,66 +490,35 @@ def ours(args) -> None:
     barrier()
     bad_warm = eng.verify_pattern(RS_DST, SEED)[0]
 
-    barrier()
-    launches = 0
-    dev_ms = []
-    with ClockSampler(device) as clk:
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            if world > 1:
-                torch.distributed.barrier()  # every GPU starts the handoff together
-            rep = one_step()
-            dev_ms.append(rep["device_ms"])
-            launches += rep["kernel_launches"]
-        barrier()
-        wall = time.perf_counter() - t0
-    step_ms = sum(dev_ms) / len(dev_ms)
+    dev_ms, launches, wall, clocks, rep = timed_steps(one_step, args.steps, world, barrier, device)
     mismatches = eng.verify_pattern(RS_DST, SEED)[0]
-    if world > 1:
-        t = torch.tensor([step_ms, float(mismatches), float(bad_warm), float(launches)], dtype=torch.float64)
-        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
-        tt = t[1:].clone()
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.SUM)
-        step_ms = float(t[0])
-        mismatches, bad_warm, launches = int(tt[0]), int(tt[1]), int(tt[2])
+    step_ms, (mismatches, bad_warm, launches) = reduce_ranks(world, sum(dev_ms) / len(dev_ms),
+                                                             [mismatches, bad_warm, launches])
 
     pk = peaks()
+    kname = kernel_name(args.mode, rep)
+    roof = roofline(traffic, step_ms, pk["hbm_gbs"], pk["nvlink_gbs"])
+    roof.update({"traffic": None, "kernel": kname, "peak_source": pk["source"] if roof["bound"] == "hbm"
+                 else pk["nvlink_source"], "hbm_peak_gbs": pk["hbm_gbs"], "nvlink_peak_gbs": pk["nvlink_gbs"]})
     if world == 1:
-        # algorithmic bytes: every moved byte read once + written once (the
-        # floor for any path; STAGED's ring slots are staging overhead on top)
-        algo_bytes = 2 * (total + summ["carryover_bytes"])
-        kernel = "rs_exchange_kernel" if args.mode == "staged" else "rs_copy_tma_np_kernel"
-        achieved = algo_bytes / (step_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None, "kernel": kernel,
-                "algorithmic_bytes_per_launch": algo_bytes, "peak_source": pk["source"],
-                "note": ("the peak is torch copy_ of 2 GiB (MEASURED_PEAKS.json); the TMA bulk copy kernel "
-                         "sustains 6.82-6.95 TB/s on a plain contiguous 2-32 GiB copy where copy_ gets "
-                         "6.50-6.69 (profiles/r1/contig_probe.jsonl), so frac can exceed 1; "
-                         "frac_vs_contiguous_copy compares with the kernel's own contiguous 32 GiB copy")}
-        if args.mode == "direct":
+        roof["note"] = ("the HBM peak is torch copy_ of 2 GiB (MEASURED_PEAKS.json); the TMA bulk copy kernel "
+                        "sustains 6.82-6.95 TB/s on a plain contiguous 2-32 GiB copy where copy_ gets "
+                        "6.50-6.69 (profiles/r1/contig_probe.jsonl), so frac can exceed 1")
+        if kname == "rs_copy_tma_np_kernel":
             contiguous = 6922.3  # profiles/r1/contig_probe.jsonl: this kernel (TMA-NP, 16 KB items), 32 GiB copy
             roof["contiguous_copy_gbs"] = contiguous
-            roof["frac_vs_contiguous_copy"] = round(achieved / contiguous, 4)
+            roof["frac_vs_contiguous_copy"] = round(roof["achieved"] / contiguous, 4)
         if args.mode == "staged":  # with DRAM-resident rings each remote byte costs 2 more
-            ring = algo_bytes + 2 * summ["remote_bytes"]
+            ring = roof["algorithmic_bytes_per_launch"] + 2 * summ["remote_bytes"]
             roof["ring_staged_bytes_per_launch"] = ring
             roof["frac_vs_dram_resident_ring"] = round(ring / (step_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)
         tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp) and args.mode == "direct" and not args.profile_layers:
-            with open(tp) as f:  # measured on this exact launch (full-size C2, DIRECT)
-                roof["traffic"] = json.load(f).get("rs_copy_kernel_dram_bytes_per_launch")
-    else:
-        # the busiest GPU's NVLink direction bounds the handoff
-        link = max(max(t[0], t[1]) for t in traffic)
-        achieved = link / (step_ms / 1e3) / 1e9
-        nvl = 770.0
-        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": nvl, "unit": "GB/s",
-                "frac": round(achieved / nvl, 4), "traffic": None, "kernel": ("rs_exchange_kernel (ring lanes over peer memory)" if args.mode == "staged"
-                                                                 else "rs_copy_kernel<8> non-persistent (peer stores)"),
-                "algorithmic_bytes_per_launch": link,
-                "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
-                "per_gpu_egress_ingress_GB": [[round(t[0] / 1e9, 2), round(t[1] / 1e9, 2)] for t in traffic]}
+        if os.path.exists(tp) and not args.profile_layers:
+            with open(tp) as f:  # ncu DRAM bytes of this exact launch (same kernel, same workload bytes)
+                t = json.load(f)
+            if t.get("kernel") == kname and t.get("algorithmic_bytes_per_launch") == roof["algorithmic_bytes_per_launch"]:
+                roof["traffic"] = t.get("rs_copy_kernel_dram_bytes_per_launch")
+                roof["traffic_source"] = t.get("source")
 
     line = {"metric": METRIC, "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -426,13 +527,28 @@ def ours(args) -> None:
             "data": "synthetic: reference pattern state (shard_store.cpp:51-85), random-init-equivalent bytes",
             "config": {"workload": desc if world == 1 else desc.replace(
                            "all logical ranks on one B200 (intra-device relayout)",
-                           f"rank r on GPU r*{world}//8, one process per GPU"),
+                           f"rank r on GPU r*{world}//8, one process per GPU"
+                           + (" (all processes on one GPU: RS_BENCH_SAME_DEVICE)" if same_device else "")),
                        "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"],
-                       "tasks": summ["task_count"], "mode": args.mode, "placement": args.placement, "staging_bytes": args.staging_bytes,
-                       "strict_layers": bool(args.strict), "copy_kernel": copy_kernel_label(args.mode, world),
-                       "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed"},
-            "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "wall_s": round(wall, 3),
+                       "tasks": summ["task_count"], "mode": args.mode, "placement": args.placement,
+                       "staging_bytes": args.staging_bytes, "strict_layers": bool(args.strict),
+                       "copy_kernel": kernel_label(kname),
+                       "l2": "inputs 188.7 GB >> 126 MB L2: no flush needed" if not args.profile_layers
+                       else "profiling slice"},
+            "roofline": roof, "clocks": clocks, "gpu_launches": launches, "wall_s": round(wall, 3),
             "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}
+    if args.mode == "staged":
+        line["config"]["ring_same_slot"] = rep["ring_same_slot"]
+        line["config"]["peak_staging_bytes"] = rep["peak_staging_bytes"]
+
+    run_staged = args.mode == "direct" and not args.no_staged and (
+        not same_device or world == 1 or os.environ.get("RS_BENCH_STAGED"))
+    if run_staged:
+        line["staged"] = staged_leg(eng, sp, co, so, cn, sn, plan, traffic, args, world, rank, device, barrier, pk)
+    elif args.mode == "direct":
+        line["staged"] = {"skipped": "processes time-share one GPU (RS_BENCH_SAME_DEVICE): ring lanes of different "
+                                     "processes are never co-resident; set RS_BENCH_STAGED=1 to run it anyway"
+                          if same_device else "--no-staged"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_layers = int(os.environ.get("RS_BENCH_CPU_SAMPLE_LAYERS", "4"))  # ~12 s of single-thread work
@@ -543,8 +659,11 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-staged", action="store_true", help="skip the STAGED sub-object of a DIRECT run")
     ap.add_argument("--profile-layers", type=int, default=0, help="profiling slice (not a bench value)")
     args = ap.parse_args()
+    if args.strict and args.mode == "xfer":
+        ap.error("--strict applies to --mode direct / staged (xfer rounds are host-driven)")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -111,7 +111,8 @@ typedef struct {
                                copies in a multi-slot job), 1 = always rings, 2 = always direct */
 } rs_engine_options;
 
-#define RS_COPY_AUTO 0     /* engine default: RS_COPY_LDG8_NP */
+#define RS_COPY_AUTO 0     /* engine default: RS_COPY_TMA_NP when every descriptor is 16 B aligned with
+                              runs <= 16 KB and no descriptor stores into another slot, else RS_COPY_LDG8_NP */
 #define RS_COPY_LDG4 1     /* warp-per-row 16 B vectors, 4 loads in flight per lane */
 #define RS_COPY_LDG8 2     /* same, 8 loads in flight per lane, persistent grid (3 CTAs/SM) */
 #define RS_COPY_BULK 3     /* cp.async.bulk global->smem->global ring, one issuer per CTA */
@@ -140,6 +141,12 @@ typedef struct {
   double device_ms;           /* CUDA-event time of the run on the slowest device */
   double host_ms;             /* host wall time of the call */
   char error[512];
+  /* What ran (so a caller / the bench can tell which kernel moved the bytes
+   * without assuming it): the RS_COPY_* variant device 0's copy launches
+   * resolved to (DIRECT / host path; -1 none), and the STAGED policy for
+   * cross-rank tasks whose ranks share a GPU (1 rings, 2 direct, 0 n/a). */
+  int32_t copy_kernel;
+  int32_t ring_same_slot;
 } rs_exec_report;
 
 const char* rs_last_error(void);

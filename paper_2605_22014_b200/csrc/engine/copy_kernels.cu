@@ -5,6 +5,8 @@
 // 16 KB item); the LDG warp engine serves unaligned plans and peer stores;
 // the persistent / ring variants are kept as measured alternatives.
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include "desc.h"
@@ -273,17 +275,28 @@ __global__ void __launch_bounds__(32) rs_copy_tma_np_kernel(const rs_copy_desc* 
   bulk_wait_all();
 }
 
+// The dynamic shared-memory opt-in is a per-device function attribute: one
+// bit per device ordinal records where it has been set, so a process driving
+// several GPUs opts in on each of them (not just the first one launched on).
+template <class K>
+cudaError_t opt_in_smem(K* kernel, int smem, std::atomic<uint64_t>& configured) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (configured.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) configured.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 template <int W, int S, int L, uint32_t T>
 cudaError_t launch_bulk_mw(const rs_copy_desc* descs, const uint64_t* item0, uint32_t ndesc, uint64_t item_begin,
                            uint64_t item_end, int grid, cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const int smem = W * S * static_cast<int>(T);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_mw_kernel<W, S, L, T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = opt_in_smem(rs_copy_bulk_mw_kernel<W, S, L, T>, smem, configured);
+  if (e != cudaSuccess) return e;
   rs_copy_bulk_mw_kernel<W, S, L, T><<<grid, W * 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
   return cudaGetLastError();
 }
@@ -337,13 +350,10 @@ cudaError_t rs_launch_copy(const rs_copy_desc* descs, const uint64_t* item0, uin
     case 11: return launch_bulk_mw<8, 6, 4, 4096>(descs, item0, ndesc, item_begin, item_end, grid, stream);
     case 12: return launch_bulk_mw<16, 3, 2, 4096>(descs, item0, ndesc, item_begin, item_end, grid, stream);
     case 3: {
-      static bool configured = false;
+      static std::atomic<uint64_t> configured{0};
       const int smem = kBulkStages * static_cast<int>(kBulkStageBytes);
-      if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(rs_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-      }
+      cudaError_t e = opt_in_smem(rs_copy_bulk_kernel, smem, configured);
+      if (e != cudaSuccess) return e;
       rs_copy_bulk_kernel<<<grid, 32, smem, stream>>>(descs, item0, ndesc, item_begin, item_end);
       break;
     }

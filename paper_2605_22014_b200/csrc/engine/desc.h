@@ -78,8 +78,24 @@ typedef struct {
   uint64_t bytes;            // payload bytes in this batch
   uint64_t extent;           // slot bytes in use (last frame end), for the L2 discard
   uint32_t layer;            // layer of the batch's frames (trace)
-  uint32_t pad;
+  uint32_t layer_idx;        // index of that layer in the plan's layer order (strict layer barriers)
 } rs_batch_desc;
+
+// Strict layer order in STAGED mode (executor.cpp:208: all
+// layer-l traffic before any layer-(l+1) traffic): every CTA of the exchange
+// launch meets a barrier after each plan layer.  Two levels: the CTAs of one
+// GPU count in `arrive`; the last one publishes this slot's `done_self` flag
+// and, in a multi-GPU job, waits for every slot's flag (peer-mapped,
+// system scope) before releasing its GPU's CTAs through `release`.
+typedef struct {
+  uint32_t nlayers;                 // 0: no barriers (fused layers)
+  uint32_t nslots;                  // slots whose flags `done_all` lists (1: this GPU only)
+  unsigned long long* arrive;       // per-launch arrival counter (zeroed before the launch)
+  uint64_t* release;                // this GPU's release flag (epoch + layer + 1)
+  uint64_t* done_self;              // this slot's layer-done flag (in its comm arena)
+  const uint64_t* const* done_all;  // every slot's layer-done flag as mapped here (device array)
+  const uint64_t* local_layer_end;  // local-copy item end of each layer (device array, nlayers)
+} rs_layer_sync;
 
 // Transport trace (the RecordingTransport of proj/include/reshard/transport.hpp:50-75
 // on the device): one record per (batch, role) of the last STAGED run;

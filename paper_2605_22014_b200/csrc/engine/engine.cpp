@@ -132,10 +132,12 @@ std::int64_t Store::total_bytes() const {
 Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
   if (opts.num_devices < 1 || !opts.device_ids) throw DomainError("engine: no devices");
   if (opts.staging_bytes < 1) throw DomainError("engine: staging_bytes must be >= 1");
-  if (opts.strict_layers && opts.mode != RS_MODE_DIRECT)
-    // one launch per layer is a DIRECT-mode schedule; ring lanes already stream
-    // every link's batches in layer order (verified by rs_trace_read)
-    throw DomainError("engine: strict_layers applies to RS_MODE_DIRECT");
+  if (opts.strict_layers && opts.mode == RS_MODE_XFER)
+    // XFER rounds are host-driven chunk rounds of the comparator, not layers
+    throw DomainError("engine: strict_layers applies to RS_MODE_DIRECT and RS_MODE_STAGED");
+  if (opts.strict_layers && opts.mode == RS_MODE_STAGED && (opts.ring_discard & 8))
+    // the layer barriers live in the classic lane loop
+    throw DomainError("engine: strict_layers needs classic ring lanes (ring_discard without bit 8)");
   for (int i = 0; i < opts.num_devices; ++i)
     for (int j = 0; j < i; ++j)
       if (opts.device_ids[i] == opts.device_ids[j])
@@ -145,6 +147,8 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
                           " listed twice; one slot per GPU per process (several processes may share a GPU)");
   if (opts.mode != RS_MODE_DIRECT && opts.mode != RS_MODE_STAGED && opts.mode != RS_MODE_XFER)
     throw DomainError("engine: unknown mode");
+  if (opts.ring_same_slot < 0 || opts.ring_same_slot > 2)
+    throw DomainError("engine: ring_same_slot must be 0 (auto), 1 (rings) or 2 (direct)");
   if (opts_.ring_cta_threads == 0) opts_.ring_cta_threads = 256;
   if (opts_.ring_cta_threads != 256 && opts_.ring_cta_threads != 512 && opts_.ring_cta_threads != 1024)
     throw DomainError("engine: ring_cta_threads must be 256, 512 or 1024");
@@ -386,8 +390,10 @@ int Engine::grid_for(int dev, int which_kernel) const {
   return devices_[static_cast<std::size_t>(dev)].sms * per_sm;
 }
 
-// RS_COPY_AUTO = LDG8 at 3 CTAs (24 warps) per SM with 256 KB work items:
-// the best of the full-size C2 sweep on B200 (profiles/r1/sweep.jsonl).
+// Resolved copy kernel of a device's program (RS_COPY_* numbering).
+// RS_COPY_AUTO = the non-persistent TMA bulk copy (17) when every descriptor
+// is 16 B aligned with runs <= 16 KB and nothing is stored into another slot,
+// else the non-persistent LDG8 warp copy (15) -- see the default case.
 int Engine::copy_variant(int dev) const {
   switch (opts_.copy_kernel) {
     case RS_COPY_LDG4: return 1;
@@ -780,6 +786,7 @@ void Engine::upload_programs() {
       if (opts_.trace) p.d_trace = DeviceBuffer(dv.ordinal, 2 * std::max<std::size_t>(1, p.batches.size()) * sizeof(rs_trace_record));
       p.d_frames = DeviceBuffer(dv.ordinal, p.frames.size() * sizeof(rs_copy_desc));
       p.d_error = DeviceBuffer(dv.ordinal, sizeof(unsigned int));
+      if (opts_.strict_layers) upload_layer_sync(d);
       p.d_lanes.upload(p.lanes.data(), p.lanes.size() * sizeof(rs_lane_desc), dv.stream);
       p.d_batches.upload(p.batches.data(), p.batches.size() * sizeof(rs_batch_desc), dv.stream);
       p.d_frames.upload(p.frames.data(), p.frames.size() * sizeof(rs_copy_desc), dv.stream);
@@ -843,11 +850,18 @@ rs_exec_report Engine::run() {
         throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) +
                           " ring lanes exceed the co-resident CTA capacity " + std::to_string(cap) +
                           "; lower lanes_per_link");
-      if (!p.ntx && !p.nrx && !p.local_items) continue;
+      if (!p.ntx && !p.nrx && !p.local_items && !opts_.strict_layers) continue;
       DeviceGuard g(devices_[d].ordinal);
       if (opts_.trace && p.d_trace.size())
         cuda_check(cudaMemsetAsync(p.d_trace.data(), 0, p.d_trace.size(), devices_[d].stream), "trace reset");
       const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
+      // strict layers: zero the launch's arrival counter; the barrier flags
+      // are epoch-valued and never reset
+      rs_layer_sync sync{};
+      if (opts_.strict_layers) {
+        sync = p.layer_sync;
+        cuda_check(cudaMemsetAsync(sync.arrive, 0, sizeof(unsigned long long), devices_[d].stream), "memset");
+      }
       // ring slots in L2: 0 = default (discard + policies), else bit flags (2 = neither)
       const int ring_l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;
       cuda_check(rs_launch_exchange(lanes, static_cast<std::uint32_t>(p.ntx), lanes + p.ntx,
@@ -865,7 +879,7 @@ rs_exec_report Engine::run() {
                                         ((ring_l2 & 24) == 24 && opts_.ring_cta_threads == 256 ? 16 : 0),
                                     cap - p.ntx - p.nrx, opts_.ring_cta_threads,
                                     opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
-                                    devices_[d].stream),
+                                    opts_.strict_layers ? &sync : nullptr, devices_[d].stream),
                  "exchange kernel launch");
       ++launches;
     }
@@ -895,7 +909,15 @@ rs_exec_report Engine::run() {
   rep.device_ms = worst;
   rep.kernel_launches = launches;
   rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  describe_run(rep);
   return rep;
+}
+
+void Engine::describe_run(rs_exec_report& rep) const {
+  rep.copy_kernel = -1;
+  if (opts_.mode == RS_MODE_DIRECT && !devices_.empty() && !programs_.empty())
+    rep.copy_kernel = opts_.copy_kernel == RS_COPY_CE ? RS_COPY_CE : copy_variant(0);
+  rep.ring_same_slot = opts_.mode == RS_MODE_STAGED ? same_slot_policy() : 0;
 }
 
 // ------------------------------------------------------------ live handoff

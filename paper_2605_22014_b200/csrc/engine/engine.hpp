@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <map>
+#include <set>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -106,6 +107,9 @@ struct DeviceProgram {
   std::vector<rs_batch_desc> batches;
   std::vector<rs_copy_desc> frames;
   DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error, d_trace;
+  // STAGED strict layers: [arrival counter][release flag][done_all: nslots ptrs][layer item ends]
+  DeviceBuffer d_sync;
+  rs_layer_sync layer_sync{};
   std::uint64_t local_bytes = 0;
   bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
   std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)
@@ -197,10 +201,15 @@ class Engine {
     std::map<int, std::uint64_t> slot_bytes_of;      // dst rank -> ring slot bytes
     std::map<int, std::uint64_t> ring_bytes_of;      // dst rank -> bytes of all its rings
     std::map<int, int> k_of;                         // dst rank -> ring depth (K, or 1 for a tiny B)
+    std::set<int> direct_dst;                        // dst ranks whose B cannot hold a ring: direct stores
   };
   RingGeometry ring_geometry(const reshard::TransferPlan& plan) const;
   // STAGED: does this cross-rank task go through a ring (else a direct copy)?
   bool ringed(const reshard::TransferTask& t) const;
+  int same_slot_policy() const;  // resolved ring_same_slot: 1 rings, 2 direct copies
+  void describe_run(rs_exec_report& rep) const;  // which kernels / policy the run used
+  void upload_layer_sync(std::size_t dev);         // STAGED strict layers: barrier state of a device
+  char* layer_done_flag(int slot) const;           // a slot's layer-done flag in its comm arena
   struct CommLayout {
     std::vector<std::map<int, std::pair<std::size_t, std::size_t>>> regions;  // per slot: rank -> (offset, bytes)
     std::vector<std::size_t> slot_bytes;                                      // per slot, incl. flags

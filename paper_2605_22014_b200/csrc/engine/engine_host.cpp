@@ -241,6 +241,7 @@ rs_exec_report Engine::run_host(void* const* host_src, void* const* host_dst, in
   rep.device_ms = worst;
   rep.kernel_launches = launches;
   rep.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  describe_run(rep);
   return rep;
 }
 

@@ -59,10 +59,13 @@ char* Engine::comm_base(int slot) const {
   return imp ? imp->data() : nullptr;
 }
 
+int Engine::same_slot_policy() const {
+  return opts_.ring_same_slot == 0 ? (nslots_ > 1 ? 2 : 1) : opts_.ring_same_slot;
+}
+
 bool Engine::ringed(const reshard::TransferTask& t) const {
   if (t.is_local()) return false;
-  const int mode = opts_.ring_same_slot == 0 ? (nslots_ > 1 ? 2 : 1) : opts_.ring_same_slot;
-  if (mode == 1) return true;
+  if (same_slot_policy() == 1) return true;
   const Entry* se = stores_[RS_SRC].find(t.src_rank, t.tensor_index);
   const Entry* de = stores_[RS_DST].find(t.dst_rank, t.tensor_index);
   return !(se && de && se->slot == de->slot);
@@ -201,6 +204,19 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     if (sb >= 4096) sb = sb / kAlign * kAlign;
     else if (sb >= 16) sb = sb / 16 * 16;
     else if (need_eb[d]) sb = sb / need_eb[d] * need_eb[d];
+    if (sb < need_eb[d]) {
+      // B / inbound links < one element: no ring geometry fits the budget.
+      // The reference executor still succeeds (it needs B >= one element,
+      // executor.cpp:183-206), so this destination receives its bytes by
+      // direct stores into its shards -- zero staging, the budget holds.
+      geo.direct_dst.insert(d);
+      for (auto it = lanes_of.begin(); it != lanes_of.end();)
+        it = it->first.second == d ? lanes_of.erase(it) : std::next(it);
+      inbound_lanes[d] = 0;
+      slot_bytes_of[d] = 0;
+      geo.ring_bytes_of[d] = 0;
+      continue;
+    }
     slot_bytes_of[d] = sb;
     geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(k);
   }
@@ -271,8 +287,14 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   std::map<std::pair<int, int>, int> link_first_lane, link_cursor;
 
   std::vector<std::size_t> mark(devices_.size());
+  std::map<int, std::uint32_t> layer_idx;
+  for (std::size_t i = 0; i < plan_layers_.size(); ++i) layer_idx[plan_layers_[i]] = static_cast<std::uint32_t>(i);
   for (int layer : plan_layers_) {
     for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
+    // strict layers: a batch never spans two layers (the lanes meet a barrier
+    // between them), so every lane opens a fresh batch here
+    if (opts_.strict_layers)
+      for (auto& lb : lanes) lb.fill = lb.slot_bytes + 1;
     std::vector<std::size_t> lane_mark_batches(lanes.size()), lane_mark_frames(lanes.size());
     std::vector<std::uint64_t> lane_mark_fill(lanes.size());
     for (std::size_t i = 0; i < lanes.size(); ++i) {
@@ -316,7 +338,9 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
             delta.local_copy_bytes += t.bounds.element_count() * eb;
             continue;
           }
-          if (!ringed(t)) {  // cross-rank, both ranks on one GPU of a multi-slot job
+          if (!ringed(t) || geo.direct_dst.count(t.dst_rank)) {
+            // cross-rank, both ranks on one GPU of a multi-slot job, or a
+            // destination whose budget cannot host a ring (ring_geometry)
             local_copy(se, de, t.bounds, eb);
             delta.bytes_moved += t.bounds.element_count() * eb;
             continue;
@@ -401,7 +425,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
                         "re-run rs_comm_alloc_plan with this plan");
     auto& fr = flag_used[static_cast<std::size_t>(lb.dslot)];
     auto& fc = flag_used[static_cast<std::size_t>(lb.sslot)];
-    if (fr + flags_per_lane > kFlagBytes || fc + flags_per_lane > kFlagBytes)
+    if (fr + flags_per_lane > kFlagBytes - kSyncFlagBytes || fc + flags_per_lane > kFlagBytes - kSyncFlagBytes)
       throw DomainError("staged: too many ring lanes for the flag area; lower lanes_per_link");
     where[i].ready_off = fr;
     fr += flags_per_lane;
@@ -476,6 +500,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         Bd.extent = std::max(Bd.extent, f.off + n);
       }
       Bd.layer = lb.batches[b].empty() ? 0u : static_cast<std::uint32_t>(lb.batches[b].front().layer);
+      Bd.layer_idx = lb.batches[b].empty() ? 0u : layer_idx.at(lb.batches[b].front().layer);
       Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
       Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
       Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
@@ -542,6 +567,42 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);
     p.nrx = static_cast<int>(p.lanes.size()) - p.ntx;
   }
+}
+
+char* Engine::layer_done_flag(int slot) const {
+  char* b = comm_base(slot);
+  return b ? b + comm_bytes(slot) - kSyncFlagBytes : nullptr;
+}
+
+// STAGED strict layers: the barrier state of one local device -- an arrival
+// counter, a release flag, the address (as mapped in this process) of every
+// slot's layer-done flag, and the local-copy item end of every plan layer.
+void Engine::upload_layer_sync(std::size_t d) {
+  DeviceProgram& p = programs_[d];
+  const Device& dv = devices_[d];
+  const std::size_t nl = p.layers.size();
+  const std::size_t ns = nslots_ > 1 ? static_cast<std::size_t>(nslots_) : 0;
+  std::vector<std::uint64_t> words(2 + ns + nl, 0);
+  for (std::size_t s = 0; s < ns; ++s) {
+    char* f = layer_done_flag(static_cast<int>(s));
+    if (!f)
+      throw DomainError("staged strict_layers: comm arena of slot " + std::to_string(s) +
+                        " not mapped in this process (rs_arena_import RS_COMM on every process)");
+    words[2 + s] = addr(f);
+  }
+  for (std::size_t li = 0; li < nl; ++li) words[2 + ns + li] = p.layers[li].item_end;
+  DeviceGuard g(dv.ordinal);
+  p.d_sync = DeviceBuffer(dv.ordinal, words.size() * sizeof(std::uint64_t));
+  p.d_sync.upload(words.data(), words.size() * sizeof(std::uint64_t), dv.stream);
+  auto* base = reinterpret_cast<std::uint64_t*>(p.d_sync.data());
+  p.layer_sync = rs_layer_sync{};
+  p.layer_sync.nlayers = static_cast<std::uint32_t>(nl);
+  p.layer_sync.nslots = static_cast<std::uint32_t>(ns);
+  p.layer_sync.arrive = reinterpret_cast<unsigned long long*>(base);
+  p.layer_sync.release = base + 1;
+  p.layer_sync.done_self = ns ? reinterpret_cast<std::uint64_t*>(layer_done_flag(dv.slot)) : nullptr;
+  p.layer_sync.done_all = reinterpret_cast<const std::uint64_t* const*>(base + 2);
+  p.layer_sync.local_layer_end = base + 2 + ns;
 }
 
 }  // namespace rsb

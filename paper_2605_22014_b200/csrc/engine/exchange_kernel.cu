@@ -63,6 +63,36 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
   return true;
 }
 
+// Strict layer barrier `li`: the whole CTA calls it after its
+// layer-li work.  Arrivals are cumulative over the launch (a CTA cannot pass
+// barrier li before every CTA arrived at it), so one counter serves every
+// layer.  The GPU's last arriver publishes the slot's layer-done flag, waits
+// for every slot's (peer-mapped, system scope) and releases its GPU.
+// Bounded like every ring wait: false = abort (error flag raised).
+__device__ __noinline__ bool layer_barrier(const rs_layer_sync& S, uint32_t li, uint64_t epoch,
+                                           unsigned int* error_flag, uint64_t spin_limit) {
+  __shared__ int passed;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t want = epoch + li + 1;
+    bool ok = true;
+    __threadfence_system();  // this CTA's layer-li stores (peer rings / shards) before its arrival
+    const unsigned long long n = atomicAdd(S.arrive, 1ull) + 1ull;
+    if (n == static_cast<unsigned long long>(li + 1) * gridDim.x) {
+      if (S.nslots) {
+        st_release_sys(S.done_self, want);
+        for (uint32_t s = 0; ok && s < S.nslots; ++s) ok = wait_geq(S.done_all[s], want, error_flag, spin_limit, true);
+      }
+      if (ok) st_release_gpu(S.release, want);
+    } else {
+      ok = wait_geq(S.release, want, error_flag, spin_limit, false);
+    }
+    passed = ok;
+  }
+  __syncthreads();
+  return passed != 0;
+}
+
 // Drop one 128 B line from L2 without writing it back (its value becomes
 // undefined).  A drained ring slot is rewritten by the next batch, so its
 // dirty lines never need to reach HBM: with slots small enough to stay
@@ -157,7 +187,8 @@ __global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
     uint32_t nrx, const rs_batch_desc* __restrict__ batches,
     const rs_copy_desc* __restrict__ frames, const rs_copy_desc* __restrict__ local_descs,
     const uint64_t* __restrict__ local_item0, uint32_t nlocal, uint64_t local_items, uint64_t epoch,
-    unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace) {
+    unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace,
+    const rs_layer_sync sync) {
   const int lane_id = threadIdx.x & 31;
   const int warp_in_block = threadIdx.x >> 5;
   const int warps_per_block = blockDim.x >> 5;
@@ -301,8 +332,12 @@ __global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
       }
       return;
     } else {
+    uint32_t li = 0;  // strict: layer barriers passed so far
     for (uint32_t b = 0; b < L.nbatches; ++b) {
       const rs_batch_desc B = batches[L.batch0 + b];
+      // strict: batches never span layers; meet the barriers of the layers before this batch's
+      for (; li < sync.nlayers && li < B.layer_idx; ++li)
+        if (!layer_barrier(sync, li, epoch, error_flag, spin_limit)) return;
       const uint32_t slot = b % L.slots;
       const uint64_t seq = epoch + b + 1;           // value published for batch b
       if (threadIdx.x == 0) {
@@ -356,6 +391,8 @@ __global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
         }
       }
     }
+    for (; li < sync.nlayers; ++li)
+      if (!layer_barrier(sync, li, epoch, error_flag, spin_limit)) return;
     return;
     }  // classic lanes
   }
@@ -363,6 +400,19 @@ __global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
   // local copy role
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x - ntx - nrx) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x - ntx - nrx) * blockDim.x) >> 5;
+  if (sync.nlayers) {  // strict: layer by layer, a barrier after each
+    uint64_t begin = 0;
+    for (uint32_t li = 0; li < sync.nlayers; ++li) {
+      const uint64_t end = sync.local_layer_end[li];
+      for (uint64_t item = begin + warp; item < end; item += nwarps) {
+        const uint32_t di = find_desc(local_item0, nlocal, item);
+        warp_copy_item<true, 8>(local_descs[di], item - local_descs[di].item0, lane_id);
+      }
+      begin = end;
+      if (!layer_barrier(sync, li, epoch, error_flag, spin_limit)) return;
+    }
+    return;
+  }
   for (uint64_t item = warp; item < local_items; item += nwarps) {
     const uint32_t di = find_desc(local_item0, nlocal, item);
     warp_copy_item<true, 8>(local_descs[di], item - local_descs[di].item0, lane_id);
@@ -378,9 +428,15 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
                                const rs_copy_desc* local_descs, const uint64_t* local_item0,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
                                unsigned int* error_flag, uint64_t spin_limit, int flags,
-                               int local_blocks, int threads, rs_trace_record* trace, cudaStream_t stream) {
-  const int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
+                               int local_blocks, int threads, rs_trace_record* trace,
+                               const rs_layer_sync* sync_in, cudaStream_t stream) {
+  rs_layer_sync sync{};
+  if (sync_in) sync = *sync_in;
+  int grid = static_cast<int>(ntx + nrx) + (local_items ? local_blocks : 0);
+  // strict: a slot with no work of its own still meets every layer barrier
+  if (grid == 0 && sync.nlayers) grid = 1;
   if (grid == 0) return cudaSuccess;
+  if (sync.nlayers && (flags & kExWarpSpec)) return cudaErrorInvalidValue;  // classic lanes only
   const int smem = (flags & kExLaneTma) ? (threads / 32 - 1) * static_cast<int>(kLaneTmaBytes) : 0;
   const bool ws = (flags & kExWarpSpec) != 0;
   if (smem > 48 * 1024) {  // TMA lanes: 256-thread warp-specialised kernel only
@@ -390,7 +446,7 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
 #define RS_EXCHANGE_LAUNCH(T, W)                                                                                 \
   rs_exchange_kernel<T, W><<<grid, T, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, local_descs,  \
                                                       local_item0, nlocal, local_items, epoch, error_flag,         \
-                                                      spin_limit, flags, trace)
+                                                      spin_limit, flags, trace, sync)
   if (threads == 1024) {
     if (ws) RS_EXCHANGE_LAUNCH(1024, true); else RS_EXCHANGE_LAUNCH(1024, false);
   } else if (threads == 512) {

@@ -27,6 +27,7 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
                                uint32_t nlocal, uint64_t local_items, uint64_t epoch,
                                unsigned int* error_flag, uint64_t spin_limit, int flags,
                                int local_blocks, int threads, rs_trace_record* trace,
+                               const rs_layer_sync* sync,  // NULL or nlayers == 0: fused layers
                                cudaStream_t stream);  // flags: 1 fault-inject, 2 L2 discard, 4 L2 policies
 
 // which: 0 LDG4, 3 LDG8, 5 LDG16, 6 CTA8, 4 bulk, 1 pattern, 2/7/8 exchange 256/512/1024 threads

@@ -107,7 +107,8 @@ class ExecReport(C.Structure):
                 ("peak_staging_bytes", C.c_int64), ("bytes_moved", C.c_int64),
                 ("local_copy_bytes", C.c_int64), ("carryover_bytes", C.c_int64),
                 ("layers_processed", C.c_int32), ("kernel_launches", C.c_int32),
-                ("device_ms", C.c_double), ("host_ms", C.c_double), ("error", C.c_char * 512)]
+                ("device_ms", C.c_double), ("host_ms", C.c_double), ("error", C.c_char * 512),
+                ("copy_kernel", C.c_int32), ("ring_same_slot", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {"ok": bool(self.ok),
@@ -119,7 +120,8 @@ class ExecReport(C.Structure):
                 "layers_processed": int(self.layers_processed),
                 "kernel_launches": int(self.kernel_launches),
                 "device_ms": float(self.device_ms), "host_ms": float(self.host_ms),
-                "error": self.error.decode()}
+                "error": self.error.decode(),
+                "copy_kernel": int(self.copy_kernel), "ring_same_slot": int(self.ring_same_slot)}
 
 
 class SwitchStats(C.Structure):

@@ -212,6 +212,9 @@ LLAMA = {
     "llama2-13b": (5120, 40, 40, 40, 128, 13824, 32000),
     # test scale: same tensor structure (GQA fused QKV, SwiGLU fc1), tiny dims
     "llama-mini": (256, 4, 16, 8, 16, 688, 1000),
+    # same, with ffn / vocab multiples of 64: every TP split of every tensor is
+    # a 16 B-aligned run, so the default DIRECT kernel is the TMA bulk copy
+    "llama-mini-a16": (256, 4, 16, 8, 16, 704, 1024),
 }
 
 # bf16 model weights + fp32 master weights + fp32 Adam m / v
@@ -281,6 +284,13 @@ def sliced_case(name: str, num_layers: int):
         spec = llama(arch, num_layers, zero=name == "c3z")
     c_old = dataclasses.replace(c_old, layer_stage=None)
     c_new = dataclasses.replace(c_new, layer_stage=None)
+    if name == "c4" and num_layers >= 3:
+        # keep C4's point: an uneven PP2 stage migration (21/19 of 40 layers at
+        # full size -> ceil(21 L / 40), never an even split, on an L-layer slice)
+        first = -(-21 * num_layers // 40)
+        if 2 * first == num_layers:
+            first += 1
+        c_new = dataclasses.replace(c_new, layer_stage=[0] * first + [1] * (num_layers - first))
     return spec, c_old, c_new
 
 

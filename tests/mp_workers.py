@@ -49,11 +49,13 @@ def ipc_reshard(rank, world, mode):
     co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
     so = [i * world // co.world for i in range(co.world)]
     sn = [(i + 1) * world // cn.world % world for i in range(cn.world)]  # shifted placement
-    copy_kernel = 0
+    copy_kernel, strict = 0, False
     if mode == "direct-tma":  # TMA bulk stores into the peer process's IPC-mapped arena
         mode, copy_kernel = "direct", 17
+    if mode == "staged-strict":  # layer barriers across the two slots (peer-mapped done flags)
+        mode, strict = "staged", True
     eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
-                   first_local_slot=rank, copy_kernel=copy_kernel)
+                   first_local_slot=rank, copy_kernel=copy_kernel, strict_layers=strict)
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
     eng.alloc(RS_SRC)

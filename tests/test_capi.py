@@ -63,8 +63,21 @@ def test_engine_rejects_duplicate_devices_before_touching_cuda():
         R.Engine([0, 0])
 
 
-def test_strict_layers_is_a_direct_mode_option():
+def test_strict_layers_option_checks():
+    """strict_layers is a DIRECT / STAGED schedule (XFER rounds are host
+    driven); STAGED barriers need the classic lanes.  Checked before CUDA."""
     from paper_2605_22014_b200 import reshard as R
     import pytest
     with pytest.raises(N.DomainError, match="strict_layers"):
-        R.Engine([0], mode="staged", strict_layers=True)
+        R.Engine([0], mode="xfer", strict_layers=True)
+    with pytest.raises(N.DomainError, match="strict_layers"):
+        R.Engine([0], mode="staged", strict_layers=True, ring_discard=8 | 5)
+
+
+def test_ring_same_slot_is_validated():
+    """a typo in ring_same_slot must not silently select a policy."""
+    from paper_2605_22014_b200 import reshard as R
+    import pytest
+    for bad in (3, -1):
+        with pytest.raises(N.DomainError, match="ring_same_slot"):
+            R.Engine([0], mode="staged", ring_same_slot=bad)

@@ -61,14 +61,28 @@ def test_random_pairs_bitexact(mode, golden, oracle_c):
         eng.close()
 
 
-@pytest.mark.parametrize("mode,copy_kernel", [("direct", 1), ("direct", 2), ("direct", 3), ("staged", 0)])
+RS_COPY_TMA_NP, RS_COPY_LDG8_NP = 17, 15
+
+
+@pytest.mark.parametrize("mode,copy_kernel", [("direct", 0), ("direct", RS_COPY_TMA_NP), ("direct", RS_COPY_LDG8_NP),
+                                              ("direct", 1), ("direct", 2), ("direct", 3), ("staged", 0)])
 def test_c1_gpt2_bitexact(mode, copy_kernel, golden, oracle_c):
+    """Full GPT-2 C1 against the reference executor's own destination digest
+    (oracle/_ref, tests/golden/c1_exec.json), for the default kernel (0 =
+    auto, which must resolve to the TMA bulk copy that carries the headline
+    bench) and every explicit variant."""
     sp, co, cn = specs.baseline_case("c1")
     eng = make_engine(sp, co, cn, mode, 1 << 30 if mode == "direct" else 256 << 20, lanes_per_link=2,
                       copy_kernel=copy_kernel)
     plan = R.compute_transfer_plan(co, cn, sp)
     rep = R.execute_plan(plan, eng)
     want = golden["c1_exec"]["1073741824"]
+    if mode == "direct" and copy_kernel in (0, RS_COPY_TMA_NP):
+        assert rep["copy_kernel"] == RS_COPY_TMA_NP, rep  # the headline kernel ran
+    elif mode == "direct":
+        assert rep["copy_kernel"] == copy_kernel, rep
+    else:
+        assert rep["copy_kernel"] == -1 and rep["ring_same_slot"] == 1, rep
     assert rep["ok"] and rep["bytes_moved"] == want["bytes_moved"]
     assert rep["local_copy_bytes"] == want["local_copy_bytes"]
     assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"]
@@ -498,6 +512,45 @@ def test_tensor_beyond_2_32_elements(mode):
     eng.close()
 
 
+def test_strict_layers_staged_global_layer_order(golden, oracle_c):
+    """STAGED strict_layers: every CTA of the launch meets a barrier after each
+    plan layer, so the transport trace shows the reference's global order
+    (executor.cpp:208): every layer-l batch (both roles) ends
+    before any layer-(l+1) batch begins.  Bytes stay bit-exact."""
+    sp = mini_llama(4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 1)
+    eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=2, ring_slot_kib=4, trace=True,
+                      strict_layers=True)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0, rep
+    text = plan.text()
+    orep, ostore = oracle_c.execute(sp, co, cn, text, SEED, 1 << 20)
+    for (ti, rank), want in ostore.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), want), (ti, rank)
+    tr = eng.trace(0)
+    layers = sorted({r["layer"] for r in tr})
+    assert len(layers) == 4
+    for a, b in zip(layers, layers[1:]):
+        end_a = max(r["t_end"] for r in tr if r["layer"] == a)
+        begin_b = min(r["t_begin"] for r in tr if r["layer"] == b)
+        assert begin_b >= end_a - 1000, (a, b, end_a, begin_b)  # globaltimer granularity
+    # repeated strict runs (epoch-valued barrier flags, fresh arrival counter)
+    for _ in range(3):
+        assert eng.run()["ok"]
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
+    # every golden random pair, strict STAGED, against the reference's digests
+    rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
+    for seed, sp, co, cn in specs.iter_random_cases(60, golden["random_pairs"]["base_seed"]):
+        want = rows[seed]["exec"]["4096"]
+        eng = make_engine(sp, co, cn, "staged", 1 << 16, lanes_per_link=1, strict_layers=True)
+        rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+        assert rep["ok"] and rep["layers_processed"] == want["layers_processed"], (seed, rep)
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"], seed
+        eng.close()
+
+
 def test_transport_trace_layer_order_and_causality():
     """STAGED transport trace (rs_trace_read, the reference's RecordingTransport
     on the device): every remote byte appears once per role; each lane
@@ -545,7 +598,26 @@ def test_tiny_staging_budget_like_reference(mode, golden, oracle_c):
         eng.close()
 
 
-@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_budget_below_one_element_per_inbound_link(oracle_c):
+    """B = 32 bytes, 16 inbound links into one destination (TP16 -> TP1, fp32):
+    no ring fits (32 / 16 < 4 bytes), the reference executor still succeeds
+    (B >= one element), so that destination gets direct stores -- same bytes,
+    ok, zero staging."""
+    sp = specs.ModelSpec("fan-in", 1, [specs.TensorSpec("W", 0, [64, 48], 0, "param", 4),
+                                       specs.TensorSpec("b", 0, [64], 0, "param", 4)], 4)
+    co, cn = specs.iota_config(1, 16, 1, 1), specs.iota_config(2, 1, 1, 1)
+    text = oracle_c.plan_text(sp, co, cn)[0]
+    orep, ostore = oracle_c.execute(sp, co, cn, text, SEED, 32)
+    eng = make_engine(sp, co, cn, "staged", 32)
+    rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+    assert rep["ok"] and orep["ok"], rep["error"]
+    assert rep["bytes_moved"] == orep["bytes_moved"] and rep["peak_staging_bytes"] == 0
+    for (ti, rank), want in ostore.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), want), (ti, rank)
+    eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged", "direct-ldg8"])
 def test_spec_known_answer_cases_on_device(mode, golden, oracle_ref):
     """The SPEC's known-answer resizes (TP4->TP8 column / row split, DP2->DP4
     replicated, identity, PP layer move; tests/golden/kat.json from the
@@ -560,10 +632,15 @@ def test_spec_known_answer_cases_on_device(mode, golden, oracle_ref):
         co, cn = cfg_from_json(case["old"]), cfg_from_json(case["new"])
         plan = R.compute_transfer_plan(co, cn, sp)
         assert plan.text() == case["plan"], case["name"]
-        eng = make_engine(sp, co, cn, mode, 1 << 20)
+        if mode == "direct-ldg8":
+            eng = make_engine(sp, co, cn, "direct", 1 << 20, copy_kernel=RS_COPY_LDG8_NP)
+        else:
+            eng = make_engine(sp, co, cn, mode, 1 << 20)
         rep = R.execute_plan(plan, eng)
         orep, ostore = oracle_ref.execute(sp, co, cn, case["plan"], SEED, 1 << 20)
         assert rep["ok"] and orep["ok"], case["name"]
+        if mode == "direct":  # every KAT spec is 16 B aligned: the default is the TMA bulk copy
+            assert rep["copy_kernel"] == RS_COPY_TMA_NP, (case["name"], rep)
         assert (rep["bytes_moved"], rep["local_copy_bytes"]) == (orep["bytes_moved"], orep["local_copy_bytes"])
         for (ti, rank), want in ostore.entries.items():
             assert np.array_equal(eng.read(RS_DST, rank, ti), want), (case["name"], ti, rank)
@@ -587,3 +664,22 @@ def test_ring_same_slot_policy(same_slot, golden, oracle_c):
             assert rep["peak_staging_bytes"] == 0
         assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == want["dst_sha"], seed
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged", "staged-strict"])
+def test_c4_uneven_stage_migration_on_device(mode):
+    """BASELINE config 4's point on the device: Llama-2-13B shapes, TP2PP4 ->
+    TP4PP2 with an uneven new stage split (4-layer slice: 3/1, the full-size
+    21/19 proportion), bf16 + fp32 master/m/v; every destination byte checked
+    against the analytic pattern (pinned to the reference's fill_pattern)."""
+    sp, co, cn = specs.sliced_case("c4", 4)
+    assert cn.layer_stage == [0, 0, 0, 1]
+    strict = mode == "staged-strict"
+    eng = make_engine(sp, co, cn, "staged" if strict else mode, 1 << 30, strict_layers=strict)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    assert R.verify_plan(plan, co, cn) == []
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["bytes_moved"] + rep["local_copy_bytes"] == plan.total_bytes(), rep
+    assert rep["layers_processed"] == 4
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
