@@ -6,6 +6,7 @@
 #include <sstream>
 #include <stdexcept>
 
+#include "records.hpp"
 #include "reshard_b200/reshard.hpp"
 
 namespace reshard {
@@ -150,55 +151,42 @@ std::vector<std::string> ModelSpec::validate() const {
 }
 
 ModelSpec ModelSpec::parse(const std::string& text) {
+  using SpecLine = records::Line<std::invalid_argument>;
   ModelSpec m;
   bool have_model = false;
-  std::istringstream in(text);
-  std::string line;
-  int lineno = 0;
-  while (std::getline(in, line)) {
-    ++lineno;
-    if (auto h = line.find('#'); h != std::string::npos) line.resize(h);
-    std::istringstream ls(line);
-    std::string kind;
-    if (!(ls >> kind)) continue;
-    auto fail = [&](const std::string& why) {
-      throw std::invalid_argument("spec parse: line " + std::to_string(lineno) + ": " + why);
-    };
-    if (kind == "model") {
-      std::string kl, kb;
-      if (!(ls >> m.name >> kl >> m.num_layers >> kb >> m.bytes_per_element) || kl != "layers" ||
-          kb != "bpe")
-        fail("bad model record");
+  records::for_each_line(text, true, [&](std::string_view line, int lineno) {
+    SpecLine in(line, "spec parse", lineno);
+    if (in.blank()) return;
+    if (in.kind() == "model") {
+      // model <name> layers <L> bpe <bytes per element>
+      m.name = std::string(in.word("model name"));
+      if (in.word("'layers'") != "layers") in.fail("bad model record");
+      m.num_layers = in.number<int>("layer count");
+      if (in.word("'bpe'") != "bpe") in.fail("bad model record");
+      m.bytes_per_element = in.number<std::int64_t>("bytes per element");
       have_model = true;
-    } else if (kind == "tensor") {
+    } else if (in.kind() == "tensor") {
+      // tensor <id> <layer> <d0,d1,...> <tp axis | -> <param|m1|m2> <bytes per element> [dp=<axis>]
       TensorSpec t;
-      std::string shape, axis, role;
-      if (!(ls >> t.tensor_id >> t.layer >> shape >> axis >> role >> t.element_bytes))
-        fail("bad tensor record");
-      std::string opt;
-      while (ls >> opt) {  // optional key=value extensions
-        if (opt.rfind("dp=", 0) == 0) t.dp_shard_axis = std::stoi(opt.substr(3));
-        else fail("unknown tensor option " + opt);
-      }
-      std::size_t pos = 0;
-      while (pos <= shape.size()) {
-        std::size_t comma = shape.find(',', pos);
-        std::string tok = shape.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
-        if (tok.empty()) fail("bad shape");
-        t.shape.push_back(std::stoll(tok));
-        if (comma == std::string::npos) break;
-        pos = comma + 1;
-      }
-      if (axis != "-") t.tp_shard_axis = std::stoi(axis);
+      t.tensor_id = std::string(in.word("tensor id"));
+      t.layer = in.number<int>("layer");
+      t.shape = in.int_list("shape");
+      if (const auto axis = in.word("tp axis"); axis != "-") t.tp_shard_axis = std::stoi(std::string(axis));
+      const auto role = in.word("role");
       if (role == "param") t.role = TensorRole::kParameter;
       else if (role == "m1") t.role = TensorRole::kOptimizerMoment1;
       else if (role == "m2") t.role = TensorRole::kOptimizerMoment2;
-      else fail("unknown role " + role);
+      else in.fail("unknown role " + std::string(role));
+      t.element_bytes = in.number<std::int64_t>("element bytes");
+      while (auto opt = in.maybe_word()) {  // optional key=value extensions
+        if (opt->substr(0, 3) == "dp=") t.dp_shard_axis = std::stoi(std::string(opt->substr(3)));
+        else in.fail("unknown tensor option " + std::string(*opt));
+      }
       m.tensors.push_back(std::move(t));
     } else {
-      fail("unknown record '" + kind + "'");
+      in.fail("unknown record '" + std::string(in.kind()) + "'");
     }
-  }
+  });
   if (!have_model) throw std::invalid_argument("spec parse: missing model record");
   return m;
 }

@@ -10,7 +10,7 @@ import pytest
 from paper_2605_22014_b200 import specs
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HOST = ["model.cpp", "layout.cpp", "planner.cpp", "plan_io.cpp", "placement.cpp"]
+HOST = ["model.cpp", "layout.cpp", "planner.cpp", "plan_text.cpp", "placement.cpp"]
 
 
 def test_planner_is_sanitizer_clean(tmp_path):

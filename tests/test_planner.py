@@ -161,3 +161,20 @@ def test_c3_distributed_optimizer_plan(oracle_c):
     ti = next(i for i, t in enumerate(sp.tensors) if t.tensor_id == "L0.embed.master")
     v0, v1 = R.view(sp, ti, cn, 0), R.view(sp, ti, cn, 4)
     assert v0 and v1 and v0 != v1
+
+
+def test_plan_text_rejects_malformed_records():
+    """read_plan parses every field strictly (records.hpp) and names the line;
+    write_plan -> read_plan -> write_plan is the identity on golden plans
+    (test above), and the optional ' local' flag / unknown header keys are
+    accepted like the reference's reader (transfer_plan.cpp:73-141)."""
+    from paper_2605_22014_b200.native import IntegrityError
+    sp = specs.ModelSpec("w", 1, [specs.TensorSpec("W", 0, [8, 8], 0, "param", 4)], 4)
+    ok = "plan src_gen=1 dst_gen=2 note=x\ntask W 0 0 1 0:4,0:8 128\ntask W 0 1 1 4:8,0:8 128 local\nkeep W 0 1 4:8,0:8 128\n"
+    plan = R.read_plan(ok, sp)
+    assert plan.text() == ok.replace(" note=x", "")
+    for bad, where in (("task W 0 0 x 0:4,0:8 128\n", "line 2"), ("task W 0 0 1 0-4,0:8 128\n", "bounds"),
+                       ("task W 0 0 1 0:4,0:8\n", "byte size"), ("keep W 0 1 4:8,0:8 12z\n", "byte size"),
+                       ("frob W\n", "unknown record")):
+        with pytest.raises(IntegrityError, match=where):
+            R.read_plan("plan src_gen=1 dst_gen=2\n" + bad, sp)
