@@ -10,9 +10,12 @@
 //   plan       proj/include/reshard/transfer_plan.hpp:18-82
 //   planner    proj/include/reshard/planner.hpp:14-47
 //   chunking   proj/include/reshard/executor.hpp:43-44
-// Execution (the reference's execute_plan over a host Transport,
-// proj/include/reshard/executor.hpp:50-53) is replaced by the device engine
-// behind the C ABI in rs_reshard.h.
+//   execution  proj/include/reshard/{executor,shard_store,transport}.hpp
+// execute_plan keeps the reference's signature (executor.hpp:50-53) and runs
+// the plan on the B200 engine (the same code as rs_execute_host); the
+// Transport argument selects the device transport and receives the per-frame
+// accounting.  include/reshard/*.hpp forward the reference's header names
+// here, so a reference caller compiles unchanged.
 //
 // Extension over the reference: TensorSpec::element_bytes (0 = the model's
 // bytes_per_element) so bf16 params and fp32 master/Adam state share one plan.
@@ -25,6 +28,7 @@
 #include <optional>
 #include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 namespace reshard {
@@ -254,5 +258,138 @@ struct PlacementResult {
 PlacementResult choose_placement(const ParallelConfig& c_old, const ParallelConfig& c_new,
                                  const ModelSpec& model, const std::vector<int>& candidates,
                                  const PlacementOptions& options = {});
+
+// ------------------------------------------------------------------ execution
+// The reference's execution surface (proj/include/reshard/executor.hpp:16-53,
+// shard_store.hpp:14-50, transport.hpp:16-75) over the device engine.
+
+struct ExecutionReport {
+  bool ok = false;
+  std::string error;
+  std::optional<int> failed_layer;
+  std::int64_t peak_staging_bytes = 0;  // resident ring capacity per destination rank, max (<= staging_bytes)
+  std::int64_t bytes_moved = 0;         // cross-rank task bytes
+  std::int64_t local_copy_bytes = 0;
+  int layers_processed = 0;
+};
+
+// One framed point-to-point chunk of a transfer task.
+struct Frame {
+  std::uint32_t tensor_index = 0;
+  int layer = 0;
+  ShardView bounds;
+  std::vector<std::uint8_t> data;
+};
+
+// Point-to-point transport (reference interface).  On the device path no
+// host Frame is materialised: execute_plan reports every chunk the engine
+// moved across ranks through on_device_frame (plan order, layer by layer)
+// and calls barrier() after each layer, like the reference's executor.
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual void send(int src, int dst, Frame frame) = 0;
+  virtual std::optional<std::pair<int, Frame>> receive(int dst) = 0;
+  virtual void barrier() = 0;
+  virtual std::int64_t bytes_sent() const = 0;
+  // extension: a chunk of `bytes` payload bytes went src -> dst on the device
+  virtual void on_device_frame(int layer, int src, int dst, std::uint32_t tensor_index, const ShardView& bounds,
+                               std::int64_t bytes);
+};
+
+// In-memory loopback: per-link FIFOs for host frames (lowest source first),
+// plus the byte count of device frames.
+class LoopbackTransport : public Transport {
+ public:
+  void send(int src, int dst, Frame frame) override;
+  std::optional<std::pair<int, Frame>> receive(int dst) override;
+  void barrier() override {}
+  std::int64_t bytes_sent() const override { return bytes_sent_; }
+  void on_device_frame(int layer, int src, int dst, std::uint32_t tensor_index, const ShardView& bounds,
+                       std::int64_t bytes) override;
+
+ private:
+  std::map<std::pair<int, int>, std::vector<Frame>> queues_;  // (dst, src) -> FIFO
+  std::map<std::pair<int, int>, std::size_t> heads_;
+  std::int64_t bytes_sent_ = 0;
+};
+
+// Per-event trace (layer, src, dst, bytes) of everything passing through.
+class RecordingTransport : public Transport {
+ public:
+  struct Event {
+    std::int64_t sequence = 0;
+    int layer = 0;
+    int src = 0;
+    int dst = 0;
+    std::int64_t bytes = 0;
+  };
+  explicit RecordingTransport(Transport& inner) : inner_(inner) {}
+  void send(int src, int dst, Frame frame) override;
+  std::optional<std::pair<int, Frame>> receive(int dst) override { return inner_.receive(dst); }
+  void barrier() override { inner_.barrier(); }
+  std::int64_t bytes_sent() const override { return inner_.bytes_sent(); }
+  void on_device_frame(int layer, int src, int dst, std::uint32_t tensor_index, const ShardView& bounds,
+                       std::int64_t bytes) override;
+  const std::vector<Event>& events() const { return events_; }
+
+ private:
+  Transport& inner_;
+  std::vector<Event> events_;
+  std::int64_t next_sequence_ = 0;
+};
+
+// Extension: choose how the device moves cross-rank chunks -- bounded
+// staging rings (STAGED, the reference's staging-budget semantics; default for
+// any other Transport) or direct stores into the destination shards (DIRECT).
+class DeviceTransport : public LoopbackTransport {
+ public:
+  enum class Mode { kStaged, kDirect };
+  explicit DeviceTransport(Mode mode = Mode::kStaged, int device = 0) : mode_(mode), device_(device) {}
+  Mode mode() const { return mode_; }
+  int device() const { return device_; }
+
+ private:
+  Mode mode_;
+  int device_;
+};
+
+// Host-resident per-(rank, tensor) shard buffers, row-major over each view.
+class ShardStore {
+ public:
+  struct Entry {
+    ShardView view;
+    std::vector<std::uint8_t> bytes;
+  };
+  // zero-filled buffers for every present view under `config`
+  static ShardStore allocate(const ModelSpec& model, const ParallelConfig& config);
+
+  bool has(int rank, std::uint32_t tensor_index) const;
+  Entry& at(int rank, std::uint32_t tensor_index);
+  const Entry& at(int rank, std::uint32_t tensor_index) const;
+  // the reference pattern (shard_store.cpp:51-85), generated on the device
+  void fill_pattern(const ModelSpec& model, std::uint64_t seed);
+  static std::uint8_t pattern_byte(std::uint32_t tensor_index, std::int64_t element, std::int64_t byte_in_element,
+                                   std::uint64_t seed);
+  std::int64_t total_bytes() const;
+  std::size_t entry_count() const { return entries_.size(); }
+  // extension: the model and layout the store was allocated for (the device
+  // engine lays its shard buffers out from them)
+  const ModelSpec& model() const { return model_; }
+  const ParallelConfig& config() const { return config_; }
+
+ private:
+  std::map<std::pair<int, std::uint32_t>, Entry> entries_;
+  ModelSpec model_;
+  ParallelConfig config_;
+};
+
+// Runs `plan` from src_store (C_old) into dst_store (C_new) on the device:
+// stores go H2D, the engine executes layer by layer within `staging_bytes`
+// of staging per destination rank, results come back D2H.  Integrity
+// failures come back as ok = false + error + failed_layer (executor.cpp:210-215);
+// CUDA errors throw std::runtime_error.
+ExecutionReport execute_plan(const TransferPlan& plan, const ShardStore& src_store, ShardStore& dst_store,
+                             Transport& transport, std::int64_t staging_bytes, std::int64_t bytes_per_element);
 
 }  // namespace reshard
