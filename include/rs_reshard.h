@@ -97,7 +97,7 @@ typedef struct {
   int32_t first_local_slot; /* slots [first, first+num_devices) are driven by this process */
   int64_t spin_limit;       /* ring flag polls before a wait fails (0: default ~10 s) */
   int32_t fault_inject;     /* test hook: 1 = ring receivers drop out (peer failure) */
-  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 128, -1: no cap,
+  int32_t ring_slot_kib;    /* STAGED: cap on one ring slot in KiB (0: default 64 stream / 128 classic, -1: no cap,
                                slot = B / (inbound lanes x K)); B stays the upper bound */
   int32_t ring_discard;     /* STAGED ring mode bit flags (0 = default 1|4; 2 = none):
                                1 receivers drop drained slot lines (discard.global.L2);
@@ -109,6 +109,12 @@ typedef struct {
   int32_t ring_same_slot;   /* STAGED, cross-rank tasks whose ranks share a GPU: 0 = auto (rings
                                on a one-slot engine -- the transport is what runs -- and direct
                                copies in a multi-slot job), 1 = always rings, 2 = always direct */
+  int32_t ring_kernel;      /* STAGED lane kernel: 0 = auto (TMA stream lanes when every frame is
+                               16 B aligned and strict_layers is off, else classic), 1 = classic
+                               register lanes (rs_exchange_kernel), 2 = TMA stream lanes
+                               (rs_stream_lane_kernel; falls back to classic when ineligible) */
+  int32_t ring_stages;      /* stream lanes: 16 KB shared-memory stages per lane end (0: default 2;
+                               1, 2, 3, 4, 6, 8, 10 or 13) */
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default: RS_COPY_TMA_NP when every descriptor is 16 B aligned with

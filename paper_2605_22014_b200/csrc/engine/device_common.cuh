@@ -142,13 +142,18 @@ __device__ __forceinline__ void row_offsets(const rs_copy_desc& D, uint32_t r, i
                                             int64_t& dof) {
   so = 0;
   dof = 0;
-  for (uint32_t k = 0; k < D.nouter; ++k) {
-    const uint32_t e = static_cast<uint32_t>(D.ext[k]);
-    const uint32_t q = r / e;
-    const uint32_t i = r - q * e;
-    so += static_cast<int64_t>(i) * D.sstr[k];
-    dof += static_cast<int64_t>(i) * D.dstr[k];
-    r = q;
+  // unrolled over the fixed capacity (constant indices: a descriptor held by
+  // value stays in registers)
+#pragma unroll
+  for (uint32_t k = 0; k < RS_MAX_OUTER; ++k) {
+    if (k < D.nouter) {
+      const uint32_t e = static_cast<uint32_t>(D.ext[k]);
+      const uint32_t q = r / e;
+      const uint32_t i = r - q * e;
+      so += static_cast<int64_t>(i) * D.sstr[k];
+      dof += static_cast<int64_t>(i) * D.dstr[k];
+      r = q;
+    }
   }
 }
 

@@ -149,6 +149,14 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
     throw DomainError("engine: unknown mode");
   if (opts.ring_same_slot < 0 || opts.ring_same_slot > 2)
     throw DomainError("engine: ring_same_slot must be 0 (auto), 1 (rings) or 2 (direct)");
+  if (opts.ring_kernel < 0 || opts.ring_kernel > 2)
+    throw DomainError("engine: ring_kernel must be 0 (auto), 1 (classic) or 2 (stream)");
+  // stream lanes: 2 x 16 KB stages -> 7 lane CTAs per SM; more lanes beat
+  // deeper lanes (profiles/r2/stream_sweep.jsonl)
+  if (opts_.ring_stages == 0) opts_.ring_stages = 2;
+  if (opts_.ring_stages != 1 && opts_.ring_stages != 2 && opts_.ring_stages != 3 && opts_.ring_stages != 4 && opts_.ring_stages != 6 &&
+      opts_.ring_stages != 8 && opts_.ring_stages != 10 && opts_.ring_stages != 13)
+    throw DomainError("engine: ring_stages must be 1, 2, 3, 4, 6, 8, 10 or 13");
   if (opts_.ring_cta_threads == 0) opts_.ring_cta_threads = 256;
   if (opts_.ring_cta_threads != 256 && opts_.ring_cta_threads != 512 && opts_.ring_cta_threads != 1024)
     throw DomainError("engine: ring_cta_threads must be 256, 512 or 1024");
@@ -176,6 +184,8 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
     cuda_check(cudaEventCreate(&d.ev_begin), "event");
     cuda_check(cudaEventCreate(&d.ev_end), "event");
     cuda_check(cudaEventCreate(&d.ev_call), "event");
+    cuda_check(cudaStreamCreateWithFlags(&d.aux, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&d.ev_aux, cudaEventDisableTiming), "event");
     devices_.push_back(d);
   }
   for (auto& a : devices_)
@@ -209,6 +219,8 @@ Engine::~Engine() {
     if (d.ev_begin) cudaEventDestroy(d.ev_begin);
     if (d.ev_end) cudaEventDestroy(d.ev_end);
     if (d.ev_call) cudaEventDestroy(d.ev_call);
+    if (d.aux) cudaStreamDestroy(d.aux);
+    if (d.ev_aux) cudaEventDestroy(d.ev_aux);
   }
 }
 
@@ -845,6 +857,10 @@ rs_exec_report Engine::run() {
     epoch_ += 1ull << 32;
     for (std::size_t d = 0; d < devices_.size(); ++d) {
       DeviceProgram& p = programs_[d];
+      if (p.stream_lanes) {
+        launches += run_stream_lanes(d);
+        continue;
+      }
       const int cap = grid_for(static_cast<int>(d), exchange_kernel_id());
       if (p.ntx + p.nrx >= cap)
         throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) +

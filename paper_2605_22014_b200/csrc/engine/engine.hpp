@@ -115,6 +115,7 @@ struct DeviceProgram {
   std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)
   std::uint64_t max_row_bytes = 0; // longest contiguous run (TMA-NP items must fit shared memory)
   bool peer_stores = false;        // some descriptor writes another slot's memory (NVLink peer / IPC)
+  bool stream_lanes = false;       // STAGED: this device's lanes run rs_stream_lane_kernel
 };
 
 struct Device {
@@ -125,6 +126,8 @@ struct Device {
   cudaStream_t h2d = nullptr, d2h = nullptr;  // host-store copies (rs_execute_host)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   cudaEvent_t ev_call = nullptr;  // rs_switch: the moment the switch was requested
+  cudaStream_t aux = nullptr;     // STAGED stream lanes: the local copies beside the lane kernel
+  cudaEvent_t ev_aux = nullptr;
 };
 
 class Engine {
@@ -207,6 +210,9 @@ class Engine {
   // STAGED: does this cross-rank task go through a ring (else a direct copy)?
   bool ringed(const reshard::TransferTask& t) const;
   int same_slot_policy() const;  // resolved ring_same_slot: 1 rings, 2 direct copies
+  bool stream_lanes_wanted() const;  // STAGED: TMA stream lanes requested / chosen by auto
+  int lane_capacity(int dev) const;  // co-resident lane CTAs of the device's lane kernel
+  int run_stream_lanes(std::size_t dev);  // enqueue the stream-lane launch + local copies; returns launches
   void describe_run(rs_exec_report& rep) const;  // which kernels / policy the run used
   void upload_layer_sync(std::size_t dev);         // STAGED strict layers: barrier state of a device
   char* layer_done_flag(int slot) const;           // a slot's layer-done flag in its comm arena

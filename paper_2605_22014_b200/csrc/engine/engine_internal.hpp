@@ -15,6 +15,7 @@ constexpr std::size_t kAlign = 256;
 constexpr std::size_t kFlagBytes = 1 << 20;  // ring flags per slot (131072 u64)
 constexpr std::size_t kSyncFlagBytes = 256;   // tail of a slot's flag area: the strict-layer done flag
 constexpr std::uint64_t kRingSlotDefault = 128u << 10;  // default ring slot cap (rs_engine_options.ring_slot_kib)
+constexpr std::uint64_t kRingSlotStreamDefault = 64u << 10;  // same, stream lanes
 constexpr std::uint64_t kSpinLimit = 200000000ull;
 
 inline std::uint64_t key(int rank, std::uint32_t ti) {

@@ -4,6 +4,7 @@
 // chunk_bounds cuts tasks to the ring slot size, a destination rank's rings
 // live in its budget B.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <exception>
 #include <thread>
@@ -126,9 +127,11 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     for (const auto& kv : plan.carryover_by_layer)
       for (const auto& k : kv.second) local_total += static_cast<std::uint64_t>(k.byte_size);
     const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
-    double frac = std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
+    // stream lanes: the local copies run as their own launch beside the lane
+    // kernel, so the lanes may take (almost) every co-resident CTA slot
+    double frac = stream_lanes_wanted() ? 0.98 : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
     if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
-    const int capacity = static_cast<int>(grid_for(0, exchange_kernel_id()) * frac);
+    const int capacity = static_cast<int>(lane_capacity(0) * frac);
     int max_lanes = 64;  // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than 32)
     if (const char* env = std::getenv("RS_RING_MAX_LANES")) max_lanes = std::atoi(env);
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
@@ -168,8 +171,11 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   // spill to DRAM (profiles/r1/ring_sweep_v3.jsonl).  The kernel adds
   // evict-first / evict-last L2 policies and discards drained slots by
   // default (ring_sweep_v4.jsonl: 15.4 -> 13.1 ms on the C5 slice).
+  // stream lanes: 64 KiB slots (4 stage-sized items per batch) keep ~450
+  // lanes' rings in L2 (profiles/r2/stream_sweep.jsonl: 128 KiB -> 48 ms, 64 KiB -> 38.7 ms on full C2)
+  const std::uint64_t slot_default = stream_lanes_wanted() ? kRingSlotStreamDefault : kRingSlotDefault;
   const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
-                                 : opts_.ring_slot_kib == 0 ? kRingSlotDefault
+                                 : opts_.ring_slot_kib == 0 ? slot_default
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
   auto& inbound_lanes = geo.inbound_lanes;
   for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
@@ -475,6 +481,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   }
   std::uint64_t item_div = 32;  // work items per slot (RS_FRAME_ITEMS overrides; diagnostic)
   if (const char* env = std::getenv("RS_FRAME_ITEMS")) item_div = std::max(1, std::atoi(env));
+  const bool stream = stream_lanes_wanted();  // items = one 16 KB shared-memory stage of a stream lane
   std::vector<std::vector<rs_copy_desc>> lane_frames(lanes.size());
   std::vector<std::vector<rs_batch_desc>> lane_batches(lanes.size());
   auto build_lane = [&](std::size_t i) {
@@ -485,7 +492,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     batches.reserve(lb.batches.size());
     // work items inside a batch: ~32 per slot so all 8 warps of the lane's
     // CTA share even a small (L2-resident) slot
-    const std::uint64_t frame_item = std::clamp<std::uint64_t>(lb.slot_bytes / item_div, 2048, 65536);
+    const std::uint64_t frame_item =
+        stream ? 16384 : std::clamp<std::uint64_t>(lb.slot_bytes / item_div, 2048, 65536);
     for (std::size_t b = 0; b < lb.batches.size(); ++b) {
       const std::uint64_t slot_addr = ring_addr + (b % static_cast<std::size_t>(lb.k)) * lb.slot_bytes;
       rs_batch_desc Bd{};
@@ -566,7 +574,119 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     for (std::size_t i = 0; i < lanes.size(); ++i)
       if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);
     p.nrx = static_cast<int>(p.lanes.size()) - p.ntx;
+    // stream lanes need every frame this device touches to be bulk-copyable:
+    // 16 B aligned runs of <= one 16 KB stage (the slot-side layout and the
+    // flag protocol are the same for both lane kernels, so processes may differ)
+    p.stream_lanes = stream && !p.lanes.empty();
+    for (const auto& f : p.frames)
+      if (f.vec_log2 != 4 || f.row_bytes > 16384 || f.rows_per_item * f.row_bytes > 16384) {
+        p.stream_lanes = false;
+        break;
+      }
   }
+}
+
+bool Engine::stream_lanes_wanted() const {
+  if (opts_.mode != RS_MODE_STAGED) return false;
+  if (opts_.ring_kernel == 1) return false;
+  if (opts_.strict_layers || (opts_.ring_discard & 8)) return false;  // barriers / warp-specialised: classic only
+  return true;
+}
+
+int Engine::lane_capacity(int dev) const {
+  if (stream_lanes_wanted())
+    return devices_[static_cast<std::size_t>(dev)].sms * std::max(1, stream_max_blocks_per_sm(opts_.ring_stages));
+  return grid_for(dev, exchange_kernel_id());
+}
+
+// Stream lanes: the lane kernel on the device stream (launched first, so its
+// CTAs -- which wait on each other -- are all resident), the local copies as
+// a TMA / LDG copy launch on the aux stream beside it, joined before ev_end.
+int Engine::run_stream_lanes(std::size_t d) {
+  DeviceProgram& p = programs_[d];
+  Device& dv = devices_[d];
+  const int cap = lane_capacity(static_cast<int>(d));
+  if (p.ntx + p.nrx > cap)
+    throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) + " stream lanes exceed the co-resident CTA capacity " +
+                      std::to_string(cap) + "; lower lanes_per_link");
+  DeviceGuard g(dv.ordinal);
+  int launches = 0;
+  if (opts_.trace && p.d_trace.size())
+    cuda_check(cudaMemsetAsync(p.d_trace.data(), 0, p.d_trace.size(), dv.stream), "trace reset");
+  const int ring_l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;
+  static const int stream_flags = [] {  // diagnostics: RS_STREAM_FLAGS (64 = register stores), RS_STREAM_PROF
+    const char* e = std::getenv("RS_STREAM_FLAGS");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const bool prof_on = std::getenv("RS_STREAM_PROF") != nullptr;
+  DeviceBuffer prof;
+  if (prof_on && p.ntx + p.nrx) {
+    prof = DeviceBuffer(dv.ordinal, 64ull * static_cast<std::size_t>(p.ntx + p.nrx));
+    cuda_check(cudaMemsetAsync(prof.data(), 0, prof.size(), dv.stream), "memset");
+  }
+  if (p.ntx + p.nrx) {
+    const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
+    cuda_check(rs_launch_stream_exchange(lanes, static_cast<std::uint32_t>(p.ntx), lanes + p.ntx,
+                                         static_cast<std::uint32_t>(p.nrx),
+                                         reinterpret_cast<const rs_batch_desc*>(p.d_batches.data()),
+                                         reinterpret_cast<const rs_copy_desc*>(p.d_frames.data()), epoch_,
+                                         reinterpret_cast<unsigned int*>(p.d_error.data()),
+                                         opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit) : kSpinLimit,
+                                         (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | stream_flags,
+                                         opts_.ring_stages,
+                                         opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
+                                         prof.size() ? reinterpret_cast<unsigned long long*>(prof.data()) : nullptr,
+                                         dv.stream),
+               "stream lane kernel launch");
+    ++launches;
+    if (prof.size()) {  // diagnostic summary on stderr: mean cycles per phase, senders / receivers
+      std::vector<unsigned long long> h(prof.size() / 8);
+      cuda_check(cudaMemcpyAsync(h.data(), prof.data(), prof.size(), cudaMemcpyDeviceToHost, dv.stream), "prof");
+      cuda_check(cudaStreamSynchronize(dv.stream), "prof");
+      double acc[2][9] = {};
+      int n[2] = {0, 0};
+      for (std::size_t i = 0; i < h.size() / 8; ++i) {
+        const int role = h[8 * i + 6] ? 0 : 1;
+        ++n[role];
+        for (int k = 0; k < 8; ++k) acc[role][k] += static_cast<double>(h[8 * i + k]);
+        acc[role][1] -= static_cast<double>(h[8 * i + 1]);
+        acc[role][1] += static_cast<double>(h[8 * i + 1] & 0xffffffffull);
+        acc[role][8] += static_cast<double>(h[8 * i + 1] >> 32);
+      }
+      for (int role = 0; role < 2; ++role)
+        if (n[role])
+          std::fprintf(stderr,
+                       "[stream prof] %s lanes=%d total=%.0f load_loop=%.0f reuse_wait=%.0f store_issue=%.0f "
+                       "publish_wait=%.0f idle=%.0f items=%.0f land_latency_per_item=%.0f (cycles, mean per lane)\n",
+                       role ? "rx" : "tx", n[role], acc[role][0] / n[role], acc[role][8] / n[role],
+                       acc[role][1] / n[role], acc[role][2] / n[role], acc[role][3] / n[role], acc[role][4] / n[role],
+                       acc[role][5] / n[role], acc[role][7] / std::max(1.0, acc[role][5]));
+    }
+  }
+  static const int local_after = [] {  // diagnostic: 1 = local copies after the lanes, same stream
+    const char* e = std::getenv("RS_STREAM_LOCAL_AFTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (p.local_items && local_after) {
+    cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
+                              reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
+                              static_cast<std::uint32_t>(p.local.size()), 0, p.local_items,
+                              copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), dv.stream),
+               "local copy launch");
+    return launches + 1;
+  }
+  if (p.local_items) {
+    cuda_check(cudaStreamWaitEvent(dv.aux, dv.ev_begin, 0), "wait");
+    cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
+                              reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
+                              static_cast<std::uint32_t>(p.local.size()), 0, p.local_items,
+                              copy_grid(static_cast<int>(d)), copy_variant(static_cast<int>(d)), dv.aux),
+               "local copy launch");
+    ++launches;
+    cuda_check(cudaEventRecord(dv.ev_aux, dv.aux), "event");
+    cuda_check(cudaStreamWaitEvent(dv.stream, dv.ev_aux, 0), "wait");
+  }
+  return launches;
 }
 
 char* Engine::layer_done_flag(int slot) const {

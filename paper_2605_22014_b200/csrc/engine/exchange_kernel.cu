@@ -419,6 +419,356 @@ __global__ void __launch_bounds__(kThreads, 768 / kThreads) rs_exchange_kernel(
   }
 }
 
+// ------------------------------------------------------------ stream lanes
+//
+// TMA-pipelined ring lanes (RS_RING_STREAM).  One 1-warp CTA per lane end.
+// The classic lanes move a batch through registers, 32 KB in flight per CTA,
+// and a 9.6 us pack of a 128 KiB slot is latency-bound (profiles/r1
+// trace_capacity.jsonl: ~10 GB/s per lane).  Here the warp streams the
+// lane's items through kStages x 16 KB shared-memory stages with bulk copies:
+// loads run up to kStages items ahead of the stores and across batch
+// boundaries (a sender prefetches the next batch's source rows before its
+// credit arrives; a receiver returns the credit as soon as a batch's slot
+// bytes have landed in shared memory, before its destination stores finish),
+// so ~kStages x 16 KB are in flight per lane without registers.  Rows are
+// dealt to the 32 lanes, each issuing its own bulk copies; the slot side of an
+// item is contiguous and moves as one bulk copy.  Flags / credits / epochs are
+// the classic lanes' protocol (bounded waits, .sys scope across GPUs).
+constexpr uint32_t kStreamStageBytes = 16384;
+
+// wait until at most n of this thread's bulk groups are still reading smem
+__device__ __forceinline__ void bulk_wait_read_dyn(uint32_t n) {
+  switch (n) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    case 3: bulk_wait_read<3>(); break;
+    case 4: bulk_wait_read<4>(); break;
+    case 5: bulk_wait_read<5>(); break;
+    case 6: bulk_wait_read<6>(); break;
+    case 7: bulk_wait_read<7>(); break;
+    case 8: bulk_wait_read<8>(); break;
+    case 9: bulk_wait_read<9>(); break;
+    case 10: bulk_wait_read<10>(); break;
+    case 11: bulk_wait_read<11>(); break;
+    case 12: bulk_wait_read<12>(); break;
+    case 13: bulk_wait_read<13>(); break;
+    default: bulk_wait_read<14>(); break;
+  }
+}
+
+// Is the descriptor's source (src_side) / destination run sequence one
+// contiguous span?  (A packed ring-slot frame is.)
+__device__ __forceinline__ bool side_contiguous(const rs_copy_desc& D, bool src_side) {
+  uint64_t span = D.row_bytes;
+  bool contiguous = true;
+#pragma unroll
+  for (uint32_t k = 0; k < RS_MAX_OUTER; ++k) {
+    if (k < D.nouter) {
+      const int64_t st = src_side ? D.sstr[k] : D.dstr[k];
+      contiguous = contiguous && st == static_cast<int64_t>(span);
+      span *= D.ext[k];
+    }
+  }
+  return contiguous;
+}
+
+// Walks a lane's work items in order: batch b, its frames [f, fend), item k
+// of nk.  The current frame's descriptor is held by value (registers): one
+// broadcast load per frame instead of a global re-read per field per item
+// (the bulk-copy asm clobbers memory, so a reference would be re-loaded).
+struct ItemCursor {
+  uint32_t b = 0, f = 0, fend = 0;
+  uint64_t k = 0, nk = 0;
+  bool first_of_batch = true;  // the item at the cursor opens batch b
+  bool src_contig = false, dst_contig = false;
+  rs_copy_desc D;
+};
+
+__device__ __forceinline__ void cursor_load_frame(ItemCursor& c, const rs_copy_desc* frames) {
+  c.D = frames[c.f];
+  c.nk = (c.D.rows + c.D.rows_per_item - 1) / c.D.rows_per_item;
+  c.src_contig = side_contiguous(c.D, true);
+  c.dst_contig = side_contiguous(c.D, false);
+}
+
+// position the cursor on the first item of batch b (or past the end)
+__device__ __forceinline__ void cursor_open(ItemCursor& c, const rs_lane_desc& L, const rs_batch_desc* batches,
+                                            const rs_copy_desc* frames, bool sender, uint32_t b) {
+  c.b = b;
+  c.k = 0;
+  c.first_of_batch = true;
+  while (c.b < L.nbatches) {
+    const rs_batch_desc& B = batches[L.batch0 + c.b];
+    c.f = sender ? B.pack0 : B.unpack0;
+    c.fend = c.f + (sender ? B.npack : B.nunpack);
+    if (c.f < c.fend) {
+      cursor_load_frame(c, frames);
+      return;
+    }
+    ++c.b;  // (an empty batch still needs its flag: never emitted by compile_staged)
+  }
+}
+
+// advance one item; returns true when the item just passed was its batch's last
+__device__ __forceinline__ bool cursor_next(ItemCursor& c, const rs_lane_desc& L, const rs_batch_desc* batches,
+                                            const rs_copy_desc* frames, bool sender) {
+  c.first_of_batch = false;
+  if (++c.k < c.nk) return false;
+  c.k = 0;
+  if (++c.f < c.fend) {
+    cursor_load_frame(c, frames);
+    return false;
+  }
+  cursor_open(c, L, batches, frames, sender, c.b + 1);
+  return true;
+}
+
+// Issue the loads of item (D, k) into `stage` (lanes split the rows; the
+// slot side, when contiguous, is one copy by lane 0).  Lane 0 has armed the
+// stage's mbarrier with the item's bytes.
+__device__ __forceinline__ void stream_item_load(const rs_copy_desc& D, bool contiguous, uint64_t k,
+                                                 unsigned char* stage, uint64_t* bar, uint64_t pol, int lane) {
+  const uint64_t r0 = k * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  if (contiguous) {
+    if (lane == 0) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r0), so, dof);
+      bulk_load_hint(stage, reinterpret_cast<const void*>(D.src + so), static_cast<uint32_t>((r1 - r0) * D.row_bytes),
+                     bar, pol);
+    }
+    return;
+  }
+  for (uint64_t r = r0 + lane; r < r1; r += 32) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    bulk_load_hint(stage + (r - r0) * D.row_bytes, reinterpret_cast<const void*>(D.src + so),
+                   static_cast<uint32_t>(D.row_bytes), bar, pol);
+  }
+}
+
+__device__ __forceinline__ void stream_item_store(const rs_copy_desc& D, bool contiguous, uint64_t k,
+                                                  const unsigned char* stage, uint64_t pol, int lane) {
+  const uint64_t r0 = k * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  if (contiguous) {
+    if (lane == 0) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r0), so, dof);
+      bulk_store_hint(reinterpret_cast<void*>(D.dst + dof), stage, static_cast<uint32_t>((r1 - r0) * D.row_bytes), pol);
+    }
+  } else {
+    for (uint64_t r = r0 + lane; r < r1; r += 32) {
+      int64_t so, dof;
+      row_offsets(D, static_cast<uint32_t>(r), so, dof);
+      bulk_store_hint(reinterpret_cast<void*>(D.dst + dof), stage + (r - r0) * D.row_bytes,
+                      static_cast<uint32_t>(D.row_bytes), pol);
+    }
+  }
+  bulk_commit();  // one group per item on every lane (possibly empty): stage reuse counts groups
+}
+
+// Same as stream_item_store, through registers: the warp reads the stage
+// (ld.shared) and writes the rows with 16 B stores, so the stage is free as
+// soon as the loop ends (no bulk-store read-out to wait for).
+__device__ __forceinline__ void stream_item_store_regs(const rs_copy_desc& D, uint64_t k, const unsigned char* stage,
+                                                       uint64_t pol, int lane) {
+  const uint64_t r0 = k * D.rows_per_item;
+  const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  const uint64_t rb = D.row_bytes;
+  for (uint64_t r = r0; r < r1; ++r) {
+    int64_t so, dof;
+    row_offsets(D, static_cast<uint32_t>(r), so, dof);
+    const uint4* src = reinterpret_cast<const uint4*>(stage + (r - r0) * rb);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(D.dst) + dof);
+    const uint32_t n = static_cast<uint32_t>(rb >> 4);
+    uint32_t i = static_cast<uint32_t>(lane);
+    for (; i + 96 < n; i += 128) {
+      const uint4 a = src[i], b = src[i + 32], c = src[i + 64], d = src[i + 96];
+      store_hint(dst + i, a, pol);
+      store_hint(dst + i + 32, b, pol);
+      store_hint(dst + i + 64, c, pol);
+      store_hint(dst + i + 96, d, pol);
+    }
+    for (; i < n; i += 32) store_hint(dst + i, src[i], pol);
+  }
+  // the stage's next bulk load (async proxy) is ordered after these reads
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int kExStreamRegStore = 64;  // stream lanes: stores from the stage through registers
+
+template <int kStages>
+__global__ void __launch_bounds__(32) rs_stream_lane_kernel(
+    const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
+    uint32_t nrx, const rs_batch_desc* __restrict__ batches, const rs_copy_desc* __restrict__ frames,
+    uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace,
+    unsigned long long* __restrict__ prof) {
+  extern __shared__ __align__(128) unsigned char stages[];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  const int lane = threadIdx.x;
+  const bool sender = blockIdx.x < ntx;
+  if (blockIdx.x >= ntx + nrx) return;
+  if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
+  const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
+  const bool peer = (L.flags & RS_LANE_PEER) != 0;
+  if (lane == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  // sender: shard rows in evict-first, slot out evict-last; receiver: slot in
+  // evict-first (it is discarded next), shard out evict-first
+  const uint64_t ld_pol = pol_first, st_pol = sender ? pol_last : pol_first;
+
+  ItemCursor ld, st;
+  cursor_open(ld, L, batches, frames, sender, 0);
+  cursor_open(st, L, batches, frames, sender, 0);
+  uint64_t g_ld = 0, g_st = 0;       // items loaded (issued) / stored (issued)
+  uint32_t ready_b = 0xffffffffu;    // receiver: batch whose ready flag was acquired last
+  uint32_t credit_b = 0xffffffffu;   // sender: batch whose slot credit was acquired last
+  uint64_t idle = 0;
+  // register stores: 64 both roles, 128 receivers only, 256 senders only
+  const bool reg_store = (flags & kExStreamRegStore) || ((flags & 128) && !sender) || ((flags & 256) && sender);
+  uint64_t prof_reuse = 0, prof_store = 0, prof_pub = 0, prof_idle = 0, prof_items = 0;
+  const uint64_t prof_t0 = clock64();
+  __shared__ uint64_t t_open[kStages];  // trace: flag-acquire time of each open batch (<= kStages open)
+  __shared__ uint64_t t_issue[kStages];  // diagnostic: load issue time per stage
+  uint64_t prof_land = 0, prof_loadloop = 0;
+
+  auto flag_up = [&](uint32_t b) -> bool {  // lane 0 polls, the warp agrees
+    int up = 0;
+    if (lane == 0) {
+      if (sender) {
+        up = b < L.slots ||
+             (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + b % L.slots)
+                   : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + b % L.slots)) >=
+                 epoch + b - L.slots + 1;
+      } else {
+        up = (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)
+                   : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)) >=
+             epoch + b + 1;
+      }
+    }
+    return __shfl_sync(0xffffffffu, up, 0) != 0;
+  };
+
+  while (st.b < L.nbatches) {
+    bool progress = false;
+    // ---- loads: up to kStages items ahead of the stores
+    const uint64_t tl0 = prof ? clock64() : 0;
+    while (ld.b < L.nbatches && g_ld - g_st < static_cast<uint64_t>(kStages)) {
+      if (!sender && ld.first_of_batch && ready_b != ld.b) {
+        if (!flag_up(ld.b)) break;
+        ready_b = ld.b;
+        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[ld.b % kStages]));
+        fence_proxy_async_global();  // the slot bytes were published through the generic proxy
+      }
+      const uint32_t s = static_cast<uint32_t>(g_ld % kStages);
+      if (g_ld >= static_cast<uint64_t>(kStages) && !reg_store) {  // the stage's previous item must have been read out
+        const uint64_t t0 = prof ? clock64() : 0;
+        bulk_wait_read_dyn(static_cast<uint32_t>(g_st - 1 - (g_ld - kStages)));
+        if (prof && lane == 0) prof_reuse += clock64() - t0;
+      }
+      const uint64_t r0 = ld.k * ld.D.rows_per_item;
+      const uint32_t bytes = static_cast<uint32_t>((min(r0 + ld.D.rows_per_item, ld.D.rows) - r0) * ld.D.row_bytes);
+      if (lane == 0) mbar_expect_tx(&bar[s], bytes);
+      if (prof && lane == 0) t_issue[s] = clock64();
+      __syncwarp();
+      stream_item_load(ld.D, ld.src_contig, ld.k, stages + static_cast<size_t>(s) * kStreamStageBytes, &bar[s], ld_pol,
+                       lane);
+      cursor_next(ld, L, batches, frames, sender);
+      ++g_ld;
+      progress = true;
+    }
+    if (prof && lane == 0) prof_loadloop += clock64() - tl0;
+    // ---- stores of landed items, in order
+    while (g_st < g_ld) {
+      const uint32_t s = static_cast<uint32_t>(g_st % kStages);
+      const uint32_t parity = static_cast<uint32_t>((g_st / kStages) & 1);
+      // lane 0 tests, the warp agrees; every lane then observes the completed
+      // phase itself (acquire of the bulk-loaded bytes it is about to store)
+      const int landed = lane == 0 ? mbar_test(&bar[s], parity) : 0;
+      if (!__shfl_sync(0xffffffffu, landed, 0)) break;
+      mbar_wait(&bar[s], parity);
+      if (prof && lane == 0) prof_land += clock64() - t_issue[s];
+      if (sender && st.first_of_batch && credit_b != st.b) {
+        if (!flag_up(st.b)) break;  // the receiver has not drained this slot yet
+        credit_b = st.b;
+        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[st.b % kStages]));
+      }
+      const uint32_t b = st.b;
+      const uint64_t ts0 = prof ? clock64() : 0;
+      if (reg_store)
+        stream_item_store_regs(st.D, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane);
+      else
+        stream_item_store(st.D, st.dst_contig, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane);
+      if (prof && lane == 0) prof_store += clock64() - ts0;
+      const bool last = cursor_next(st, L, batches, frames, sender);
+      ++g_st;
+      progress = true;
+      if (!last) continue;
+      const rs_batch_desc& B = batches[L.batch0 + b];
+      const uint32_t slot = b % L.slots;
+      if (sender) {
+        // the batch's slot writes complete, then one release publishes them
+        const uint64_t tw0 = prof ? clock64() : 0;
+        if (!reg_store) {
+          bulk_wait_all();
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        if (prof && lane == 0) prof_pub += clock64() - tw0;
+        if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
+      } else {
+        // every slot byte of batch b is in shared memory: drop the slot's
+        // lines from L2 and hand the slot back (the shard stores still run)
+        if ((flags & kExDiscard) && B.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
+          const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(slot) * L.slot_bytes;
+          const uint64_t lines = (B.extent + 127) >> 7;
+          for (uint64_t i = lane; i < lines; i += 32) discard_l2_line(base + (i << 7));
+        }
+        __syncwarp();
+        if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
+      }
+      if (trace && lane == 0) record_batch(trace, L, B, b, sender ? 0 : 1, t_open[b % kStages]);
+    }
+    if (progress) {
+      idle = 0;
+      continue;
+    }
+    int stop = 0;
+    const uint64_t ti0 = prof ? clock64() : 0;
+    if (lane == 0) {
+      if (*reinterpret_cast<volatile unsigned int*>(error_flag)) stop = 1;
+      else if (++idle > spin_limit) {
+        atomicExch(error_flag, 1u);
+        stop = 1;
+      } else {
+        __nanosleep(32);
+      }
+    }
+    if (prof && lane == 0) prof_idle += clock64() - ti0;
+    if (__shfl_sync(0xffffffffu, stop, 0)) break;
+  }
+  bulk_wait_all();  // shared memory stays valid until every store has read it
+  if (prof && lane == 0) {  // diagnostic: cycles per phase, per lane end
+    unsigned long long* p = prof + 8ull * blockIdx.x;
+    p[0] = clock64() - prof_t0;
+    p[1] = prof_reuse;
+    p[2] = prof_store;
+    p[3] = prof_pub;
+    p[4] = prof_idle;
+    p[5] = g_st;
+    p[6] = sender;
+    p[7] = prof_land;
+    p[1] = prof_reuse | (prof_loadloop << 32);  // (packed: reuse wait low, load loop high; both < 2^32 per slice run)
+    (void)prof_items;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -456,6 +806,56 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const
   }
 #undef RS_EXCHANGE_LAUNCH
   return cudaGetLastError();
+}
+
+cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const rs_lane_desc* lanes_rx,
+                                      uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
+                                      uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags,
+                                      int stages, rs_trace_record* trace, unsigned long long* prof,
+                                      cudaStream_t stream) {
+  const int grid = static_cast<int>(ntx + nrx);
+  if (grid == 0) return cudaSuccess;
+  const int smem = stages * static_cast<int>(kStreamStageBytes);
+#define RS_STREAM_LAUNCH(S)                                                                                    \
+  do {                                                                                                         \
+    cudaError_t e = cudaFuncSetAttribute(rs_stream_lane_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         smem);                                                                \
+    if (e != cudaSuccess) return e;                                                                            \
+    rs_stream_lane_kernel<S><<<grid, 32, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, epoch, \
+                                                         error_flag, spin_limit, flags, trace, prof);          \
+  } while (0)
+  switch (stages) {
+    case 1: RS_STREAM_LAUNCH(1); break;
+    case 2: RS_STREAM_LAUNCH(2); break;
+    case 3: RS_STREAM_LAUNCH(3); break;
+    case 4: RS_STREAM_LAUNCH(4); break;
+    case 8: RS_STREAM_LAUNCH(8); break;
+    case 10: RS_STREAM_LAUNCH(10); break;
+    case 13: RS_STREAM_LAUNCH(13); break;
+    default: RS_STREAM_LAUNCH(6); break;
+  }
+#undef RS_STREAM_LAUNCH
+  return cudaGetLastError();
+}
+
+int stream_max_blocks_per_sm(int stages) {
+  int n = 0;
+  const int smem = stages * static_cast<int>(kStreamStageBytes);
+#define RS_STREAM_OCC(S)                                                                                         \
+  cudaFuncSetAttribute(rs_stream_lane_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);             \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_stream_lane_kernel<S>, 32, smem)
+  switch (stages) {
+    case 1: RS_STREAM_OCC(1); break;
+    case 2: RS_STREAM_OCC(2); break;
+    case 3: RS_STREAM_OCC(3); break;
+    case 4: RS_STREAM_OCC(4); break;
+    case 8: RS_STREAM_OCC(8); break;
+    case 10: RS_STREAM_OCC(10); break;
+    case 13: RS_STREAM_OCC(13); break;
+    default: RS_STREAM_OCC(6); break;
+  }
+#undef RS_STREAM_OCC
+  return n;
 }
 
 int exchange_max_blocks_per_sm(int which) {

@@ -30,6 +30,15 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
                                const rs_layer_sync* sync,  // NULL or nlayers == 0: fused layers
                                cudaStream_t stream);  // flags: 1 fault-inject, 2 L2 discard, 4 L2 policies
 
+// TMA-pipelined ring lanes (one 1-warp CTA per lane end, `stages` x 16 KB of
+// shared memory); the local copies run as a separate copy launch.
+cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const rs_lane_desc* lanes_rx,
+                                      uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
+                                      uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags,
+                                      int stages, rs_trace_record* trace, unsigned long long* prof,
+                                      cudaStream_t stream);
+int stream_max_blocks_per_sm(int stages);
+
 // which: 0 LDG4, 3 LDG8, 5 LDG16, 6 CTA8, 4 bulk, 1 pattern, 2/7/8 exchange 256/512/1024 threads
 int rs_kernel_max_blocks_per_sm(int which);
 // per-file occupancy helpers behind rs_kernel_max_blocks_per_sm

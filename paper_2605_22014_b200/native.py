@@ -80,7 +80,8 @@ class EngineOptions(C.Structure):
                 ("world_slots", C.c_int32), ("first_local_slot", C.c_int32),
                 ("spin_limit", C.c_int64), ("fault_inject", C.c_int32),
                 ("ring_slot_kib", C.c_int32), ("ring_discard", C.c_int32),
-                ("ring_cta_threads", C.c_int32), ("trace", C.c_int32), ("ring_same_slot", C.c_int32)]
+                ("ring_cta_threads", C.c_int32), ("trace", C.c_int32), ("ring_same_slot", C.c_int32),
+                ("ring_kernel", C.c_int32), ("ring_stages", C.c_int32)]
 
 
 class TraceRecord(C.Structure):

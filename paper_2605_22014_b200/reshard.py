@@ -161,7 +161,7 @@ class Engine:
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
                  spin_limit: int = 0, fault_inject: int = 0, ring_slot_kib: int = 0,
                  ring_discard: int = 0, ring_cta_threads: int = 0, trace: bool = False,
-                 ring_same_slot: int = 0):
+                 ring_same_slot: int = 0, ring_kernel: int = 0, ring_stages: int = 0):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
@@ -169,7 +169,7 @@ class Engine:
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
                             blocks_per_sm, copy_kernel, world_slots, first_local_slot,
                             spin_limit, fault_inject, ring_slot_kib, ring_discard, ring_cta_threads,
-                            int(trace), ring_same_slot)
+                            int(trace), ring_same_slot, ring_kernel, ring_stages)
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h
