@@ -205,13 +205,14 @@ class Engine {
     std::map<int, std::uint64_t> ring_bytes_of;      // dst rank -> bytes of all its rings
     std::map<int, int> k_of;                         // dst rank -> ring depth (K, or 1 for a tiny B)
     std::set<int> direct_dst;                        // dst ranks whose B cannot hold a ring: direct stores
+    bool stream = false;                             // lanes run rs_stream_lane_kernel (stream_lanes_for)
   };
   RingGeometry ring_geometry(const reshard::TransferPlan& plan) const;
   // STAGED: does this cross-rank task go through a ring (else a direct copy)?
   bool ringed(const reshard::TransferTask& t) const;
   int same_slot_policy() const;  // resolved ring_same_slot: 1 rings, 2 direct copies
-  bool stream_lanes_wanted() const;  // STAGED: TMA stream lanes requested / chosen by auto
-  int lane_capacity(int dev) const;  // co-resident lane CTAs of the device's lane kernel
+  bool stream_lanes_for(const reshard::TransferPlan& plan) const;  // STAGED: TMA stream lanes run this plan
+  int lane_capacity(int dev, bool stream) const;  // co-resident lane CTAs of the lane kernel
   int run_stream_lanes(std::size_t dev);  // enqueue the stream-lane launch + local copies; returns launches
   void describe_run(rs_exec_report& rep) const;  // which kernels / policy the run used
   void upload_layer_sync(std::size_t dev);         // STAGED strict layers: barrier state of a device

@@ -81,6 +81,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   const std::int64_t B = opts_.staging_bytes;
   const int K = opts_.slots_per_link;
   RingGeometry geo;
+  geo.stream = stream_lanes_for(plan);
   // inbound links per destination rank (remote tasks only)
   std::map<int, std::set<int>> inbound;
   for (const auto& kv : plan.tasks_by_layer)
@@ -129,9 +130,9 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
     // stream lanes: the local copies run as their own launch beside the lane
     // kernel, so the lanes may take (almost) every co-resident CTA slot
-    double frac = stream_lanes_wanted() ? 0.98 : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
+    double frac = geo.stream ? 0.98 : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
     if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
-    const int capacity = static_cast<int>(lane_capacity(0) * frac);
+    const int capacity = static_cast<int>(lane_capacity(0, geo.stream) * frac);
     int max_lanes = 64;  // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than 32)
     if (const char* env = std::getenv("RS_RING_MAX_LANES")) max_lanes = std::atoi(env);
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
@@ -173,7 +174,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   // default (ring_sweep_v4.jsonl: 15.4 -> 13.1 ms on the C5 slice).
   // stream lanes: 64 KiB slots (4 stage-sized items per batch) keep ~450
   // lanes' rings in L2 (profiles/r2/stream_sweep.jsonl: 128 KiB -> 48 ms, 64 KiB -> 38.7 ms on full C2)
-  const std::uint64_t slot_default = stream_lanes_wanted() ? kRingSlotStreamDefault : kRingSlotDefault;
+  const std::uint64_t slot_default = geo.stream ? kRingSlotStreamDefault : kRingSlotDefault;
   const std::uint64_t slot_cap = opts_.ring_slot_kib < 0    ? ~0ull
                                  : opts_.ring_slot_kib == 0 ? slot_default
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
@@ -481,7 +482,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   }
   std::uint64_t item_div = 32;  // work items per slot (RS_FRAME_ITEMS overrides; diagnostic)
   if (const char* env = std::getenv("RS_FRAME_ITEMS")) item_div = std::max(1, std::atoi(env));
-  const bool stream = stream_lanes_wanted();  // items = one 16 KB shared-memory stage of a stream lane
+  const bool stream = geo.stream;  // items = one 16 KB shared-memory stage of a stream lane
   std::vector<std::vector<rs_copy_desc>> lane_frames(lanes.size());
   std::vector<std::vector<rs_batch_desc>> lane_batches(lanes.size());
   auto build_lane = [&](std::size_t i) {
@@ -578,23 +579,47 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     // 16 B aligned runs of <= one 16 KB stage (the slot-side layout and the
     // flag protocol are the same for both lane kernels, so processes may differ)
     p.stream_lanes = stream && !p.lanes.empty();
-    for (const auto& f : p.frames)
-      if (f.vec_log2 != 4 || f.row_bytes > 16384 || f.rows_per_item * f.row_bytes > 16384) {
-        p.stream_lanes = false;
-        break;
-      }
+    if (p.stream_lanes)
+      for (const auto& f : p.frames)
+        if (f.vec_log2 != 4 || f.row_bytes > 16384 || f.rows_per_item * f.row_bytes > 16384)
+          // the plan was bulk-copy eligible (stream_lanes_for), so only a
+          // caller-bound shard buffer off a 16 B boundary gets here; every
+          // process must run the geometry it computed, so this cannot fall back
+          throw DomainError("staged: stream lanes need 16 B aligned shard buffers (rs_store_bind); "
+                            "use ring_kernel = 1 (classic lanes) for this job");
   }
 }
 
-bool Engine::stream_lanes_wanted() const {
-  if (opts_.mode != RS_MODE_STAGED) return false;
-  if (opts_.ring_kernel == 1) return false;
+// Stream lanes (TMA bulk copies) run a plan when the options allow them and
+// every ringed task is bulk-copyable on both sides: 16 B aligned runs and
+// strides with the engine's 256 B-aligned shard arenas and 16 B-aligned slot
+// offsets.  Decided from the plan and the layouts alone, so every process of
+// a job makes the same choice (the ring geometry depends on it).
+bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
+  if (opts_.mode != RS_MODE_STAGED || opts_.ring_kernel == 1) return false;
   if (opts_.strict_layers || (opts_.ring_discard & 8)) return false;  // barriers / warp-specialised: classic only
+  const Store& src = stores_[RS_SRC];
+  const Store& dst = stores_[RS_DST];
+  const auto& m = src.model;
+  std::vector<rs_copy_desc> scratch;
+  for (const auto& kv : plan.tasks_by_layer)
+    for (const auto& t : kv.second) {
+      if (!ringed(t)) continue;
+      const Entry* se = src.find(t.src_rank, t.tensor_index);
+      const Entry* de = dst.find(t.dst_rank, t.tensor_index);
+      if (!se || !de) continue;  // an integrity failure: reported by compile_staged
+      const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
+      scratch.clear();
+      append_copy(scratch, 0, se->view, 0, t.bounds, t.bounds, eb, 0);  // pack: shard -> packed frame
+      append_copy(scratch, 0, t.bounds, 0, de->view, t.bounds, eb, 0);  // unpack: packed frame -> shard
+      for (const auto& d : scratch)
+        if (d.vec_log2 != 4 || d.row_bytes > 16384) return false;
+    }
   return true;
 }
 
-int Engine::lane_capacity(int dev) const {
-  if (stream_lanes_wanted())
+int Engine::lane_capacity(int dev, bool stream) const {
+  if (stream)
     return devices_[static_cast<std::size_t>(dev)].sms * std::max(1, stream_max_blocks_per_sm(opts_.ring_stages));
   return grid_for(dev, exchange_kernel_id());
 }
@@ -605,7 +630,7 @@ int Engine::lane_capacity(int dev) const {
 int Engine::run_stream_lanes(std::size_t d) {
   DeviceProgram& p = programs_[d];
   Device& dv = devices_[d];
-  const int cap = lane_capacity(static_cast<int>(d));
+  const int cap = lane_capacity(static_cast<int>(d), true);
   if (p.ntx + p.nrx > cap)
     throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) + " stream lanes exceed the co-resident CTA capacity " +
                       std::to_string(cap) + "; lower lanes_per_link");
