@@ -317,13 +317,17 @@ def xfer_one_gpu(args) -> None:
 def kernel_name(mode: str, rep: dict) -> str:
     """The kernel that moved the bytes, from the run's own report."""
     if mode == "staged":
-        return "rs_exchange_kernel"
+        return "rs_stream_lane_kernel" if rep.get("ring_kernel") == 2 else "rs_exchange_kernel"
     if mode == "xfer":
         return "rs_copy_kernel pack/unpack + NCCL"
     return COPY_KERNEL_NAMES.get(rep.get("copy_kernel", -1), f"RS_COPY variant {rep.get('copy_kernel')}")
 
 
 def kernel_label(name: str) -> str:
+    if name == "rs_stream_lane_kernel":
+        return ("rs_stream_lane_kernel: TMA-pipelined ring lanes (one 1-warp CTA per lane end; the sender bulk-copies "
+                "shard rows through shared-memory stages into the receiver's staging ring, the receiver bulk-copies "
+                "them out; bounded staging), local tasks as a TMA copy launch beside it")
     if name == "rs_exchange_kernel":
         return ("rs_exchange_kernel: ring lanes (sender CTA packs into the receiver's staging ring, receiver "
                 "CTA unpacks; bounded staging), spare CTAs copy local tasks")
@@ -375,9 +379,12 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
     destination rank), runs K timed handoffs, and pattern-verifies."""
     from paper_2605_22014_b200 import reshard as R
     from paper_2605_22014_b200.native import RS_COMM, RS_DST, RS_SRC
+    relay = world > 1 and args.relay and not args.strict  # relay chains ride the stream lanes
     eng = R.Engine([device], staging_bytes=args.staging_bytes, mode="staged", lanes_per_link=args.lanes,
                    ring_slot_kib=args.ring_slot_kib, strict_layers=args.strict, world_slots=world,
-                   first_local_slot=rank)
+                   first_local_slot=rank, relay=relay)
+    if relay:  # forwarded DP broadcasts leave from the relaying GPU
+        traffic = R.plan_traffic(plan, co, so, cn, sn, world, relay=True)
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
     for which in (RS_SRC, RS_DST):
@@ -410,7 +417,8 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
            "frac": roof["frac"], "bound": roof["bound"], "roofline_ms": roof["roofline_ms"],
            "peak_staging_bytes": staging, "staging_budget_bytes": args.staging_bytes,
            "within_budget": staging <= args.staging_bytes, "kernel": kernel_name("staged", rep),
-           "ring_same_slot": rep["ring_same_slot"], "gpu_launches": launches, "clocks": clocks,
+           "ring_same_slot": rep["ring_same_slot"], "relay": bool(relay), "relay_routes": rep["relay_routes"],
+           "gpu_launches": launches, "clocks": clocks,
            "wall_s": round(wall, 3), "dst_pattern_mismatches": int(bad)}
     eng.close()
     return out
@@ -446,11 +454,12 @@ def ours(args) -> None:
     slot_of = lambda r: r * world // nranks  # noqa: E731
     so = [slot_of(r) for r in co.ranks]
     sn = [slot_of(r) for r in cn.ranks]
-    traffic = R.plan_traffic(plan, co, so, cn, sn, world)
+    relay = args.mode == "staged" and world > 1 and bool(args.relay) and not args.strict
+    traffic = R.plan_traffic(plan, co, so, cn, sn, world, relay=relay)
 
     eng = R.Engine([device], staging_bytes=args.staging_bytes, mode=args.mode, lanes_per_link=args.lanes,
                    ring_slot_kib=args.ring_slot_kib,
-                   strict_layers=args.strict, world_slots=world, first_local_slot=rank)
+                   strict_layers=args.strict, world_slots=world, first_local_slot=rank, relay=relay)
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
     eng.alloc(RS_SRC)
@@ -539,6 +548,8 @@ def ours(args) -> None:
             "correct": {"dst_pattern_mismatches": int(mismatches), "warmup_check": int(bad_warm)}}
     if args.mode == "staged":
         line["config"]["ring_same_slot"] = rep["ring_same_slot"]
+        line["config"]["relay"] = relay
+        line["config"]["relay_routes"] = rep["relay_routes"]
         line["config"]["peak_staging_bytes"] = rep["peak_staging_bytes"]
 
     run_staged = args.mode == "direct" and not args.no_staged and (
@@ -653,6 +664,7 @@ def main() -> None:
     ap.add_argument("--staging-bytes", type=int, default=1 << 30)
     ap.add_argument("--lanes", type=int, default=0, help="ring lanes per link (0: automatic)")
     ap.add_argument("--strict", type=int, default=0)
+    ap.add_argument("--relay", type=int, default=1, help="STAGED, N>1: relay chains for DP broadcasts (1) or p2p (0)")
     ap.add_argument("--placement", default="iota", choices=["iota", "searched"],
                     help="destination rank list: BASELINE iota, or rs_plan_placement's choice")
     ap.add_argument("--ring-slot-kib", type=int, default=0, help="STAGED ring slot cap (0: default, -1: none)")

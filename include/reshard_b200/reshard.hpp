@@ -23,6 +23,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <iosfwd>
 #include <map>
 #include <optional>
@@ -258,6 +259,20 @@ struct PlacementResult {
 PlacementResult choose_placement(const ParallelConfig& c_old, const ParallelConfig& c_new,
                                  const ModelSpec& model, const std::vector<int>& candidates,
                                  const PlacementOptions& options = {});
+
+// Relay chains for DP broadcasts (extension): tasks of one
+// layer with the same source rank, tensor and bounds but destinations on
+// different slots are served src -> d0 -> d1 -> ... (each destination's ring
+// receiver forwards the drained batches to the next), so the source sends the
+// box once.  Only groups where chaining lowers the highest per-slot egress
+// are returned (greedy, largest first; deterministic).  `tasks` are indices
+// into plan.tasks_by_layer.at(layer) in hop order.
+struct RelayChain {
+  int layer = 0;
+  std::vector<std::size_t> tasks;
+};
+std::vector<RelayChain> relay_chains(const TransferPlan& plan, const std::function<int(int)>& src_slot,
+                                     const std::function<int(int)>& dst_slot);
 
 // ------------------------------------------------------------------ execution
 // The reference's execution surface (proj/include/reshard/executor.hpp:16-53,

@@ -89,7 +89,8 @@ typedef struct {
   int32_t mode;             /* RS_MODE_* */
   int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 2), STAGED */
   int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
-  int32_t strict_layers;    /* 1: one launch per layer (layer barrier), 0: fused; DIRECT only */
+  int32_t strict_layers;    /* 1: layer barriers (DIRECT: one launch per layer; STAGED: classic lanes
+                               meet a device-wide barrier after each layer), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
   int32_t blocks_per_sm;    /* 0: occupancy maximum */
   int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
@@ -115,6 +116,10 @@ typedef struct {
                                (rs_stream_lane_kernel; falls back to classic when ineligible) */
   int32_t ring_stages;      /* stream lanes: 16 KB shared-memory stages per lane end (0: default 2;
                                1, 2, 3, 4, 6, 8, 10 or 13) */
+  int32_t relay;            /* STAGED, multi-slot jobs: 1 = relay chains for DP broadcasts (a box
+                               several destination GPUs need from one source leaves the source once;
+                               each destination's ring receiver forwards it to the next,
+                               reshard::relay_chains); needs stream lanes.  0 = point to point */
 } rs_engine_options;
 
 #define RS_COPY_AUTO 0     /* engine default: RS_COPY_TMA_NP when every descriptor is 16 B aligned with
@@ -153,6 +158,9 @@ typedef struct {
    * cross-rank tasks whose ranks share a GPU (1 rings, 2 direct, 0 n/a). */
   int32_t copy_kernel;
   int32_t ring_same_slot;
+  int32_t ring_kernel;        /* STAGED lane kernel of device 0: 1 classic (rs_exchange_kernel),
+                                 2 TMA stream lanes (rs_stream_lane_kernel), 0 n/a */
+  int32_t relay_routes;       /* STAGED relay: distinct (source, destination chain) routes forwarded */
 } rs_exec_report;
 
 const char* rs_last_error(void);
@@ -218,6 +226,13 @@ int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handl
  * of remote task bytes, local task bytes, carryover bytes, out[4*slot + k]. */
 int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old,
                     const rs_config* c_new, const int32_t* slot_new, int32_t nslots, int64_t* out);
+/* Same with flags: RS_TRAFFIC_RELAY counts each relay-chained task (DP
+ * broadcast forwarding, rs_engine_options.relay) as egress of the slot that
+ * forwards it (reshard::relay_chains), i.e. the traffic a relay run moves. */
+#define RS_TRAFFIC_RELAY 1
+int rs_plan_traffic_ex(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old,
+                       const rs_config* c_new, const int32_t* slot_new, int32_t nslots, int32_t flags,
+                       int64_t* out);
 
 /* Placement-aware destination rank ordering (extension):
  * fills ranks_out[c_new->num_ranks] with the rank list for c_new's shape,

@@ -416,21 +416,36 @@ int rs_arena_import(rs_engine* e, int32_t which, int32_t slot, const void* handl
   });
 }
 
-int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old, const rs_config* c_new,
-                    const int32_t* slot_new, int32_t nslots, int64_t* out) {
+int rs_plan_traffic_ex(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old, const rs_config* c_new,
+                       const int32_t* slot_new, int32_t nslots, int32_t flags, int64_t* out) {
   return guarded([&] {
     if (!plan || !out || nslots < 1) throw std::invalid_argument("bad argument");
+    if (flags & ~RS_TRAFFIC_RELAY) throw std::invalid_argument("plan traffic: unknown flags");
     const int L = plan->model.num_layers;
     const auto co = to_config(c_old, L), cn = to_config(c_new, L);
     auto slot_in = [&](const reshard::ParallelConfig& c, const int32_t* slots, int rank) {
       const int s = slots ? slots[c.index_of(rank)] : c.index_of(rank);
       if (s < 0 || s >= nslots) throw std::invalid_argument("slot out of range");
-      return static_cast<std::size_t>(s);
+      return s;
     };
+    auto src_slot = [&](int r) { return slot_in(co, slot_old, r); };
+    auto dst_slot = [&](int r) { return slot_in(cn, slot_new, r); };
+    // relay chains (extension): hop k of a chain leaves from the previous
+    // destination's slot instead of the source's
+    std::map<std::pair<int, std::size_t>, int> sender_slot;  // (layer, task index) -> slot it leaves from
+    if (flags & RS_TRAFFIC_RELAY)
+      for (const auto& ch : reshard::relay_chains(plan->plan, src_slot, dst_slot)) {
+        const auto& tasks = plan->plan.tasks_by_layer.at(ch.layer);
+        for (std::size_t k = 1; k < ch.tasks.size(); ++k)
+          sender_slot[{ch.layer, ch.tasks[k]}] = dst_slot(tasks[ch.tasks[k - 1]].dst_rank);
+      }
     std::fill(out, out + 4 * nslots, 0);
-    for (const auto& kv : plan->plan.tasks_by_layer)
-      for (const auto& t : kv.second) {
-        const std::size_t s = slot_in(co, slot_old, t.src_rank), d = slot_in(cn, slot_new, t.dst_rank);
+    for (const auto& [layer, tasks] : plan->plan.tasks_by_layer)
+      for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const auto& t = tasks[i];
+        const auto d = static_cast<std::size_t>(dst_slot(t.dst_rank));
+        auto it = sender_slot.find({layer, i});
+        const auto s = static_cast<std::size_t>(it == sender_slot.end() ? src_slot(t.src_rank) : it->second);
         if (t.is_local() || s == d) {
           out[4 * d + 2] += t.byte_size;  // moved inside one GPU
         } else {
@@ -439,8 +454,13 @@ int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* 
         }
       }
     for (const auto& kv : plan->plan.carryover_by_layer)
-      for (const auto& k : kv.second) out[4 * slot_in(cn, slot_new, k.rank) + 3] += k.byte_size;
+      for (const auto& k : kv.second) out[4 * static_cast<std::size_t>(dst_slot(k.rank)) + 3] += k.byte_size;
   });
+}
+
+int rs_plan_traffic(const rs_plan* plan, const rs_config* c_old, const int32_t* slot_old, const rs_config* c_new,
+                    const int32_t* slot_new, int32_t nslots, int64_t* out) {
+  return rs_plan_traffic_ex(plan, c_old, slot_old, c_new, slot_new, nslots, 0, out);
 }
 
 int rs_plan_placement(const char* model_spec, const rs_config* c_old, const rs_config* c_new,

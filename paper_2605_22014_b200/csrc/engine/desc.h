@@ -66,6 +66,14 @@ typedef struct {
   uint32_t nbatches;
   uint32_t batch0;          // index of the lane's first batch in the batch table
   uint32_t flags;           // RS_LANE_PEER: sender and receiver are not one device of one process
+  // Relay (receiver lanes of a relay chain's hop k < n-1, stream lanes only):
+  // every drained batch is also stored into the next hop's ring at the same
+  // slot offsets, published there, and credited back by the next receiver.
+  uint64_t fwd_slot_base;     // next hop's slot 0 as mapped here (0: this lane does not forward)
+  uint64_t fwd_ready_flags;   // next hop's ready flags (next receiver's memory, as mapped here)
+  uint64_t fwd_credit_flags;  // next hop's credit flags (this slot's memory)
+  uint32_t fwd_flags;         // RS_LANE_PEER: the next hop crosses slots
+  uint32_t fwd_pad;
 } rs_lane_desc;
 
 #define RS_LANE_PEER 1u       // flags / fences at .sys scope (else .gpu)

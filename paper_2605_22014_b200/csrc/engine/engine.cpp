@@ -934,6 +934,10 @@ void Engine::describe_run(rs_exec_report& rep) const {
   if (opts_.mode == RS_MODE_DIRECT && !devices_.empty() && !programs_.empty())
     rep.copy_kernel = opts_.copy_kernel == RS_COPY_CE ? RS_COPY_CE : copy_variant(0);
   rep.ring_same_slot = opts_.mode == RS_MODE_STAGED ? same_slot_policy() : 0;
+  rep.ring_kernel = 0;
+  if (opts_.mode == RS_MODE_STAGED && !programs_.empty())
+    rep.ring_kernel = programs_[0].stream_lanes ? 2 : (programs_[0].ntx + programs_[0].nrx ? 1 : 0);
+  rep.relay_routes = relay_routes_;
 }
 
 // ------------------------------------------------------------ live handoff

@@ -10,6 +10,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -198,8 +199,16 @@ class Engine {
   void copy_runs(const Store& s, const std::vector<std::size_t>& idx, void* const* host, bool to_device);
   void compile_direct(const reshard::TransferPlan& plan);
   void compile_staged(const reshard::TransferPlan& plan);
+  // A ring link: (source rank, first destination rank, relay route or -1).
+  // Route r's lanes carry src -> chain[0] and are forwarded hop by hop.
+  using LaneKey = std::tuple<int, int, int>;
   struct RingGeometry {
-    std::map<std::pair<int, int>, int> lanes_of;     // (src rank, dst rank) -> lanes
+    std::map<LaneKey, int> lanes_of;                 // link -> lanes
+    // relay chains (rs_engine_options.relay): (layer, task index) -> (route, hop)
+    std::map<std::pair<int, std::size_t>, std::pair<int, int>> relay_of;
+    std::vector<std::vector<int>> route_chain;       // route -> destination ranks in hop order
+    std::vector<std::uint64_t> route_slot_bytes;     // route -> ring slot bytes on every hop
+    std::vector<int> route_k;                        // route -> ring depth on every hop
     std::map<int, std::uint64_t> inbound_lanes;      // dst rank -> lanes into it
     std::map<int, std::uint64_t> slot_bytes_of;      // dst rank -> ring slot bytes
     std::map<int, std::uint64_t> ring_bytes_of;      // dst rank -> bytes of all its rings
@@ -258,6 +267,7 @@ class Engine {
   rs_exec_report planned_{};  // compile-time report fields (reference semantics)
   std::int64_t planned_total_bytes_ = 0;
   std::vector<int> plan_layers_;
+  int relay_routes_ = 0;  // STAGED relay routes of the compiled plan
 };
 
 }  // namespace rsb

@@ -82,11 +82,65 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   const int K = opts_.slots_per_link;
   RingGeometry geo;
   geo.stream = stream_lanes_for(plan);
-  // inbound links per destination rank (remote tasks only)
-  std::map<int, std::set<int>> inbound;
-  for (const auto& kv : plan.tasks_by_layer)
-    for (const auto& t : kv.second)
-      if (ringed(t)) inbound[t.dst_rank].insert(t.src_rank);
+  std::map<int, int> src_slot, dst_slot;  // rank -> slot
+  for (const auto& e : src.entries) src_slot.emplace(e.rank, e.slot);
+  for (const auto& e : dst.entries) dst_slot.emplace(e.rank, e.slot);
+  auto slot_in = [](const std::map<int, int>& m, int rank) {
+    auto it = m.find(rank);
+    return it == m.end() ? -1 : it->second;
+  };
+
+  // Relay chains for DP broadcasts (reshard::relay_chains): route = distinct
+  // (source rank, destination chain); hop 0 of a chain rides the route's
+  // lanes, later hops are forwarded by the previous hop's receivers.
+  std::map<std::pair<int, std::vector<int>>, int> route_id;
+  if (opts_.relay && nslots_ > 1) {
+    if (!geo.stream)
+      throw DomainError("relay: needs stream lanes (16 B aligned plans, ring_kernel != 1, strict_layers off)");
+    const auto chains = reshard::relay_chains(
+        plan, [&](int r) { return slot_in(src_slot, r); }, [&](int r) { return slot_in(dst_slot, r); });
+    for (const auto& ch : chains) {
+      const auto& tasks = plan.tasks_by_layer.at(ch.layer);
+      std::vector<int> ranks;
+      for (std::size_t i : ch.tasks) ranks.push_back(tasks[i].dst_rank);
+      const auto key = std::make_pair(tasks[ch.tasks[0]].src_rank, ranks);
+      auto it = route_id.find(key);
+      if (it == route_id.end()) {
+        it = route_id.emplace(key, static_cast<int>(geo.route_chain.size())).first;
+        geo.route_chain.push_back(ranks);
+      }
+      for (std::size_t k = 0; k < ch.tasks.size(); ++k)
+        geo.relay_of[{ch.layer, ch.tasks[k]}] = {it->second, static_cast<int>(k)};
+    }
+  }
+
+  // ring links: bytes, the sender's slot, the receivers' ranks and slots
+  struct Link {
+    std::uint64_t bytes = 0;
+    int tx_slot = 0;
+    std::vector<int> rx_ranks;
+  };
+  std::map<LaneKey, Link> links;
+  for (const auto& [layer, tasks] : plan.tasks_by_layer)
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+      const auto& t = tasks[i];
+      if (!ringed(t)) continue;
+      LaneKey key{t.src_rank, t.dst_rank, -1};
+      if (auto it = geo.relay_of.find({layer, i}); it != geo.relay_of.end()) {
+        if (it->second.second > 0) continue;  // a forwarded hop: the route's lanes carry it
+        key = LaneKey{t.src_rank, t.dst_rank, it->second.first};
+      }
+      Link& lk = links[key];
+      if (lk.rx_ranks.empty()) {
+        lk.tx_slot = slot_in(src_slot, t.src_rank);
+        lk.rx_ranks = std::get<2>(key) < 0 ? std::vector<int>{t.dst_rank}
+                                           : geo.route_chain[static_cast<std::size_t>(std::get<2>(key))];
+      }
+      lk.bytes += static_cast<std::uint64_t>(t.byte_size);
+    }
+  std::map<int, std::set<LaneKey>> inbound;  // dst rank -> links with a receiver there
+  for (const auto& [key, lk] : links)
+    for (int r : lk.rx_ranks) inbound[r].insert(key);
 
   // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
   // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
@@ -94,29 +148,19 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   // Automatic choice: lanes proportional to each link's bytes (a link's
   // lanes finish together, so the launch ends when the heaviest link does),
   // scaled so every slot's sender + receiver lanes fit a share of one
-  // device's CTA capacity (below), at least one and at most 32 per link (same
-  // answer on every process: the plan and the placement are global).
-  std::map<std::pair<int, int>, std::uint64_t> link_bytes;
-  for (const auto& kv : plan.tasks_by_layer)
-    for (const auto& t : kv.second)
-      if (ringed(t)) link_bytes[{t.src_rank, t.dst_rank}] += static_cast<std::uint64_t>(t.byte_size);
+  // device's CTA capacity (below), at least one and at most 64 per link (same
+  // answer on every process: the plan and the placement are global).  A
+  // relay route's lanes have a receiver (forwarder) CTA on every hop.
   auto& lanes_of = geo.lanes_of;
   if (opts_.lanes_per_link > 0) {
-    for (const auto& kv : link_bytes) lanes_of[kv.first] = opts_.lanes_per_link;
-  } else if (!link_bytes.empty()) {
-    auto slot_of = [&](const Store& s, int rank) {
-      for (const auto& e : s.entries)
-        if (e.rank == rank) return e.slot;
-      return 0;
-    };
-    std::map<int, int> src_slot, dst_slot;
+    for (const auto& kv : links) lanes_of[kv.first] = opts_.lanes_per_link;
+  } else if (!links.empty()) {
     std::vector<std::uint64_t> slot_bytes(static_cast<std::size_t>(nslots_), 0);
-    for (const auto& [lk, b] : link_bytes) {
-      if (!src_slot.count(lk.first)) src_slot[lk.first] = slot_of(src, lk.first);
-      if (!dst_slot.count(lk.second)) dst_slot[lk.second] = slot_of(dst, lk.second);
-      slot_bytes[static_cast<std::size_t>(src_slot[lk.first])] += b;
-      slot_bytes[static_cast<std::size_t>(dst_slot[lk.second])] += b;
-    }
+    auto touches = [&](const Link& lk, auto&& fn) {  // every CTA-hosting slot of a link, once per CTA
+      fn(lk.tx_slot);
+      for (int r : lk.rx_ranks) fn(slot_in(dst_slot, r));
+    };
+    for (const auto& [key, lk] : links) touches(lk, [&](int sl) { slot_bytes[static_cast<std::size_t>(sl)] += lk.bytes; });
     // Share of the co-resident CTAs given to ring lanes; the rest run the
     // local copies (local tasks + carryovers) in the same launch.  Balanced so
     // both finish together: a lane pair (2 CTAs) streams ~10 GB/s of payload,
@@ -138,27 +182,28 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
     const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
     std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
-    for (const auto& [lk, b] : link_bytes) {
-      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(b)), 1, max_lanes);
-      lanes_of[lk] = n;
-      slot_lanes[static_cast<std::size_t>(src_slot[lk.first])] += n;
-      slot_lanes[static_cast<std::size_t>(dst_slot[lk.second])] += n;
+    for (const auto& [key, lk] : links) {
+      const int n = std::clamp(static_cast<int>(scale * static_cast<double>(lk.bytes)), 1, max_lanes);
+      lanes_of[key] = n;
+      touches(lk, [&](int sl) { slot_lanes[static_cast<std::size_t>(sl)] += n; });
     }
     // the max(1, .) floor can overshoot a slot with many light links: trim
     // the widest links touching it
     for (int sl = 0; sl < nslots_; ++sl)
       while (slot_lanes[static_cast<std::size_t>(sl)] > capacity) {
-        std::pair<int, int> widest{-1, -1};
+        const LaneKey* widest = nullptr;
         int w = 1;
-        for (const auto& [lk, n] : lanes_of)
-          if ((src_slot[lk.first] == sl || dst_slot[lk.second] == sl) && n > w) {
-            w = n;
-            widest = lk;
+        for (const auto& [key, lk] : links) {
+          bool hit = false;
+          touches(lk, [&](int x) { hit = hit || x == sl; });
+          if (hit && lanes_of[key] > w) {
+            w = lanes_of[key];
+            widest = &key;
           }
-        if (widest.first < 0) break;  // every link at one lane: the launch check reports it
-        --lanes_of[widest];
-        --slot_lanes[static_cast<std::size_t>(src_slot[widest.first])];
-        --slot_lanes[static_cast<std::size_t>(dst_slot[widest.second])];
+        }
+        if (!widest) break;  // every link at one lane: the launch check reports it
+        --lanes_of[*widest];
+        touches(links.at(*widest), [&](int x) { --slot_lanes[static_cast<std::size_t>(x)]; });
       }
   }
   // Ring slot size per dst rank: B split over its inbound lanes, capped at
@@ -179,18 +224,19 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
                                  : opts_.ring_slot_kib == 0 ? slot_default
                                                             : static_cast<std::uint64_t>(opts_.ring_slot_kib) << 10;
   auto& inbound_lanes = geo.inbound_lanes;
-  for (const auto& [lk, n] : lanes_of) inbound_lanes[lk.second] += static_cast<std::uint64_t>(n);
+  for (const auto& [key, lk] : links)
+    for (int r : lk.rx_ranks) inbound_lanes[r] += static_cast<std::uint64_t>(lanes_of.at(key));
   // largest element a destination rank receives over rings
   std::map<int, std::uint64_t> need_eb;
-  for (const auto& kv : plan.tasks_by_layer)
-    for (const auto& t : kv.second)
+  for (const auto& [layer, tasks] : plan.tasks_by_layer)
+    for (const auto& t : tasks)
       if (ringed(t)) {
         const auto& m = src.model;
         auto& e = need_eb[t.dst_rank];
         e = std::max<std::uint64_t>(e, static_cast<std::uint64_t>(m.element_bytes(m.tensors[t.tensor_index])));
       }
   auto& slot_bytes_of = geo.slot_bytes_of;
-  for (const auto& [d, srcs] : inbound) {
+  for (const auto& [d, keys] : inbound) {
     // A tiny budget cannot host K slots on every lane into d: fall back to one
     // lane per link, then to K = 1 (strictly alternating pack / unpack), so
     // the ring path accepts every B the reference's executor accepts (a
@@ -198,9 +244,13 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     int k = K;
     const std::uint64_t need = std::max<std::uint64_t>(need_eb[d], 16);
     auto slot_for = [&]() { return static_cast<std::uint64_t>(B) / (inbound_lanes.at(d) * static_cast<std::uint64_t>(k)); };
+    const bool relayed = std::any_of(keys.begin(), keys.end(), [](const LaneKey& x) { return std::get<2>(x) >= 0; });
     if (slot_for() < need) {
-      for (auto& [lk, n] : lanes_of)
-        if (lk.second == d && n > 1) {
+      if (relayed)  // one lane per link would change the route's lanes on every hop
+        throw DomainError("relay: staging budget " + std::to_string(B) + " B is too small for the relay rings into dst rank " +
+                          std::to_string(d) + "; disable relay");
+      for (const auto& key : keys)
+        if (int& n = lanes_of.at(key); n > 1) {
           inbound_lanes[d] -= static_cast<std::uint64_t>(n - 1);
           n = 1;
         }
@@ -216,9 +266,11 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       // The reference executor still succeeds (it needs B >= one element,
       // executor.cpp:183-206), so this destination receives its bytes by
       // direct stores into its shards -- zero staging, the budget holds.
+      if (relayed)
+        throw DomainError("relay: staging budget " + std::to_string(B) + " B cannot hold a relay ring into dst rank " +
+                          std::to_string(d) + "; disable relay");
       geo.direct_dst.insert(d);
-      for (auto it = lanes_of.begin(); it != lanes_of.end();)
-        it = it->first.second == d ? lanes_of.erase(it) : std::next(it);
+      for (const auto& key : keys) lanes_of.erase(key);
       inbound_lanes[d] = 0;
       slot_bytes_of[d] = 0;
       geo.ring_bytes_of[d] = 0;
@@ -226,6 +278,18 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     }
     slot_bytes_of[d] = sb;
     geo.ring_bytes_of[d] = slot_bytes_of[d] * inbound_lanes.at(d) * static_cast<std::uint64_t>(k);
+  }
+  // a route's rings are alike on every hop (the forwarder stores each batch at
+  // the same slot offsets): the smallest slot and depth of its destinations
+  for (const auto& chain : geo.route_chain) {
+    std::uint64_t sb = ~0ull;
+    int k = K;
+    for (int r : chain) {
+      sb = std::min(sb, slot_bytes_of.at(r));
+      k = std::min(k, geo.k_of.at(r));
+    }
+    geo.route_slot_bytes.push_back(sb);
+    geo.route_k.push_back(k);
   }
 
   return geo;
@@ -263,6 +327,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   const int K = opts_.slots_per_link;
 
   const RingGeometry geo = ring_geometry(plan);
+  relay_routes_ = static_cast<int>(geo.route_chain.size());
   const auto& lanes_of = geo.lanes_of;
   const auto& slot_bytes_of = geo.slot_bytes_of;
   const auto& inbound_lanes = geo.inbound_lanes;
@@ -289,9 +354,12 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     int k;  // ring depth of this lane (geo.k_of: K, or 1 for a tiny budget)
     std::vector<std::vector<Frame>> batches;
     std::uint64_t fill = 0;
+    int route = -1;   // relay route (hop 0 lanes carry it from the source)
+    int hop = 0;      // relay hop: > 0 = fed by the previous hop's receiver (no sender CTA)
+    int next = -1;    // lane of the next hop (this lane's receiver forwards into it)
   };
   std::vector<LaneBuild> lanes;
-  std::map<std::pair<int, int>, int> link_first_lane, link_cursor;
+  std::map<LaneKey, int> link_first_lane, link_cursor;
 
   std::vector<std::size_t> mark(devices_.size());
   std::map<int, std::uint32_t> layer_idx;
@@ -331,7 +399,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
         }
       }
       if (auto it = plan.tasks_by_layer.find(layer); it != plan.tasks_by_layer.end()) {
-        for (const auto& t : it->second) {
+        for (std::size_t ti = 0; ti < it->second.size(); ++ti) {
+          const auto& t = it->second[ti];
           const Entry* se = src.find(t.src_rank, t.tensor_index);
           if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
           if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
@@ -352,18 +421,32 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
             delta.bytes_moved += t.bounds.element_count() * eb;
             continue;
           }
-          const std::uint64_t sb = slot_bytes_of.at(t.dst_rank);
+          // relay chains: hop 0 rides its route's lanes, later hops are
+          // forwarded from the previous destination's ring (no frames here)
+          int route = -1;
+          if (auto r = geo.relay_of.find({layer, ti}); r != geo.relay_of.end()) {
+            if (r->second.second > 0) {
+              delta.bytes_moved += t.bounds.element_count() * eb;
+              continue;
+            }
+            route = r->second.first;
+          }
+          const std::uint64_t sb = route < 0 ? slot_bytes_of.at(t.dst_rank)
+                                             : geo.route_slot_bytes[static_cast<std::size_t>(route)];
           if (static_cast<std::uint64_t>(eb) > sb)
             throw IntegrityError("staging: ring slot of " + std::to_string(sb) + " bytes cannot hold one element (B=" +
                                  std::to_string(B) + " over " + std::to_string(inbound_lanes.at(t.dst_rank)) +
                                  " inbound links)");
           const auto chunks = reshard::chunk_bounds(t.bounds, static_cast<std::int64_t>(sb), eb);
-          const auto lk = std::make_pair(t.src_rank, t.dst_rank);
+          const LaneKey lk{t.src_rank, t.dst_rank, route};
           const int P = lanes_of.at(lk);
           if (!link_first_lane.count(lk)) {
             link_first_lane[lk] = static_cast<int>(lanes.size());
-            for (int p = 0; p < P; ++p)
-              lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, geo.k_of.at(t.dst_rank), {}, 0});
+            const int k = route < 0 ? geo.k_of.at(t.dst_rank) : geo.route_k[static_cast<std::size_t>(route)];
+            for (int p = 0; p < P; ++p) {
+              lanes.push_back({t.src_rank, t.dst_rank, se->slot, de->slot, sb, k, {}, 0});
+              lanes.back().route = route;
+            }
           }
           for (const auto& c : chunks) {
             int& cur = link_cursor[lk];
@@ -405,6 +488,38 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       programs_[d].layers.push_back({layer, mark[d], programs_[d].local.size()});
   }
   if (planned_.failed_layer < 0) planned_.ok = 1;
+
+  // Relay hops: a route lane's batches continue along the chain.  Hop h is a
+  // copy of the route lane with the same batches and frame offsets whose
+  // receiver unpacks into chain[h]'s shards; hop h-1's receiver is its sender.
+  for (std::size_t i = 0, n0 = lanes.size(); i < n0; ++i) {
+    if (lanes[i].route < 0) continue;
+    const auto& chain = geo.route_chain[static_cast<std::size_t>(lanes[i].route)];
+    std::size_t prev = i;
+    for (std::size_t h = 1; h < chain.size(); ++h) {
+      LaneBuild hb = lanes[prev];
+      hb.src_rank = chain[h - 1];
+      hb.dst_rank = chain[h];
+      hb.sslot = lanes[prev].dslot;
+      hb.hop = static_cast<int>(h);
+      hb.next = -1;
+      for (auto& batch : hb.batches)
+        for (auto& f : batch) {
+          f.de = dst.find(chain[h], f.se->ti);
+          if (!f.de || !f.de->view.contains(f.region))  // the plan's own task for this hop was checked above
+            throw IntegrityError("relay: dst rank " + std::to_string(chain[h]) + " has no buffer for a forwarded box");
+        }
+      hb.dslot = -1;
+      for (const auto& e : dst.entries)
+        if (e.rank == chain[h]) {
+          hb.dslot = e.slot;
+          break;
+        }
+      lanes[prev].next = static_cast<int>(lanes.size());
+      prev = lanes.size();
+      lanes.push_back(std::move(hb));
+    }
+  }
 
   // Ring memory inside the comm arenas (deterministic on every process):
   // a destination rank's lanes take consecutive K-slot rings in its B region;
@@ -464,6 +579,9 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     if ((tx_local[i] || rx_local[i]) && (!ring || !ready || !credit))
       throw DomainError("staged: comm arena of slot " + std::to_string(tx_local[i] ? lb.dslot : lb.sslot) +
                         " not mapped in this process (rs_arena_import RS_COMM)");
+    if (rx_local[i] && lb.next >= 0 && !comm_base(lanes[static_cast<std::size_t>(lb.next)].dslot))
+      throw DomainError("staged: comm arena of slot " + std::to_string(lanes[static_cast<std::size_t>(lb.next)].dslot) +
+                        " not mapped in this process (relay forwarding; rs_arena_import RS_COMM)");
     rs_lane_desc& L = all_lanes[i];
     L = rs_lane_desc{};
     const std::uint64_t ring_addr = ring ? addr(ring) + where[i].ring_off : 0;
@@ -479,7 +597,17 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     L.batch0 = static_cast<std::uint32_t>(nbatch_total);
     L.nbatches = static_cast<std::uint32_t>(lb.batches.size());
     nbatch_total += lb.batches.size();
+    if (lb.next >= 0 && rx_local[i]) {  // relay forwarder: the next hop's ring, as mapped here
+      const auto j = static_cast<std::size_t>(lb.next);
+      L.fwd_slot_base = addr(comm_base(lanes[j].dslot)) + where[j].ring_off;
+      L.fwd_ready_flags = addr(flag_base(lanes[j].dslot)) + where[j].ready_off;
+      L.fwd_credit_flags = addr(flag_base(lanes[j].sslot)) + where[j].credit_off;
+      L.fwd_flags = lanes[j].sslot == lanes[j].dslot ? 0u : RS_LANE_PEER;
+    }
   }
+  // hop lanes have no sender CTA: their receiver's predecessor forwards
+  for (std::size_t i = 0; i < lanes.size(); ++i)
+    if (lanes[i].hop > 0) tx_local[i] = 0;
   std::uint64_t item_div = 32;  // work items per slot (RS_FRAME_ITEMS overrides; diagnostic)
   if (const char* env = std::getenv("RS_FRAME_ITEMS")) item_div = std::max(1, std::atoi(env));
   const bool stream = geo.stream;  // items = one 16 KB shared-memory stage of a stream lane
@@ -570,7 +698,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     }
     p.lanes.clear();
     for (std::size_t i = 0; i < lanes.size(); ++i)
-      if (lanes[i].sslot == slot) p.lanes.push_back(all_lanes[i]);
+      if (lanes[i].sslot == slot && lanes[i].hop == 0) p.lanes.push_back(all_lanes[i]);
     p.ntx = static_cast<int>(p.lanes.size());
     for (std::size_t i = 0; i < lanes.size(); ++i)
       if (lanes[i].dslot == slot) p.lanes.push_back(all_lanes[i]);

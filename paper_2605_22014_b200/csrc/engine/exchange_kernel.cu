@@ -548,10 +548,33 @@ __device__ __forceinline__ void stream_item_load(const rs_copy_desc& D, bool con
   }
 }
 
+// fwd: relay forwarder (a receiver whose batches continue to the next hop's
+// ring): the item's slot-side bytes -- already in `stage` -- are also stored
+// at the same offsets of the next ring (slot address + fwd_delta), in the same
+// bulk group, so stage reuse and the batch's publish cover both stores.
 __device__ __forceinline__ void stream_item_store(const rs_copy_desc& D, bool contiguous, uint64_t k,
-                                                  const unsigned char* stage, uint64_t pol, int lane) {
+                                                  const unsigned char* stage, uint64_t pol, int lane,
+                                                  bool fwd = false, bool src_contig = false, int64_t fwd_delta = 0,
+                                                  uint64_t fwd_pol = 0) {
   const uint64_t r0 = k * D.rows_per_item;
   const uint64_t r1 = min(r0 + D.rows_per_item, D.rows);
+  if (fwd) {
+    if (src_contig) {
+      if (lane == 0) {
+        int64_t so, dof;
+        row_offsets(D, static_cast<uint32_t>(r0), so, dof);
+        bulk_store_hint(reinterpret_cast<void*>(D.src + so + fwd_delta), stage,
+                        static_cast<uint32_t>((r1 - r0) * D.row_bytes), fwd_pol);
+      }
+    } else {
+      for (uint64_t r = r0 + lane; r < r1; r += 32) {
+        int64_t so, dof;
+        row_offsets(D, static_cast<uint32_t>(r), so, dof);
+        bulk_store_hint(reinterpret_cast<void*>(D.src + so + fwd_delta), stage + (r - r0) * D.row_bytes,
+                        static_cast<uint32_t>(D.row_bytes), fwd_pol);
+      }
+    }
+  }
   if (contiguous) {
     if (lane == 0) {
       int64_t so, dof;
@@ -613,6 +636,9 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
   const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
   const bool peer = (L.flags & RS_LANE_PEER) != 0;
+  const bool fwd = !sender && L.fwd_slot_base != 0;  // relay forwarder
+  const bool fpeer = (L.fwd_flags & RS_LANE_PEER) != 0;
+  const int64_t fwd_delta = static_cast<int64_t>(L.fwd_slot_base - L.slot_base_rx);
   if (lane == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -631,21 +657,24 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   uint32_t credit_b = 0xffffffffu;   // sender: batch whose slot credit was acquired last
   uint64_t idle = 0;
   // register stores: 64 both roles, 128 receivers only, 256 senders only
-  const bool reg_store = (flags & kExStreamRegStore) || ((flags & 128) && !sender) || ((flags & 256) && sender);
+  const bool reg_store =
+      !fwd && ((flags & kExStreamRegStore) || ((flags & 128) && !sender) || ((flags & 256) && sender));
   uint64_t prof_reuse = 0, prof_store = 0, prof_pub = 0, prof_idle = 0, prof_items = 0;
   const uint64_t prof_t0 = clock64();
   __shared__ uint64_t t_open[kStages];  // trace: flag-acquire time of each open batch (<= kStages open)
   __shared__ uint64_t t_issue[kStages];  // diagnostic: load issue time per stage
   uint64_t prof_land = 0, prof_loadloop = 0;
 
-  auto flag_up = [&](uint32_t b) -> bool {  // lane 0 polls, the warp agrees
+  // sender: slot credit of its ring; forwarder (store side): slot credit of
+  // the next hop's ring; receiver (load side): ready flag of its ring
+  auto flag_up = [&](uint32_t b, bool credit) -> bool {  // lane 0 polls, the warp agrees
     int up = 0;
     if (lane == 0) {
-      if (sender) {
-        up = b < L.slots ||
-             (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + b % L.slots)
-                   : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.credit_flags_tx) + b % L.slots)) >=
-                 epoch + b - L.slots + 1;
+      if (credit) {
+        const bool p = sender ? peer : fpeer;
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(sender ? L.credit_flags_tx : L.fwd_credit_flags) +
+                            b % L.slots;
+        up = b < L.slots || (p ? ld_acquire_sys(f) : ld_acquire_gpu(f)) >= epoch + b - L.slots + 1;
       } else {
         up = (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)
                    : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)) >=
@@ -661,7 +690,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     const uint64_t tl0 = prof ? clock64() : 0;
     while (ld.b < L.nbatches && g_ld - g_st < static_cast<uint64_t>(kStages)) {
       if (!sender && ld.first_of_batch && ready_b != ld.b) {
-        if (!flag_up(ld.b)) break;
+        if (!flag_up(ld.b, false)) break;
         ready_b = ld.b;
         if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[ld.b % kStages]));
         fence_proxy_async_global();  // the slot bytes were published through the generic proxy
@@ -694,17 +723,18 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
       if (!__shfl_sync(0xffffffffu, landed, 0)) break;
       mbar_wait(&bar[s], parity);
       if (prof && lane == 0) prof_land += clock64() - t_issue[s];
-      if (sender && st.first_of_batch && credit_b != st.b) {
-        if (!flag_up(st.b)) break;  // the receiver has not drained this slot yet
+      if ((sender || fwd) && st.first_of_batch && credit_b != st.b) {
+        if (!flag_up(st.b, true)) break;  // the (next) receiver has not drained this slot yet
         credit_b = st.b;
-        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[st.b % kStages]));
+        if (sender && trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[st.b % kStages]));
       }
       const uint32_t b = st.b;
       const uint64_t ts0 = prof ? clock64() : 0;
       if (reg_store)
         stream_item_store_regs(st.D, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane);
       else
-        stream_item_store(st.D, st.dst_contig, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane);
+        stream_item_store(st.D, st.dst_contig, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane,
+                          fwd, st.src_contig, fwd_delta, pol_last);
       if (prof && lane == 0) prof_store += clock64() - ts0;
       const bool last = cursor_next(st, L, batches, frames, sender);
       ++g_st;
@@ -723,6 +753,12 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
         if (prof && lane == 0) prof_pub += clock64() - tw0;
         if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
       } else {
+        if (fwd) {  // relay: the batch's bytes are in the next hop's slot -> publish it there
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __syncwarp();
+          if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.fwd_ready_flags) + slot, epoch + b + 1, fpeer);
+        }
         // every slot byte of batch b is in shared memory: drop the slot's
         // lines from L2 and hand the slot back (the shard stores still run)
         if ((flags & kExDiscard) && B.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {

@@ -17,6 +17,7 @@ RS_OK, RS_EDOMAIN, RS_EINTEGRITY, RS_ESYSTEM = 0, 1, 2, 3
 RS_SRC, RS_DST, RS_COMM = 0, 1, 2
 RS_IPC_HANDLE_BYTES = 64
 RS_MODE_DIRECT, RS_MODE_STAGED, RS_MODE_XFER = 0, 1, 2
+RS_TRAFFIC_RELAY = 1
 
 EXPORTS = [
     "rs_last_error", "rs_version", "rs_validate_config", "rs_view", "rs_plan_compute",
@@ -26,7 +27,7 @@ EXPORTS = [
     "rs_store_read",
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
-    "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_xfer_info", "rs_xfer_link",
+    "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_plan_traffic_ex", "rs_xfer_info", "rs_xfer_link",
     "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan", "rs_trace_read",
 ]
 
@@ -81,7 +82,7 @@ class EngineOptions(C.Structure):
                 ("spin_limit", C.c_int64), ("fault_inject", C.c_int32),
                 ("ring_slot_kib", C.c_int32), ("ring_discard", C.c_int32),
                 ("ring_cta_threads", C.c_int32), ("trace", C.c_int32), ("ring_same_slot", C.c_int32),
-                ("ring_kernel", C.c_int32), ("ring_stages", C.c_int32)]
+                ("ring_kernel", C.c_int32), ("ring_stages", C.c_int32), ("relay", C.c_int32)]
 
 
 class TraceRecord(C.Structure):
@@ -109,7 +110,8 @@ class ExecReport(C.Structure):
                 ("local_copy_bytes", C.c_int64), ("carryover_bytes", C.c_int64),
                 ("layers_processed", C.c_int32), ("kernel_launches", C.c_int32),
                 ("device_ms", C.c_double), ("host_ms", C.c_double), ("error", C.c_char * 512),
-                ("copy_kernel", C.c_int32), ("ring_same_slot", C.c_int32)]
+                ("copy_kernel", C.c_int32), ("ring_same_slot", C.c_int32),
+                ("ring_kernel", C.c_int32), ("relay_routes", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {"ok": bool(self.ok),
@@ -122,7 +124,8 @@ class ExecReport(C.Structure):
                 "kernel_launches": int(self.kernel_launches),
                 "device_ms": float(self.device_ms), "host_ms": float(self.host_ms),
                 "error": self.error.decode(),
-                "copy_kernel": int(self.copy_kernel), "ring_same_slot": int(self.ring_same_slot)}
+                "copy_kernel": int(self.copy_kernel), "ring_same_slot": int(self.ring_same_slot),
+                "ring_kernel": int(self.ring_kernel), "relay_routes": int(self.relay_routes)}
 
 
 class SwitchStats(C.Structure):
@@ -187,6 +190,7 @@ def lib() -> C.CDLL:
         L.rs_arena_export.argtypes = [VP, I32, I32, VP, P(I64)]
         L.rs_arena_import.argtypes = [VP, I32, I32, VP, I64]
         L.rs_plan_traffic.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, P(I64)]
+        L.rs_plan_traffic_ex.argtypes = [VP, P(Config), P(I32), P(Config), P(I32), I32, I32, P(I64)]
         L.rs_xfer_info.argtypes = [VP, P(I32), P(I32), P(I32)]
         L.rs_xfer_link.argtypes = [VP, I32, I32, P(I32), P(I32), P(I32), P(VP), P(I64), P(I64)]
         L.rs_xfer_step.argtypes = [VP, I32, I32]

@@ -161,7 +161,8 @@ class Engine:
                  copy_kernel: int = 0, world_slots: int = 0, first_local_slot: int = 0,
                  spin_limit: int = 0, fault_inject: int = 0, ring_slot_kib: int = 0,
                  ring_discard: int = 0, ring_cta_threads: int = 0, trace: bool = False,
-                 ring_same_slot: int = 0, ring_kernel: int = 0, ring_stages: int = 0):
+                 ring_same_slot: int = 0, ring_kernel: int = 0, ring_stages: int = 0,
+                 relay: bool = False):
         devs = list(devices)
         self._devs = (C.c_int32 * len(devs))(*devs)
         modes = {"direct": N.RS_MODE_DIRECT, "staged": N.RS_MODE_STAGED, "xfer": N.RS_MODE_XFER}
@@ -169,7 +170,7 @@ class Engine:
                             slots_per_link, lanes_per_link, int(strict_layers), item_bytes,
                             blocks_per_sm, copy_kernel, world_slots, first_local_slot,
                             spin_limit, fault_inject, ring_slot_kib, ring_discard, ring_cta_threads,
-                            int(trace), ring_same_slot, ring_kernel, ring_stages)
+                            int(trace), ring_same_slot, ring_kernel, ring_stages, int(relay))
         h = C.c_void_p()
         N.check(N.lib().rs_engine_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -356,14 +357,16 @@ class Engine:
 
 
 def plan_traffic(plan: TransferPlan, c_old: ParallelConfig, slot_old: Sequence[int],
-                 c_new: ParallelConfig, slot_new: Sequence[int], nslots: int):
-    """Per-slot [egress, ingress, intra-GPU task bytes, carryover bytes]."""
+                 c_new: ParallelConfig, slot_new: Sequence[int], nslots: int, relay: bool = False):
+    """Per-slot [egress, ingress, intra-GPU task bytes, carryover bytes].
+    relay=True: relay-chained DP broadcasts leave from the forwarding slot
+    (the traffic an Engine(relay=True) STAGED run moves)."""
     out = (C.c_int64 * (4 * nslots))()
     so = (C.c_int32 * len(slot_old))(*slot_old)
     sn = (C.c_int32 * len(slot_new))(*slot_new)
     L = plan.model.num_layers
-    N.check(N.lib().rs_plan_traffic(plan.handle, N.config_struct(c_old, L), so, N.config_struct(c_new, L),
-                                    sn, nslots, out))
+    N.check(N.lib().rs_plan_traffic_ex(plan.handle, N.config_struct(c_old, L), so, N.config_struct(c_new, L),
+                                       sn, nslots, N.RS_TRAFFIC_RELAY if relay else 0, out))
     return [list(out[4 * s:4 * s + 4]) for s in range(nslots)]
 
 

@@ -81,6 +81,63 @@ def ipc_reshard(rank, world, mode):
             "launches": rep["kernel_launches"]}
 
 
+def relay_reshard(rank, world):
+    """GPU: STAGED with relay chains for DP broadcasts across `world`
+    processes on one GPU.  The case comes from RS_RELAY_CASE (JSON: spec
+    group bytes, layers, old / new (tp, pp, dp), new-rank slots).  Returns the
+    SHA-256 of every destination shard this process holds (the test combines
+    them into the reference's digest order) and the traffic the run implies."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    from paper_2605_22014_b200 import reshard as R, specs
+    from paper_2605_22014_b200.dist import connect
+    from paper_2605_22014_b200.native import RS_DST, RS_SRC
+    case = json.loads(os.environ["RS_RELAY_CASE"])
+    dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    sp = specs.group_spec(specs.llama("llama-mini-a16", case["layers"]), case["bpe"])
+    co, cn = specs.iota_config(1, *case["old"]), specs.iota_config(2, *case["new"])
+    so = [r % world for r in co.ranks] if "slot_old" not in case else case["slot_old"]
+    sn = case["slot_new"]
+    eng = R.Engine([dev], staging_bytes=case.get("staging", 1 << 20), mode="staged", lanes_per_link=case.get("lanes", 1),
+                   world_slots=world, first_local_slot=rank, relay=case.get("relay", True))
+    eng.layout(RS_SRC, sp, co, so)
+    eng.layout(RS_DST, sp, cn, sn)
+    eng.alloc(RS_SRC)
+    eng.alloc(RS_DST)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    eng.comm_alloc(plan)
+    eng.fill_pattern(RS_SRC, 42)
+    eng.fill_pattern(RS_DST, 7)
+    connect(eng)
+    dist.barrier()
+    eng.prepare(plan)
+    dist.barrier()
+    rep = eng.run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    bad = eng.verify_pattern(RS_DST, 42)[0]
+    digests = {}
+    for ti, r, n in eng.entries(RS_DST):
+        if sn[cn.ranks.index(r)] == rank:
+            digests[f"{ti}:{r}"] = hashlib.sha256(eng.read(RS_DST, r, ti).tobytes()).hexdigest()
+    eng.fill_pattern(RS_DST, 9)
+    dist.barrier()
+    rep2 = eng.run()  # a second handoff over the same rings (epochs advance)
+    torch.cuda.synchronize()
+    dist.barrier()
+    bad2 = eng.verify_pattern(RS_DST, 42)[0]
+    dist.barrier()
+    eng.close()
+    return {"ok": rep["ok"] and rep2["ok"], "mismatches": bad + bad2, "error": rep["error"] or rep2["error"],
+            "digests": digests, "bytes_moved": rep["bytes_moved"], "launches": rep["kernel_launches"],
+            "relay_routes": rep["relay_routes"], "ring_kernel": rep["ring_kernel"],
+            "traffic": R.plan_traffic(plan, co, so, cn, sn, world, relay=True),
+            "traffic_p2p": R.plan_traffic(plan, co, so, cn, sn, world)}
+
+
 def xfer_reshard(rank, world):
     """GPU: the NCCL-style comparator transport across processes; with gloo
     (CPU test plumbing) the link buffers are staged through host memory."""
@@ -153,6 +210,8 @@ def main():
             res = plan_partition(rank, world)
         elif case == "xfer":
             res = xfer_reshard(rank, world)
+        elif case == "relay":
+            res = relay_reshard(rank, world)
         elif case.startswith("handoff-"):
             res = handoff_chain(rank, world, case.split("-", 1)[1])
         else:
