@@ -28,6 +28,7 @@ typedef struct {
   uint32_t nouter;
   uint32_t vec_log2;      // access width: 1 << vec_log2 bytes (0..4)
   uint32_t tag;           // layer (diagnostics)
+  uint64_t reserved;      // pads the descriptor to 160 B: tables stay bulk-copyable (16 B granules)
 } rs_copy_desc;
 
 // Synthetic-state descriptor: one shard buffer (row-major over its view),
@@ -73,6 +74,10 @@ typedef struct {
   uint64_t fwd_ready_flags;   // next hop's ready flags (next receiver's memory, as mapped here)
   uint64_t fwd_credit_flags;  // next hop's credit flags (this slot's memory)
   uint32_t fwd_flags;         // RS_LANE_PEER: the next hop crosses slots
+  // The lane's frames per role, contiguous in batch order (stream lanes
+  // stage them into shared memory with bulk copies)
+  uint32_t tx_frame0, tx_nframes;  // pack frames
+  uint32_t rx_frame0, rx_nframes;  // unpack frames
   uint32_t fwd_pad;
 } rs_lane_desc;
 

@@ -613,12 +613,18 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
   const bool stream = geo.stream;  // items = one 16 KB shared-memory stage of a stream lane
   std::vector<std::vector<rs_copy_desc>> lane_frames(lanes.size());
   std::vector<std::vector<rs_batch_desc>> lane_batches(lanes.size());
+  std::vector<std::uint32_t> lane_npack(lanes.size(), 0);
+  // A lane's frames are laid out per role: every pack frame in batch order,
+  // then every unpack frame in batch order, so a lane end walks one
+  // contiguous frame sequence across batch boundaries (the stream lanes
+  // prefetch the next descriptor while the current one moves).
   auto build_lane = [&](std::size_t i) {
     const auto& lb = lanes[i];
     const std::uint64_t ring_addr = all_lanes[i].slot_base;
     auto& frames = lane_frames[i];
     auto& batches = lane_batches[i];
     batches.reserve(lb.batches.size());
+    std::vector<rs_copy_desc> unpack;
     // work items inside a batch: ~32 per slot so all 8 warps of the lane's
     // CTA share even a small (L2-resident) slot
     const std::uint64_t frame_item =
@@ -640,15 +646,19 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       Bd.layer_idx = lb.batches[b].empty() ? 0u : layer_idx.at(lb.batches[b].front().layer);
       Bd.npack = static_cast<std::uint32_t>(frames.size()) - Bd.pack0;
       Bd.pack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.pack0, 0, frame_item));
-      Bd.unpack0 = static_cast<std::uint32_t>(frames.size());
+      Bd.unpack0 = static_cast<std::uint32_t>(unpack.size());  // rebased below
       if (rx_local[i])
         for (const auto& f : lb.batches[b])
-          append_copy(frames, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
+          append_copy(unpack, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
                       f.eb, static_cast<std::uint32_t>(f.layer));
-      Bd.nunpack = static_cast<std::uint32_t>(frames.size()) - Bd.unpack0;
-      Bd.unpack_items = static_cast<std::uint32_t>(assign_items(frames, Bd.unpack0, 0, frame_item));
+      Bd.nunpack = static_cast<std::uint32_t>(unpack.size()) - Bd.unpack0;
+      Bd.unpack_items = static_cast<std::uint32_t>(assign_items(unpack, Bd.unpack0, 0, frame_item));
       batches.push_back(Bd);
     }
+    const auto npack = static_cast<std::uint32_t>(frames.size());
+    for (auto& Bd : batches) Bd.unpack0 += npack;
+    frames.insert(frames.end(), unpack.begin(), unpack.end());
+    lane_npack[i] = npack;
   };
   const unsigned nthreads = std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   if (nthreads <= 1 || lanes.size() < 8) {
@@ -677,6 +687,10 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     batches.reserve(nbatch_total);
     for (std::size_t i = 0; i < lanes.size(); ++i) {
       const auto off = static_cast<std::uint32_t>(frames.size());
+      all_lanes[i].tx_frame0 = off;
+      all_lanes[i].tx_nframes = lane_npack[i];
+      all_lanes[i].rx_frame0 = off + lane_npack[i];
+      all_lanes[i].rx_nframes = static_cast<std::uint32_t>(lane_frames[i].size()) - lane_npack[i];
       for (auto Bd : lane_batches[i]) {
         Bd.pack0 += off;
         Bd.unpack0 += off;
@@ -746,9 +760,13 @@ bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
   return true;
 }
 
+bool Engine::stream_ws() const { return opts_.ring_kernel == 3; }
+
 int Engine::lane_capacity(int dev, bool stream) const {
   if (stream)
-    return devices_[static_cast<std::size_t>(dev)].sms * std::max(1, stream_max_blocks_per_sm(opts_.ring_stages));
+    return devices_[static_cast<std::size_t>(dev)].sms *
+           std::max(1, stream_ws() ? stream_ws_max_blocks_per_sm(opts_.ring_stages)
+                                   : stream_max_blocks_per_sm(opts_.ring_stages));
   return grid_for(dev, exchange_kernel_id());
 }
 
@@ -785,14 +803,35 @@ int Engine::run_stream_lanes(std::size_t d) {
                                          reinterpret_cast<const rs_copy_desc*>(p.d_frames.data()), epoch_,
                                          reinterpret_cast<unsigned int*>(p.d_error.data()),
                                          opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit) : kSpinLimit,
-                                         (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | stream_flags,
+                                         (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | stream_flags |
+                                             (stream_ws() ? 512 : 0),
                                          opts_.ring_stages,
                                          opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
                                          prof.size() ? reinterpret_cast<unsigned long long*>(prof.data()) : nullptr,
                                          dv.stream),
                "stream lane kernel launch");
     ++launches;
-    if (prof.size()) {  // diagnostic summary on stderr: mean cycles per phase, senders / receivers
+    if (prof.size() && stream_ws()) {  // diagnostic: per role and warp, mean cycles and idle polls
+      std::vector<unsigned long long> h(prof.size() / 8);
+      cuda_check(cudaMemcpyAsync(h.data(), prof.data(), prof.size(), cudaMemcpyDeviceToHost, dv.stream), "prof");
+      cuda_check(cudaStreamSynchronize(dv.stream), "prof");
+      double acc[2][2][2] = {};
+      int n[2] = {0, 0};
+      for (std::size_t i = 0; i < h.size() / 8; ++i) {
+        const int role = h[8 * i + 2] ? 0 : 1;
+        ++n[role];
+        for (int w = 0; w < 2; ++w) {
+          acc[role][w][0] += static_cast<double>(h[8 * i + 4 * w]);
+          acc[role][w][1] += static_cast<double>(h[8 * i + 4 * w + 1]);
+        }
+      }
+      for (int role = 0; role < 2; ++role)
+        if (n[role])
+          std::fprintf(stderr, "[stream ws prof] %s lanes=%d load warp: cycles=%.0f idle_polls=%.0f  store warp: "
+                       "cycles=%.0f idle_polls=%.0f (mean per lane)\n", role ? "rx" : "tx", n[role],
+                       acc[role][0][0] / n[role], acc[role][0][1] / n[role], acc[role][1][0] / n[role],
+                       acc[role][1][1] / n[role]);
+    } else if (prof.size()) {  // diagnostic summary on stderr: mean cycles per phase, senders / receivers
       std::vector<unsigned long long> h(prof.size() / 8);
       cuda_check(cudaMemcpyAsync(h.data(), prof.data(), prof.size(), cudaMemcpyDeviceToHost, dv.stream), "prof");
       cuda_check(cudaStreamSynchronize(dv.stream), "prof");

@@ -47,6 +47,31 @@ __device__ __forceinline__ void publish(uint64_t* flag, uint64_t v, bool peer) {
   }
 }
 
+// Stream lanes: one release store, no separate fence.  The lane's writes
+// are ordered before it by __syncwarp (the warp's other lanes) and, for bulk
+// copies, by cp.async.bulk.wait_group + fence.proxy.async; st.release is
+// cumulative over what the publishing lane has observed.  (__threadfence
+// before it costs a second MEMBAR + L1 invalidate per batch: profiles/r2.)
+__device__ __forceinline__ void publish_release(uint64_t* flag, uint64_t v, bool peer) {
+  if (peer) st_release_sys(flag, v);
+  else st_release_gpu(flag, v);
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p, bool peer) {
+  uint64_t v;
+  if (peer) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Poll a ring flag: relaxed loads while it is short of `want` (no L1
+// invalidate per poll), one acquire load of the same flag once it is there
+// (synchronises with the publisher's release).
+__device__ __forceinline__ bool flag_reached(const uint64_t* p, uint64_t want, bool peer) {
+  if (ld_relaxed(p, peer) < want) return false;
+  return (peer ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= want;
+}
+
 // Spin with a bounded budget; on expiry raise the error flag (no hangs on a
 // protocol bug: the host reports failed_layer instead).
 __device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
@@ -473,55 +498,132 @@ __device__ __forceinline__ bool side_contiguous(const rs_copy_desc& D, bool src_
   return contiguous;
 }
 
-// Walks a lane's work items in order: batch b, its frames [f, fend), item k
-// of nk.  The current frame's descriptor is held by value (registers): one
-// broadcast load per frame instead of a global re-read per field per item
-// (the bulk-copy asm clobbers memory, so a reference would be re-loaded).
+// A lane end's descriptors, staged into shared memory by bulk copies.  The
+// frames of one role are contiguous in batch order (compile_staged), and so
+// are the lane's batch descriptors: both are read through small rings of
+// chunks (kNB buffers, one mbarrier each) that the load cursor fills one chunk
+// ahead.  The descriptor tables are far larger than L2; demand-fetching them
+// with generic loads stalled the warp at every frame / batch boundary and
+// kept loads outstanding under every release fence (profiles/r2).
+template <int kStages>
+struct DescRing {
+  static constexpr uint32_t kNB = 3;                             // buffers per table
+  static constexpr uint32_t kCF = kStages > 6 ? kStages : 6;     // frames per chunk (>= the cursors' lag)
+  static constexpr uint32_t kCB = kStages > 8 ? kStages : 8;     // batch descriptors per chunk
+  rs_copy_desc* fbuf;   // kNB x kCF
+  rs_batch_desc* bbuf;  // kNB x kCB
+  uint64_t* fbar;       // kNB
+  uint64_t* bbar;       // kNB
+  const rs_copy_desc* frames;
+  const rs_batch_desc* batches;
+  uint32_t f0, nf;  // this role's frames in the global table
+  uint32_t b0, nb;  // the lane's batches
+
+  __device__ __forceinline__ void load_frames(uint32_t j, int lane) const {
+    if (j * kCF >= nf || lane != 0) return;
+    const uint32_t n = min(kCF, nf - j * kCF);
+    const uint32_t buf = j % kNB;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+    mbar_expect_tx(&fbar[buf], n * static_cast<uint32_t>(sizeof(rs_copy_desc)));
+    bulk_load(fbuf + buf * kCF, frames + f0 + j * kCF, n * static_cast<uint32_t>(sizeof(rs_copy_desc)), &fbar[buf]);
+  }
+  __device__ __forceinline__ void load_batches(uint32_t j, int lane) const {
+    if (j * kCB >= nb || lane != 0) return;
+    const uint32_t n = min(kCB, nb - j * kCB);
+    const uint32_t buf = j % kNB;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bbar[buf], n * static_cast<uint32_t>(sizeof(rs_batch_desc)));
+    bulk_load(bbuf + buf * kCB, batches + b0 + j * kCB, n * static_cast<uint32_t>(sizeof(rs_batch_desc)), &bbar[buf]);
+  }
+  __device__ __forceinline__ void wait_frames(uint32_t j) const { mbar_wait(&fbar[j % kNB], (j / kNB) & 1); }
+  __device__ __forceinline__ void wait_batches(uint32_t j) const { mbar_wait(&bbar[j % kNB], (j / kNB) & 1); }
+  __device__ __forceinline__ const rs_copy_desc& frame(uint32_t i) const {  // i: role-relative frame
+    return fbuf[((i / kCF) % kNB) * kCF + i % kCF];
+  }
+  __device__ __forceinline__ const rs_batch_desc& batch(uint32_t b) const {  // b: lane-relative batch
+    return bbuf[((b / kCB) % kNB) * kCB + b % kCB];
+  }
+};
+
+// Walks a lane end's work items in order: batch b, frame i (role-relative),
+// item k of nk.  The leading (load) cursor waits for descriptor chunks and
+// issues the next ones; the store cursor trails it by <= kStages items and
+// reads chunks the leader has already waited for.
 struct ItemCursor {
-  uint32_t b = 0, f = 0, fend = 0;
+  uint32_t b = 0;     // batch of the item at the cursor (lane-relative)
+  uint32_t i = 0;     // frame of the item at the cursor (role-relative)
+  uint32_t left = 0;  // frames of batch b after i
   uint64_t k = 0, nk = 0;
+  uint64_t extent = 0;  // slot bytes in use by batch b
   bool first_of_batch = true;  // the item at the cursor opens batch b
   bool src_contig = false, dst_contig = false;
   rs_copy_desc D;
 };
 
-__device__ __forceinline__ void cursor_load_frame(ItemCursor& c, const rs_copy_desc* frames) {
-  c.D = frames[c.f];
+__device__ __forceinline__ uint32_t role_frames(const rs_batch_desc& B, bool sender) {
+  return sender ? B.npack : B.nunpack;
+}
+
+template <int kStages>
+__device__ __forceinline__ void cursor_install(ItemCursor& c, const DescRing<kStages>& R) {
+  c.D = R.frame(c.i);
   c.nk = (c.D.rows + c.D.rows_per_item - 1) / c.D.rows_per_item;
   c.src_contig = side_contiguous(c.D, true);
   c.dst_contig = side_contiguous(c.D, false);
 }
 
-// position the cursor on the first item of batch b (or past the end)
-__device__ __forceinline__ void cursor_open(ItemCursor& c, const rs_lane_desc& L, const rs_batch_desc* batches,
-                                            const rs_copy_desc* frames, bool sender, uint32_t b) {
-  c.b = b;
+// position the cursor on the lane's first item (the leader also primes the rings)
+template <int kStages>
+__device__ __forceinline__ void cursor_start(ItemCursor& c, const DescRing<kStages>& R, bool sender, bool leader,
+                                             int lane) {
+  c.b = 0;
+  c.i = 0;
   c.k = 0;
   c.first_of_batch = true;
-  while (c.b < L.nbatches) {
-    const rs_batch_desc& B = batches[L.batch0 + c.b];
-    c.f = sender ? B.pack0 : B.unpack0;
-    c.fend = c.f + (sender ? B.npack : B.nunpack);
-    if (c.f < c.fend) {
-      cursor_load_frame(c, frames);
-      return;
-    }
-    ++c.b;  // (an empty batch still needs its flag: never emitted by compile_staged)
+  if (R.nb == 0) return;
+  if (leader) {
+    R.load_batches(0, lane);
+    R.load_batches(1, lane);
+    R.load_frames(0, lane);
+    R.load_frames(1, lane);
   }
+  R.wait_batches(0);  // (a trailing warp observes the chunk's completion itself)
+  R.wait_frames(0);
+  const rs_batch_desc& B0 = R.batch(0);
+  c.left = role_frames(B0, sender) - 1;  // (an empty batch is never emitted by compile_staged)
+  c.extent = B0.extent;
+  cursor_install(c, R);
 }
 
 // advance one item; returns true when the item just passed was its batch's last
-__device__ __forceinline__ bool cursor_next(ItemCursor& c, const rs_lane_desc& L, const rs_batch_desc* batches,
-                                            const rs_copy_desc* frames, bool sender) {
+template <int kStages>
+__device__ __forceinline__ bool cursor_next(ItemCursor& c, const DescRing<kStages>& R, bool sender, bool leader,
+                                            int lane) {
+  using DR = DescRing<kStages>;
   c.first_of_batch = false;
   if (++c.k < c.nk) return false;
   c.k = 0;
-  if (++c.f < c.fend) {
-    cursor_load_frame(c, frames);
-    return false;
+  const bool batch_end = c.left == 0;
+  if (batch_end) {
+    if (++c.b >= R.nb) return true;
+    if (c.b % DR::kCB == 0) {  // entering batch chunk j: wait for it (the leader then fetches j + 1)
+      R.wait_batches(c.b / DR::kCB);
+      if (leader) R.load_batches(c.b / DR::kCB + 1, lane);
+    }
+    const rs_batch_desc& B = R.batch(c.b);
+    c.left = role_frames(B, sender) - 1;
+    c.extent = B.extent;
+    c.first_of_batch = true;
+  } else {
+    --c.left;
   }
-  cursor_open(c, L, batches, frames, sender, c.b + 1);
-  return true;
+  ++c.i;
+  if (c.i % DR::kCF == 0) {
+    R.wait_frames(c.i / DR::kCF);
+    if (leader) R.load_frames(c.i / DR::kCF + 1, lane);
+  }
+  cursor_install(c, R);
+  return batch_end;
 }
 
 // Issue the loads of item (D, k) into `stage` (lanes split the rows; the
@@ -630,6 +732,10 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) unsigned char stages[];
   __shared__ __align__(8) uint64_t bar[kStages];
+  using DR = DescRing<kStages>;
+  __shared__ __align__(128) rs_copy_desc desc_frames[DR::kNB * DR::kCF];
+  __shared__ __align__(128) rs_batch_desc desc_batches[DR::kNB * DR::kCB];
+  __shared__ __align__(8) uint64_t desc_bar[2 * DR::kNB];
   const int lane = threadIdx.x;
   const bool sender = blockIdx.x < ntx;
   if (blockIdx.x >= ntx + nrx) return;
@@ -640,6 +746,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   const bool fpeer = (L.fwd_flags & RS_LANE_PEER) != 0;
   const int64_t fwd_delta = static_cast<int64_t>(L.fwd_slot_base - L.slot_base_rx);
   if (lane == 0) {
+    for (int i = 0; i < 2 * static_cast<int>(DR::kNB); ++i) mbar_init(&desc_bar[i], 1);
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -649,9 +756,11 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   // evict-first (it is discarded next), shard out evict-first
   const uint64_t ld_pol = pol_first, st_pol = sender ? pol_last : pol_first;
 
+  const DR ring{desc_frames, desc_batches, desc_bar, desc_bar + DR::kNB, frames, batches,
+                sender ? L.tx_frame0 : L.rx_frame0, sender ? L.tx_nframes : L.rx_nframes, L.batch0, L.nbatches};
   ItemCursor ld, st;
-  cursor_open(ld, L, batches, frames, sender, 0);
-  cursor_open(st, L, batches, frames, sender, 0);
+  cursor_start(ld, ring, sender, true, lane);
+  cursor_start(st, ring, sender, false, lane);
   uint64_t g_ld = 0, g_st = 0;       // items loaded (issued) / stored (issued)
   uint32_t ready_b = 0xffffffffu;    // receiver: batch whose ready flag was acquired last
   uint32_t credit_b = 0xffffffffu;   // sender: batch whose slot credit was acquired last
@@ -671,14 +780,11 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     int up = 0;
     if (lane == 0) {
       if (credit) {
-        const bool p = sender ? peer : fpeer;
         const uint64_t* f = reinterpret_cast<const uint64_t*>(sender ? L.credit_flags_tx : L.fwd_credit_flags) +
                             b % L.slots;
-        up = b < L.slots || (p ? ld_acquire_sys(f) : ld_acquire_gpu(f)) >= epoch + b - L.slots + 1;
+        up = b < L.slots || flag_reached(f, epoch + b - L.slots + 1, sender ? peer : fpeer);
       } else {
-        up = (peer ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)
-                   : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots)) >=
-             epoch + b + 1;
+        up = flag_reached(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + b % L.slots, epoch + b + 1, peer);
       }
     }
     return __shfl_sync(0xffffffffu, up, 0) != 0;
@@ -708,7 +814,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
       __syncwarp();
       stream_item_load(ld.D, ld.src_contig, ld.k, stages + static_cast<size_t>(s) * kStreamStageBytes, &bar[s], ld_pol,
                        lane);
-      cursor_next(ld, L, batches, frames, sender);
+      cursor_next(ld, ring, sender, true, lane);
       ++g_ld;
       progress = true;
     }
@@ -729,6 +835,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
         if (sender && trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[st.b % kStages]));
       }
       const uint32_t b = st.b;
+      const uint64_t extent = st.extent;
       const uint64_t ts0 = prof ? clock64() : 0;
       if (reg_store)
         stream_item_store_regs(st.D, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane);
@@ -736,11 +843,10 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
         stream_item_store(st.D, st.dst_contig, st.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane,
                           fwd, st.src_contig, fwd_delta, pol_last);
       if (prof && lane == 0) prof_store += clock64() - ts0;
-      const bool last = cursor_next(st, L, batches, frames, sender);
+      const bool last = cursor_next(st, ring, sender, false, lane);
       ++g_st;
       progress = true;
       if (!last) continue;
-      const rs_batch_desc& B = batches[L.batch0 + b];
       const uint32_t slot = b % L.slots;
       if (sender) {
         // the batch's slot writes complete, then one release publishes them
@@ -751,25 +857,25 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
         }
         __syncwarp();
         if (prof && lane == 0) prof_pub += clock64() - tw0;
-        if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
+        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
       } else {
         if (fwd) {  // relay: the batch's bytes are in the next hop's slot -> publish it there
           bulk_wait_all();
           fence_proxy_async_global();
           __syncwarp();
-          if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.fwd_ready_flags) + slot, epoch + b + 1, fpeer);
+          if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.fwd_ready_flags) + slot, epoch + b + 1, fpeer);
         }
         // every slot byte of batch b is in shared memory: drop the slot's
         // lines from L2 and hand the slot back (the shard stores still run)
-        if ((flags & kExDiscard) && B.extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
+        if ((flags & kExDiscard) && extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
           const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(slot) * L.slot_bytes;
-          const uint64_t lines = (B.extent + 127) >> 7;
+          const uint64_t lines = (extent + 127) >> 7;
           for (uint64_t i = lane; i < lines; i += 32) discard_l2_line(base + (i << 7));
         }
         __syncwarp();
-        if (lane == 0) publish(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
+        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
       }
-      if (trace && lane == 0) record_batch(trace, L, B, b, sender ? 0 : 1, t_open[b % kStages]);
+      if (trace && lane == 0) record_batch(trace, L, batches[L.batch0 + b], b, sender ? 0 : 1, t_open[b % kStages]);
     }
     if (progress) {
       idle = 0;
@@ -802,6 +908,203 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     p[7] = prof_land;
     p[1] = prof_reuse | (prof_loadloop << 32);  // (packed: reuse wait low, load loop high; both < 2^32 per slice run)
     (void)prof_items;
+  }
+}
+
+
+// ------------------------------------------------------- warp-specialised stream lanes
+//
+// Same ring protocol and shared-memory stages as rs_stream_lane_kernel, with
+// the lane end split over two warps (64 threads): a load warp (descriptor
+// chunks, the receiver's ready-flag acquire, bulk loads into free stages) and
+// a store warp (bulk stores out of landed stages, the sender's credit
+// acquire, batch publishes / credits).  Stages pass between them through
+// full / empty mbarriers.  In the one-warp lane every latency -- a release
+// fence at each batch end, a flag poll, a descriptor chunk -- stalled both
+// directions of the pipeline (profiles/r2 ncu source pages); here a store-side
+// fence no longer holds back the next loads and vice versa.
+constexpr int kExStreamWS = 512;
+
+// bounded mbarrier wait of a whole warp (lane 0 polls, the warp agrees, every
+// lane then observes the phase); false = the job aborted
+__device__ __forceinline__ bool warp_mbar_wait(uint64_t* bar, uint32_t parity, unsigned int* error_flag,
+                                               uint64_t spin_limit, int lane, uint64_t& idle) {
+  uint64_t spins = 0;
+  while (true) {
+    int st = 0;  // 1 landed, 2 abort
+    if (lane == 0) {
+      if (mbar_test(bar, parity)) st = 1;
+      else if (*reinterpret_cast<volatile unsigned int*>(error_flag)) st = 2;
+      else if (++spins > spin_limit) {
+        atomicExch(error_flag, 1u);
+        st = 2;
+      } else {
+        __nanosleep(20);
+      }
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    if (st == 1) break;
+    if (st == 2) return false;
+    ++idle;
+  }
+  mbar_wait(bar, parity);
+  return true;
+}
+
+// bounded ring-flag wait of a whole warp (relaxed polls, one acquire)
+__device__ __forceinline__ bool warp_flag_wait(const uint64_t* flag, uint64_t want, bool peer,
+                                               unsigned int* error_flag, uint64_t spin_limit, int lane,
+                                               uint64_t& idle) {
+  uint64_t spins = 0;
+  while (true) {
+    int st = 0;
+    if (lane == 0) {
+      if (flag_reached(flag, want, peer)) st = 1;
+      else if (*reinterpret_cast<volatile unsigned int*>(error_flag)) st = 2;
+      else if (++spins > spin_limit) {
+        atomicExch(error_flag, 1u);
+        st = 2;
+      } else {
+        __nanosleep(32);
+      }
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    if (st == 1) return true;
+    if (st == 2) return false;
+    ++idle;
+  }
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(64, 6) rs_stream_ws_kernel(
+    const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
+    uint32_t nrx, const rs_batch_desc* __restrict__ batches, const rs_copy_desc* __restrict__ frames,
+    uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace,
+    unsigned long long* __restrict__ prof) {
+  extern __shared__ __align__(128) unsigned char stages[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  using DR = DescRing<kStages>;
+  __shared__ __align__(128) rs_copy_desc desc_frames[DR::kNB * DR::kCF];
+  __shared__ __align__(128) rs_batch_desc desc_batches[DR::kNB * DR::kCB];
+  __shared__ __align__(8) uint64_t desc_bar[2 * DR::kNB];
+  __shared__ uint64_t t_open[kStages];  // trace: the receiver's ready-flag acquire time per open batch
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool sender = blockIdx.x < ntx;
+  if (blockIdx.x >= ntx + nrx) return;
+  if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
+  const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
+  const bool peer = (L.flags & RS_LANE_PEER) != 0;
+  const bool fwd = !sender && L.fwd_slot_base != 0;  // relay forwarder
+  const bool fpeer = (L.fwd_flags & RS_LANE_PEER) != 0;
+  const int64_t fwd_delta = static_cast<int64_t>(L.fwd_slot_base - L.slot_base_rx);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * static_cast<int>(DR::kNB); ++i) mbar_init(&desc_bar[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const DR ring{desc_frames, desc_batches, desc_bar, desc_bar + DR::kNB, frames, batches,
+                sender ? L.tx_frame0 : L.rx_frame0, sender ? L.tx_nframes : L.rx_nframes, L.batch0, L.nbatches};
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  uint64_t idle = 0;
+  const uint64_t t0 = clock64();
+  ItemCursor c;
+  cursor_start(c, ring, sender, warp == 0, lane);
+
+  if (warp == 0) {
+    // ---------------- load warp: stages in item order, up to kStages ahead of the store warp
+    uint64_t item = 0;
+    uint32_t ready_b = 0xffffffffu;
+    while (c.b < L.nbatches) {
+      const uint32_t s = static_cast<uint32_t>(item % kStages);
+      if (item >= static_cast<uint64_t>(kStages) &&
+          !warp_mbar_wait(&empty[s], static_cast<uint32_t>((item / kStages - 1) & 1), error_flag, spin_limit, lane,
+                          idle))
+        return;
+      if (!sender && c.first_of_batch && ready_b != c.b) {
+        if (!warp_flag_wait(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + c.b % L.slots, epoch + c.b + 1, peer,
+                            error_flag, spin_limit, lane, idle))
+          return;
+        ready_b = c.b;
+        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[c.b % kStages]));
+        fence_proxy_async_global();  // the slot bytes were published through the generic proxy
+      }
+      const uint64_t r0 = c.k * c.D.rows_per_item;
+      const uint32_t bytes = static_cast<uint32_t>((min(r0 + c.D.rows_per_item, c.D.rows) - r0) * c.D.row_bytes);
+      if (lane == 0) mbar_expect_tx(&full[s], bytes);
+      __syncwarp();
+      stream_item_load(c.D, c.src_contig, c.k, stages + static_cast<size_t>(s) * kStreamStageBytes, &full[s], pol_first,
+                       lane);
+      cursor_next(c, ring, sender, true, lane);
+      ++item;
+    }
+  } else {
+    // ---------------- store warp: landed stages in item order, batch publishes / credits
+    const uint64_t st_pol = sender ? pol_last : pol_first;
+    uint64_t item = 0;
+    uint32_t credit_b = 0xffffffffu;
+    uint64_t t_credit = 0;
+    while (c.b < L.nbatches) {
+      const uint32_t s = static_cast<uint32_t>(item % kStages);
+      if (!warp_mbar_wait(&full[s], static_cast<uint32_t>((item / kStages) & 1), error_flag, spin_limit, lane, idle))
+        break;
+      if ((sender || fwd) && c.first_of_batch && credit_b != c.b) {
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(sender ? L.credit_flags_tx : L.fwd_credit_flags) +
+                            c.b % L.slots;
+        if (c.b >= L.slots &&
+            !warp_flag_wait(f, epoch + c.b - L.slots + 1, sender ? peer : fpeer, error_flag, spin_limit, lane, idle))
+          break;
+        credit_b = c.b;
+        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_credit));
+      }
+      const uint32_t b = c.b;
+      const uint64_t extent = c.extent;
+      stream_item_store(c.D, c.dst_contig, c.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane, fwd,
+                        c.src_contig, fwd_delta, pol_last);
+      bulk_wait_read<0>();  // this stage's bytes are out of shared memory: hand it back
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      const bool last = cursor_next(c, ring, sender, false, lane);
+      ++item;
+      if (!last) continue;
+      const uint32_t slot = b % L.slots;
+      if (sender) {
+        // the batch's slot writes complete, then one release publishes them
+        bulk_wait_all();
+        fence_proxy_async_global();
+        __syncwarp();
+        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
+      } else {
+        if (fwd) {  // relay: the batch's bytes are in the next hop's slot -> publish it there
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __syncwarp();
+          if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.fwd_ready_flags) + slot, epoch + b + 1, fpeer);
+        }
+        // every slot byte of batch b has landed in shared memory: drop the
+        // slot's lines from L2 and hand the slot back
+        if ((flags & kExDiscard) && extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
+          const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(slot) * L.slot_bytes;
+          const uint64_t lines = (extent + 127) >> 7;
+          for (uint64_t i = lane; i < lines; i += 32) discard_l2_line(base + (i << 7));
+        }
+        __syncwarp();
+        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
+      }
+      if (trace && lane == 0)
+        record_batch(trace, L, batches[L.batch0 + b], b, sender ? 0 : 1, sender ? t_credit : t_open[b % kStages]);
+    }
+    bulk_wait_all();  // shared memory stays valid until every store has read it
+  }
+  if (prof && lane == 0) {  // diagnostic: cycles and idle polls per warp
+    unsigned long long* p = prof + 8ull * blockIdx.x + 4 * warp;
+    p[0] = clock64() - t0;
+    p[1] = idle;
+    p[2] = sender;
+    p[3] = warp;
   }
 }
 
@@ -852,6 +1155,23 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
   const int grid = static_cast<int>(ntx + nrx);
   if (grid == 0) return cudaSuccess;
   const int smem = stages * static_cast<int>(kStreamStageBytes);
+  if (flags & kExStreamWS) {  // warp-specialised lane ends (load warp + store warp)
+#define RS_WS_LAUNCH(S)                                                                                     \
+  do {                                                                                                      \
+    cudaError_t e = cudaFuncSetAttribute(rs_stream_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+    if (e != cudaSuccess) return e;                                                                         \
+    rs_stream_ws_kernel<S><<<grid, 64, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, epoch,  \
+                                                       error_flag, spin_limit, flags, trace, prof);         \
+  } while (0)
+    switch (stages) {
+      case 1: RS_WS_LAUNCH(1); break;
+      case 3: RS_WS_LAUNCH(3); break;
+      case 4: RS_WS_LAUNCH(4); break;
+      default: RS_WS_LAUNCH(2); break;
+    }
+#undef RS_WS_LAUNCH
+    return cudaGetLastError();
+  }
 #define RS_STREAM_LAUNCH(S)                                                                                    \
   do {                                                                                                         \
     cudaError_t e = cudaFuncSetAttribute(rs_stream_lane_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -872,6 +1192,22 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
   }
 #undef RS_STREAM_LAUNCH
   return cudaGetLastError();
+}
+
+int stream_ws_max_blocks_per_sm(int stages) {
+  int n = 0;
+  const int smem = stages * static_cast<int>(kStreamStageBytes);
+#define RS_WS_OCC(S)                                                                                         \
+  cudaFuncSetAttribute(rs_stream_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);           \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_stream_ws_kernel<S>, 64, smem)
+  switch (stages) {
+    case 1: RS_WS_OCC(1); break;
+    case 3: RS_WS_OCC(3); break;
+    case 4: RS_WS_OCC(4); break;
+    default: RS_WS_OCC(2); break;
+  }
+#undef RS_WS_OCC
+  return n;
 }
 
 int stream_max_blocks_per_sm(int stages) {

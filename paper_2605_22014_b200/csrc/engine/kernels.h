@@ -38,6 +38,7 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
                                       int stages, rs_trace_record* trace, unsigned long long* prof,
                                       cudaStream_t stream);
 int stream_max_blocks_per_sm(int stages);
+int stream_ws_max_blocks_per_sm(int stages);  // warp-specialised stream lanes (flags bit 512)
 
 // which: 0 LDG4, 3 LDG8, 5 LDG16, 6 CTA8, 4 bulk, 1 pattern, 2/7/8 exchange 256/512/1024 threads
 int rs_kernel_max_blocks_per_sm(int which);

@@ -683,3 +683,34 @@ def test_c4_uneven_stage_migration_on_device(mode):
     assert rep["layers_processed"] == 4
     assert eng.verify_pattern(RS_DST, SEED)[0] == 0
     eng.close()
+
+
+@pytest.mark.parametrize("ring_kernel,stages,slot_kib", [(2, 2, 64), (2, 1, 32), (3, 2, 64), (3, 1, 16), (3, 3, 128),
+                                                         (3, 4, 0)])
+def test_stream_lane_kernels_bitexact(ring_kernel, stages, slot_kib, golden, oracle_c):
+    """The TMA stream lanes -- one warp per lane end (2) or a load warp + a
+    store warp (3) -- over stage counts and slot caps: full GPT-2 C1 equals the
+    reference's digest (twice: epochs advance), and a 16 B-aligned mixed-dtype
+    Llama resize equals the C oracle's bytes.  Descriptor chunks are staged in
+    shared memory, so long lanes cross many chunk boundaries."""
+    sp, co, cn = specs.baseline_case("c1")
+    eng = make_engine(sp, co, cn, "staged", 256 << 20, ring_kernel=ring_kernel, ring_stages=stages,
+                      ring_slot_kib=slot_kib)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    for _ in range(2):
+        rep = R.execute_plan(plan, eng)
+        assert rep["ok"] and rep["ring_kernel"] == ring_kernel, rep
+        assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == \
+            golden["c1_exec"]["1073741824"]["dst_sha"]
+    eng.close()
+    sp = specs.llama("llama-mini-a16", 4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
+    eng = make_engine(sp, co, cn, "staged", 1 << 20, ring_kernel=ring_kernel, ring_stages=stages,
+                      ring_slot_kib=slot_kib, lanes_per_link=2)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["ring_kernel"] == ring_kernel, rep
+    _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 20)
+    for (ti, rank), arr in want.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)
+    eng.close()

@@ -4,7 +4,8 @@ resize, one set of device stores (a DIRECT engine's) bound into STAGED
 engines of every variant; device-timed handoffs, pattern-verified.
 
     python tools/stream_sweep.py [case] [layers|0] [variant,...]
-variant = kernel:stages:slot_kib:K  (kernel 1 classic, 2 stream)
+variant = kernel:stages:slot_kib:K[:copy_kernel]  (kernel 1 classic, 2 stream;
+copy_kernel = RS_COPY_* of the local copies, e.g. 15 LDG8-NP, default 0 = auto)
 """
 import json
 import os
@@ -34,9 +35,13 @@ def main():
     base.fill_pattern(RS_SRC, 42)
     floor_ms = 2 * (summ["total_bytes"] + summ["carryover_bytes"]) / 6552.3e9 * 1e3
     for v in variants:
-        kern, stages, slot, K = (int(x) for x in v.split(":"))
+        fields = [int(x) for x in v.split(":")]
+        kern, stages, slot, K = fields[:4]
+        copy = fields[4] if len(fields) > 4 else 0
         eng = R.Engine([0], staging_bytes=1 << 30, mode="staged", ring_kernel=kern, ring_stages=stages,
-                       ring_slot_kib=slot, slots_per_link=K, trace=bool(os.environ.get("RS_SWEEP_TRACE")))
+                       ring_slot_kib=slot, slots_per_link=K, copy_kernel=copy,
+                       ring_discard=int(os.environ.get("RS_SWEEP_RING_DISCARD", "0")),
+                       trace=bool(os.environ.get("RS_SWEEP_TRACE")))
         eng.layout(RS_SRC, sp, co)
         eng.layout(RS_DST, sp, cn)
         for which in (RS_SRC, RS_DST):
