@@ -142,6 +142,13 @@ class ParallelConfig {
   // extension: DP ranks shard tensors that declare a dp_shard_axis (ZeRO-1)
   bool distributed_optimizer() const { return dist_opt_; }
   ParallelConfig with_distributed_optimizer(bool on) const;
+  // extension: the distributed optimizer's Megatron flat-bucket layout (the
+  // DP shard of a tensor is a contiguous range of its TP-local elements,
+  // see bucket_range) instead of per-tensor dim chunks; bucket_elems 0 =
+  // Megatron's default max(40M, 1M x dp)
+  bool flat_buckets() const { return dist_opt_ && flat_; }
+  std::int64_t bucket_elems() const;
+  ParallelConfig with_flat_buckets(std::int64_t bucket_elems = 0) const;
 
  private:
   std::uint64_t gen_ = 0;
@@ -150,6 +157,8 @@ class ParallelConfig {
   std::vector<int> stage_of_;
   std::unordered_map<int, int> index_;  // rank id -> position (first occurrence)
   bool dist_opt_ = false;
+  bool flat_ = false;
+  std::int64_t bucket_elems_ = 0;
 };
 
 std::vector<std::string> validate_config(const ParallelConfig& config, const ModelSpec& model);
@@ -159,6 +168,28 @@ std::optional<Interval> tp_block(std::int64_t axis_len, int tp_degree, int tp_in
 std::optional<Interval> dp_chunk(const Interval& iv, int parts, int index);
 std::optional<ShardView> view(const TensorSpec& tensor, const ParallelConfig& config, int rank);
 std::map<int, ShardView> owners(const TensorSpec& tensor, const ParallelConfig& config);
+
+// Megatron flat-bucket distributed optimizer (extension).
+// On each pipeline stage and TP index the DP-sharded tensors of one role form
+// a flat buffer in reverse spec order (backward order), each start padded to a
+// multiple of 64 elements; a bucket closes once it holds >= bucket_elems and
+// its end is padded to a multiple of lcm(dp, 128); DP rank d owns the d-th of
+// dp equal contiguous parts of every bucket.  (Megatron-LM megatron/core/
+// distributed/param_and_grad_buffer.py, _ParamAndGradBuffer: params[::-1],
+// _pad_start_of_param_if_needed, _pad_end_of_bucket_if_needed;
+// megatron/core/optimizer/distrib_optimizer.py, _build_model_gbuf_range.)
+// Under such a config view() is the rank's TP block and the rank holds the
+// contiguous element range [lo, hi) of that block's row-major order (nullopt:
+// the whole block; an empty range: view() is nullopt).
+std::optional<std::pair<std::int64_t, std::int64_t>> bucket_range(const ModelSpec& model, std::uint32_t tensor_index,
+                                                                  const ParallelConfig& config, int rank);
+// The boxes (global coordinates, row-major order) of the elements [lo, hi) of
+// `block`'s row-major order: each box is one contiguous run of the block, at
+// most 2 (ndims - 1) + 1 of them (<= 3 for a matrix).
+std::vector<ShardView> flat_range_boxes(const ShardView& block, std::int64_t lo, std::int64_t hi);
+// What `rank` holds of a tensor as boxes: view(), or the boxes of its bucket range.
+std::vector<ShardView> held_boxes(const ModelSpec& model, std::uint32_t tensor_index, const ParallelConfig& config,
+                                  int rank);
 
 struct TransferTask {
   std::uint32_t tensor_index = 0;

@@ -61,8 +61,11 @@ typedef struct {
   int32_t num_ranks;
   const int32_t* ranks;       /* ordered rank ids (placement is semantic) */
   const int32_t* layer_stage; /* num_layers entries, or NULL: default ceil split */
-  int32_t distributed_optimizer; /* extension: DP-shard tensors with a dp_shard_axis (ZeRO-1) */
-  int32_t reserved;
+  int32_t distributed_optimizer; /* extension: DP-shard the tensors with a dp_shard_axis (ZeRO-1):
+                                    0 off, 1 per-tensor dim chunks of the TP block, 2 Megatron
+                                    flat buckets (the rank holds a contiguous element range of its
+                                    TP block, rs_view_range; reshard::bucket_range) */
+  int32_t dist_opt_bucket_elems; /* flat buckets: bucket size in elements (0: max(40M, 1M x dp)) */
 } rs_config;
 
 typedef struct {
@@ -174,6 +177,12 @@ int rs_validate_config(const char* model_spec, const rs_config* cfg, char* buf, 
                        size_t* needed, int32_t* num_violations);
 int rs_view(const char* model_spec, const rs_config* cfg, int32_t tensor_index, int32_t rank,
             int64_t* lo, int64_t* hi, int32_t* present);
+/* Flat-bucket distributed optimizer (extension): the
+ * element range [*lo, *hi) of the rank's TP block (rs_view) it holds, row
+ * major; *flat = 0 when the tensor is not flat-bucket sharded under cfg (then
+ * the range is the whole view).  A store entry holds exactly these elements. */
+int rs_view_range(const char* model_spec, const rs_config* cfg, int32_t tensor_index, int32_t rank, int64_t* lo,
+                  int64_t* hi, int32_t* flat);
 int rs_plan_compute(const char* model_spec, const rs_config* c_old, const rs_config* c_new,
                     const rs_plan_options* opts, rs_plan** out);
 int rs_plan_read(const char* model_spec, const char* plan_text, rs_plan** out);

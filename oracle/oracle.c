@@ -37,6 +37,7 @@ typedef struct {
   char id[128];
   int layer, nd, axis, bpe;       /* axis -1: replicated */
   int dp_axis;                    /* extension: -1, or the distributed-optimizer DP split axis */
+  char role[16];                  /* param / m1 / m2: flat buckets are per role */
   int64_t shape[MAXD];
 } tspec_t;
 
@@ -52,13 +53,15 @@ typedef struct {
   int32_t tp, pp, dp, nranks;
   const int32_t* ranks;
   const int32_t* layer_stage; /* NULL: default ceil split */
-  int32_t dist_opt;           /* extension (no reference counterpart): DP-shard dp_axis tensors */
-  int32_t reserved;
+  int32_t dist_opt;           /* extension (no reference counterpart): DP-shard dp_axis tensors,
+                                 1 dim chunks, 2 Megatron flat buckets */
+  int32_t bucket_elems;       /* flat buckets: bucket size in elements (0: max(40M, 1M x dp)) */
 } orc_config;
 
 typedef struct {
   uint64_t gen;
   int tp, pp, dp, n, L, dist_opt;
+  int64_t bucket;
   int* ranks;
   int* stage;
 } cfg_t;
@@ -137,6 +140,7 @@ static int parse_spec(const char* text, spec_t* sp, char* err, size_t errn) {
         snprintf(err, errn, "spec parse: bad tensor line"); return 1;
       }
       t->axis = (axis[0] == '-') ? -1 : atoi(axis);
+      snprintf(t->role, sizeof t->role, "%s", role);
       t->dp_axis = -1;
       {
         const char* dpo = strstr(line, " dp=");  /* optional extension token */
@@ -162,6 +166,7 @@ static void free_spec(spec_t* sp) { free(sp->t); sp->t = NULL; }
 static void load_cfg(const orc_config* c, int L, cfg_t* out) {
   out->gen = c->gen; out->tp = c->tp; out->pp = c->pp; out->dp = c->dp;
   out->n = c->nranks; out->L = L; out->dist_opt = c->dist_opt;
+  out->bucket = c->bucket_elems > 0 ? c->bucket_elems : (c->dp * 1000000LL > 40000000LL ? c->dp * 1000000LL : 40000000LL);
   out->ranks = (int*)malloc(sizeof(int) * (size_t)(c->nranks > 0 ? c->nranks : 1));
   for (int i = 0; i < c->nranks; ++i) out->ranks[i] = c->ranks[i];
   out->stage = (int*)malloc(sizeof(int) * (size_t)(L > 0 ? L : 1));
@@ -212,6 +217,7 @@ static int dp_chunk(iv_t iv, int parts, int idx, iv_t* out) {
 }
 
 static int dp_sharded(const tspec_t* t, const cfg_t* c) { return c->dist_opt && t->dp_axis >= 0; }
+static int flat_sharded(const tspec_t* t, const cfg_t* c) { return c->dist_opt == 2 && t->dp_axis >= 0; }
 
 /* view: topology.cpp:16-37 (rank given by its index in the rank list),
  * plus the DP chunk of the TP block for distributed-optimizer tensors */
@@ -223,12 +229,112 @@ static int view_coord(const tspec_t* t, const cfg_t* c, int tp, int dp, box_t* o
     if (!tp_block(t->shape[t->axis], c->tp, tp, &b)) return 0;
     out->b[t->axis] = b;
   }
-  if (dp_sharded(t, c)) {
+  if (dp_sharded(t, c) && !flat_sharded(t, c)) {
     iv_t ch;
     if (!dp_chunk(out->b[t->dp_axis], c->dp, dp, &ch)) return 0;
     out->b[t->dp_axis] = ch;
   }
   return 1;
+}
+
+/* Extension (parity unpinned): Megatron's flat-bucket distributed optimizer
+ * (megatron/core/distributed/param_and_grad_buffer.py: parameters laid out
+ * in reverse order, each start padded to 64 elements, a bucket closed once it
+ * reaches the bucket size and its end padded to lcm(dp, 128);
+ * megatron/core/optimizer/distrib_optimizer.py: DP rank d owns the d-th of dp
+ * equal parts of each bucket).  One flat buffer per (stage, role, TP index)
+ * over the dp_axis tensors, in global buffer positions.  Returns the element
+ * range [lo, hi) of tensor ti's TP block held by (tp, dp); empty = 0, 0. */
+static int64_t round_up64(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int64_t tp_local_numel(const tspec_t* t, const cfg_t* c, int tp) {
+  int64_t n = 1;
+  for (int i = 0; i < t->nd; ++i) {
+    if (i == t->axis) {
+      iv_t b;
+      if (!tp_block(t->shape[i], c->tp, tp, &b)) return 0;
+      n *= b.hi - b.lo;
+    } else {
+      n *= t->shape[i];
+    }
+  }
+  return n;
+}
+
+static void flat_range(const spec_t* sp, int ti, const cfg_t* c, int tp, int dp, int64_t* lo, int64_t* hi) {
+  const tspec_t* t = &sp->t[ti];
+  int st = c->stage[t->layer];
+  int64_t a = c->dp, b = 128;
+  while (b) { int64_t r = a % b; a = b; b = r; }
+  int64_t align = c->dp / a * 128;  /* lcm(dp, 128) */
+  int64_t bucket_start = 0, pos = 0, mine = -1, mine_n = 0, mine_bucket = 0, mine_end = -1;
+  for (int k = sp->nt - 1; k >= 0; --k) {
+    const tspec_t* u = &sp->t[k];
+    if (u->dp_axis < 0 || strcmp(u->role, t->role) || c->stage[u->layer] != st) continue;
+    int64_t n = tp_local_numel(u, c, tp);
+    if (!n) continue;
+    pos = round_up64(pos, 64);
+    if (k == ti) { mine = pos; mine_n = n; mine_bucket = bucket_start; }
+    pos += n;
+    if (pos - bucket_start >= c->bucket) {
+      int64_t end = round_up64(pos, align);
+      if (mine >= 0 && mine_end < 0) mine_end = end;
+      bucket_start = pos = end;
+    }
+  }
+  *lo = *hi = 0;
+  if (mine < 0) return;
+  if (mine_end < 0) mine_end = round_up64(pos, align);
+  int64_t part = (mine_end - mine_bucket) / c->dp;
+  int64_t r0 = mine_bucket + part * dp, r1 = r0 + part;
+  int64_t l = mine > r0 ? mine : r0, h = mine + mine_n < r1 ? mine + mine_n : r1;
+  if (l < h) { *lo = l - mine; *hi = h - mine; }
+}
+
+/* The boxes of elements [lo, hi) of v's row-major order, recursively: within
+ * axis d the range splits into a partial first step, whole steps, and a
+ * partial last step; partial steps recurse into axis d + 1 with axis d fixed. */
+static int range_boxes_rec(const box_t* v, int d, int64_t lo, int64_t hi, box_t pre, box_t* out, int n) {
+  if (lo >= hi) return n;
+  int64_t inner = 1;
+  for (int i = d + 1; i < v->nd; ++i) inner *= v->b[i].hi - v->b[i].lo;
+  int64_t a = lo / inner, b = hi / inner;
+  if (a == b) {  /* inside one step of axis d */
+    pre.b[d].lo = v->b[d].lo + a; pre.b[d].hi = pre.b[d].lo + 1;
+    return range_boxes_rec(v, d + 1, lo - a * inner, hi - a * inner, pre, out, n);
+  }
+  int64_t full0 = a;
+  if (lo % inner) {
+    pre.b[d].lo = v->b[d].lo + a; pre.b[d].hi = pre.b[d].lo + 1;
+    n = range_boxes_rec(v, d + 1, lo - a * inner, inner, pre, out, n);
+    full0 = a + 1;
+  }
+  if (b > full0) {
+    box_t x = pre;
+    x.b[d].lo = v->b[d].lo + full0; x.b[d].hi = v->b[d].lo + b;
+    for (int i = d + 1; i < v->nd; ++i) x.b[i] = v->b[i];
+    out[n++] = x;
+  }
+  if (hi % inner) {
+    pre.b[d].lo = v->b[d].lo + b; pre.b[d].hi = pre.b[d].lo + 1;
+    n = range_boxes_rec(v, d + 1, 0, hi - b * inner, pre, out, n);
+  }
+  return n;
+}
+
+static int range_boxes(const box_t* v, int64_t lo, int64_t hi, box_t* out) {
+  box_t pre = *v;
+  return range_boxes_rec(v, 0, lo, hi, pre, out, 0);
+}
+
+/* what (tp, dp) holds of tensor ti: its view, or the boxes of its flat range */
+static int held_coord(const spec_t* sp, int ti, const cfg_t* c, int tp, int dp, box_t* out) {
+  box_t v;
+  if (!view_coord(&sp->t[ti], c, tp, dp, &v)) return 0;
+  if (!flat_sharded(&sp->t[ti], c)) { out[0] = v; return 1; }
+  int64_t lo, hi;
+  flat_range(sp, ti, c, tp, dp, &lo, &hi);
+  return range_boxes(&v, lo, hi, out);
 }
 
 static int view_at(const tspec_t* t, const cfg_t* c, int idx, box_t* out) {
@@ -356,6 +462,62 @@ static int compute_plan(const spec_t* sp, const cfg_t* co, const cfg_t* cn, int 
     if (sharded) {
       for (int i = 0; i < co->tp; ++i) { iv_t b; if (tp_block(alen, co->tp, i, &b)) { btp[nblk] = i; biv[nblk] = b; ++nblk; } }
     } else { btp[0] = -1; biv[0].lo = 0; biv[0].hi = 1; nblk = 1; }
+    if (t->dp_axis >= 0 && (co->dist_opt == 2 || cn->dist_opt == 2)) {
+      /* extension: a flat-bucket side (parity unpinned).  Every box the new
+         (tp, dp) holds, tiled by every box an old holder holds: all dp
+         indices when the old state is DP-sharded, dp 0 otherwise; tensors
+         without a TP axis from old TP index 0 (each TP index cuts them
+         differently).  Self-held boxes keep in place when block and flat
+         offset are unchanged. */
+      int osh = co->dist_opt != 0, ntp = t->axis >= 0 ? co->tp : 1;
+      static box_t db[2 * MAXD], sb[2 * MAXD];
+      for (int dtp = 0; dtp < cn->tp; ++dtp)
+        for (int ddp = 0; ddp < cn->dp; ++ddp) {
+          int dst = rank_at(cn, dtp, ddp, sn);
+          int ndb = held_coord(sp, ti, cn, dtp, ddp, db);
+          if (!ndb) continue;
+          box_t vdn; view_coord(t, cn, dtp, ddp, &vdn);
+          int64_t lon = 0, hin = 0;
+          if (flat_sharded(t, cn)) flat_range(sp, ti, cn, dtp, ddp, &lon, &hin);
+          int have_old = 0, otp = -1, odp = -1; box_t vdo; int64_t loo = 0, hio = 0;
+          int oidx = cfg_index(co, dst);
+          if (oidx >= 0) {
+            int a, b, c; coord_of(co, oidx, &a, &b, &c);
+            if (b == so && view_coord(t, co, a, c, &vdo)) {
+              have_old = 1; otp = a; odp = c;
+              if (flat_sharded(t, co)) flat_range(sp, ti, co, a, c, &loo, &hio);
+            }
+          }
+          for (int i = 0; i < ndb; ++i)
+            for (int stp = 0; stp < ntp; ++stp)
+              for (int sdp = 0; sdp < (osh ? co->dp : 1); ++sdp) {
+                int nsb = held_coord(sp, ti, co, stp, sdp, sb);
+                int src = rank_at(co, stp, sdp, so);
+                for (int j = 0; j < nsb; ++j) {
+                  ++pairs;
+                  box_t r; r.nd = t->nd;
+                  int empty = 0;
+                  for (int x = 0; x < t->nd; ++x) {
+                    r.b[x].lo = db[i].b[x].lo > sb[j].b[x].lo ? db[i].b[x].lo : sb[j].b[x].lo;
+                    r.b[x].hi = db[i].b[x].hi < sb[j].b[x].hi ? db[i].b[x].hi : sb[j].b[x].hi;
+                    if (r.b[x].lo >= r.b[x].hi) empty = 1;
+                  }
+                  if (empty) continue;
+                  int64_t bytes = box_count(&r) * t->bpe;
+                  if (have_old && otp == stp && (!osh || odp == sdp)) {
+                    int same = loo == lon && !memcmp(vdo.b, vdn.b, sizeof(iv_t) * (size_t)t->nd) &&
+                               layout_identical(&vdo, &vdn, &r);
+                    if (same) { keep_t kk = { (uint32_t)ti, t->layer, dst, r, bytes, 0 }; push_keep(plan, kk); }
+                    else { task_t tt = { (uint32_t)ti, t->layer, dst, dst, r, bytes, 0 }; push_task(plan, tt); }
+                    continue;
+                  }
+                  task_t tt = { (uint32_t)ti, t->layer, src, dst, r, bytes, 0 };
+                  push_task(plan, tt);
+                }
+              }
+        }
+      continue;
+    }
     /* extension: distributed-optimizer DP chunks (parity unpinned) */
     int dpo = dp_sharded(t, co), dpn = dp_sharded(t, cn), dax = t->dp_axis;
     for (int dtp = 0; dtp < cn->tp; ++dtp) {
@@ -549,7 +711,33 @@ static int owners(const tspec_t* t, const cfg_t* c, int* ranks_out, box_t* views
   return m;
 }
 
-/* verify_plan: planner.cpp:194-303 */
+/* the element range of its view a rank holds: [0, count) unless flat */
+static void held_range(const spec_t* sp, int ti, const cfg_t* c, int rank, const box_t* v, int64_t* lo, int64_t* hi) {
+  *lo = 0; *hi = box_count(v);
+  if (!flat_sharded(&sp->t[ti], c)) return;
+  int tp, pp, dp;
+  coord_of(c, cfg_index(c, rank), &tp, &pp, &dp);
+  flat_range(sp, ti, c, tp, dp, lo, hi);
+}
+
+/* row-major positions of a region's first and last elements in view v */
+static void region_span(const box_t* v, const box_t* r, int64_t* first, int64_t* last) {
+  *first = *last = 0;
+  for (int i = 0; i < v->nd; ++i) {
+    int64_t len = v->b[i].hi - v->b[i].lo;
+    *first = *first * len + (r->b[i].lo - v->b[i].lo);
+    *last = *last * len + (r->b[i].hi - 1 - v->b[i].lo);
+  }
+}
+
+static int held_contains(const box_t* v, int64_t lo, int64_t hi, const box_t* r) {
+  if (!box_contains(v, r)) return 0;
+  int64_t f, l;
+  region_span(v, r, &f, &l);
+  return f >= lo && l < hi;
+}
+
+/* verify_plan: planner.cpp:194-303 (flat-bucket holders: an element range of the view) */
 static char* verify(const plan_t* p, const cfg_t* co, const cfg_t* cn, const spec_t* sp) {
   vlist v = {{0}, 0};
   int* p2m = (int*)malloc(sizeof(int) * (size_t)(p->ntid ? p->ntid : 1));
@@ -566,13 +754,16 @@ static char* verify(const plan_t* p, const cfg_t* co, const cfg_t* cn, const spe
     int ns_ = owners(t, co, sr, sv);
     for (int d = 0; d < nd_; ++d) {
       const box_t* vd = &dv[d];
+      int64_t dlo, dhi;
+      held_range(sp, mi, cn, dr[d], vd, &dlo, &dhi);
+      if (dlo >= dhi) continue;  /* an empty flat-bucket range */
       int64_t n = box_count(vd), str[MAXD];
       uint8_t* cover = (uint8_t*)calloc((size_t)n, 1);
       str[vd->nd - 1] = 1;
       for (int i = vd->nd - 2; i >= 0; --i) str[i] = str[i + 1] * (vd->b[i + 1].hi - vd->b[i + 1].lo);
       #define MARK(region, what) do {                                                  \
         const box_t* R = (region);                                                     \
-        if (!box_contains(vd, R)) {                                                    \
+        if (!held_contains(vd, dlo, dhi, R)) {                                         \
           complain(&v, "%s for tensor %s rank %d escapes destination view", what, t->id, dr[d]); \
         } else {                                                                       \
           int64_t pt[MAXD];                                                            \
@@ -594,8 +785,10 @@ static char* verify(const plan_t* p, const cfg_t* co, const cfg_t* cn, const spe
         if (box_count(&tk->bx) <= 0 || tk->bytes <= 0) { complain(&v, "empty task for tensor %s", t->id); continue; }
         int si = -1;
         for (int s = 0; s < ns_; ++s) if (sr[s] == tk->src) si = s;
-        if (si < 0) complain(&v, "task source rank %d owns nothing of tensor %s", tk->src, t->id);
-        else if (!box_contains(&sv[si], &tk->bx))
+        int64_t slo = 0, shi = 0;
+        if (si >= 0) held_range(sp, mi, co, sr[si], &sv[si], &slo, &shi);
+        if (si < 0 || slo >= shi) complain(&v, "task source rank %d owns nothing of tensor %s", tk->src, t->id);
+        else if (!held_contains(&sv[si], slo, shi, &tk->bx))
           complain(&v, "task bounds escape source view for tensor %s src %d", t->id, tk->src);
         MARK(&tk->bx, "task");
       }
@@ -605,13 +798,18 @@ static char* verify(const plan_t* p, const cfg_t* co, const cfg_t* cn, const spe
         if (p2m[kp->ti] != mi) continue;
         int si = -1;
         for (int s = 0; s < ns_; ++s) if (sr[s] == kp->rank) si = s;
-        if (si < 0 || !box_contains(&sv[si], &kp->bx))
+        int64_t slo = 0, shi = 0;
+        if (si >= 0) held_range(sp, mi, co, sr[si], &sv[si], &slo, &shi);
+        if (si < 0 || !held_contains(&sv[si], slo, shi, &kp->bx))
           complain(&v, "carryover not resident in old view for tensor %s rank %d", t->id, kp->rank);
         MARK(&kp->bx, "carryover");
       }
       #undef MARK
       int64_t gaps = 0, over = 0;
-      for (int64_t i = 0; i < n; ++i) { if (!cover[i]) ++gaps; if (cover[i] > 1) ++over; }
+      for (int64_t i = 0; i < n; ++i) {
+        if (i >= dlo && i < dhi && !cover[i]) ++gaps;
+        if (cover[i] > 1) ++over;
+      }
       if (gaps) complain(&v, "coverage gap: tensor %s rank %d missing %lld elements", t->id, dr[d], (long long)gaps);
       if (over) complain(&v, "coverage overlap: tensor %s rank %d has %lld doubly-covered elements", t->id, dr[d], (long long)over);
       free(cover);
@@ -636,8 +834,10 @@ uint8_t orc_pattern_byte(uint32_t ti, int64_t element, int64_t b, uint64_t seed)
   return (uint8_t)(h >> ((b % 8) * 8));
 }
 
-typedef struct { int rank; box_t view; uint8_t* bytes; int64_t n; } entry_t;
+typedef struct { int rank; box_t view; uint8_t* bytes; int64_t n; int flat; int64_t flo; } entry_t;
 typedef struct { int nt; int* cnt; entry_t** e; int bpe_dummy; } store_t;
+
+static int owners(const tspec_t* t, const cfg_t* c, int* ranks_out, box_t* views_out);
 
 static store_t* store_alloc(const spec_t* sp, const cfg_t* c) {
   store_t* s = (store_t*)calloc(1, sizeof(store_t));
@@ -653,6 +853,15 @@ static store_t* store_alloc(const spec_t* sp, const cfg_t* c) {
       entry_t* e = &s->e[ti][k];
       e->rank = rk[k]; e->view = vw[k];
       e->n = box_count(&vw[k]) * sp->t[ti].bpe;
+      e->flat = 0; e->flo = 0;
+      if (flat_sharded(&sp->t[ti], c)) {  /* a flat-bucket shard holds an element range of its view */
+        int tp, pp, dp;
+        int64_t lo, hi;
+        coord_of(c, cfg_index(c, rk[k]), &tp, &pp, &dp);
+        flat_range(sp, ti, c, tp, dp, &lo, &hi);
+        e->flat = 1; e->flo = lo;
+        e->n = (hi - lo) * sp->t[ti].bpe;
+      }
       e->bytes = (uint8_t*)calloc((size_t)(e->n ? e->n : 1), 1);
     }
   }
@@ -683,6 +892,21 @@ static void store_fill(store_t* s, const spec_t* sp, uint64_t seed) {
     for (int i = t->nd - 2; i >= 0; --i) gs[i] = gs[i + 1] * t->shape[i + 1];
     for (int k = 0; k < s->cnt[ti]; ++k) {
       entry_t* e = &s->e[ti][k];
+      if (e->flat) {  /* element j of the range: decode its coordinates in the view */
+        uint8_t* out = e->bytes;
+        uint64_t base = seed ^ (0x1000003ULL * (uint32_t)ti);
+        for (int64_t j = e->flo; j < e->flo + e->n / t->bpe; ++j) {
+          int64_t rem = j, g = 0;
+          for (int i = t->nd - 1; i >= 0; --i) {
+            int64_t len = e->view.b[i].hi - e->view.b[i].lo;
+            g += (e->view.b[i].lo + rem % len) * gs[i];
+            rem /= len;
+          }
+          uint64_t h = splitmix64(base ^ (uint64_t)g);
+          for (int b = 0; b < t->bpe; ++b) *out++ = (uint8_t)(h >> ((b % 8) * 8));
+        }
+        continue;
+      }
       int64_t pt[MAXD];
       for (int i = 0; i < t->nd; ++i) pt[i] = e->view.b[i].lo;
       uint8_t* out = e->bytes;
@@ -705,10 +929,37 @@ static void store_fill(store_t* s, const spec_t* sp, uint64_t seed) {
 
 /* for_each_row + slice_local / scatter_local: executor.cpp:23-93.
  * dir 0: buffer -> payload (slice), dir 1: payload -> buffer (scatter). */
+static int move_rows_at(uint8_t* buf, int64_t buflen, const box_t* owner, int flat, int64_t flo,
+                        const box_t* region, uint8_t* payload, int64_t paylen, int64_t bpe, int dir, char* err,
+                        size_t errn);
+
 static int move_rows(uint8_t* buf, int64_t buflen, const box_t* owner, const box_t* region,
                      uint8_t* payload, int64_t paylen, int64_t bpe, int dir, char* err, size_t errn) {
+  return move_rows_at(buf, buflen, owner, 0, 0, region, payload, paylen, bpe, dir, err, errn);
+}
+
+static int move_entry(entry_t* e, const box_t* region, uint8_t* payload, int64_t paylen, int64_t bpe, int dir,
+                      char* err, size_t errn) {
+  return move_rows_at(e->bytes, e->n, &e->view, e->flat, e->flo, region, payload, paylen, bpe, dir, err, errn);
+}
+
+/* flat = 1: the buffer holds elements [flo, flo + buflen / bpe) of the
+ * owner's row-major order (a flat-bucket shard) */
+static int move_rows_at(uint8_t* buf, int64_t buflen, const box_t* owner, int flat, int64_t flo,
+                        const box_t* region, uint8_t* payload, int64_t paylen, int64_t bpe, int dir, char* err,
+                        size_t errn) {
   const char* who = dir ? "scatter_local" : "slice_local";
-  if (!box_contains(owner, region)) {
+  int escapes = !box_contains(owner, region);
+  if (!escapes && flat) {  /* first and last region elements inside the held range */
+    int64_t first = 0, last = 0;
+    for (int i = 0; i < owner->nd; ++i) {
+      int64_t len = owner->b[i].hi - owner->b[i].lo;
+      first = first * len + (region->b[i].lo - owner->b[i].lo);
+      last = last * len + (region->b[i].hi - 1 - owner->b[i].lo);
+    }
+    escapes = first < flo || last >= flo + buflen / bpe;
+  }
+  if (escapes) {
     sbuf b = {0};
     sb_printf(&b, "%s: bounds ", who); box_text(&b, region, 1);
     sb_printf(&b, " escape owner view "); box_text(&b, owner, 1);
@@ -716,7 +967,7 @@ static int move_rows(uint8_t* buf, int64_t buflen, const box_t* owner, const box
     return 1;
   }
   if (dir && paylen != box_count(region) * bpe) { snprintf(err, errn, "scatter_local: payload length mismatch"); return 1; }
-  if (buflen != box_count(owner) * bpe) { snprintf(err, errn, "%s: buffer size does not match owner view", who); return 1; }
+  if (!flat && buflen != box_count(owner) * bpe) { snprintf(err, errn, "%s: buffer size does not match owner view", who); return 1; }
   int nd = owner->nd;
   int64_t st[MAXD];
   st[nd - 1] = 1;
@@ -726,6 +977,7 @@ static int move_rows(uint8_t* buf, int64_t buflen, const box_t* owner, const box
   for (;;) {
     int64_t off = 0;
     for (int i = 0; i < nd; ++i) off += (pt[i] - owner->b[i].lo) * st[i];
+    off -= flo;
     if (dir) memcpy(buf + off * bpe, payload + cur, (size_t)rowb);
     else memcpy(payload + cur, buf + off * bpe, (size_t)rowb);
     cur += rowb;
@@ -792,7 +1044,7 @@ static int flush_frames(frame_t* q, const int64_t* order, int64_t lo, int64_t hi
     frame_t* f = &q[order[k]];
     entry_t* de = store_at(dst, f->dst, f->ti);
     if (!de) { snprintf(err, errn, "shard store: no buffer for rank %d tensor %u", f->dst, f->ti); return 1; }
-    if (move_rows(de->bytes, de->n, &de->view, &f->bx, f->data, f->n, sp->t[f->ti].bpe, 1, err, errn)) return 1;
+    if (move_entry(de, &f->bx, f->data, f->n, sp->t[f->ti].bpe, 1, err, errn)) return 1;
   }
   return 0;
 }
@@ -821,8 +1073,8 @@ static void execute(const plan_t* p, const spec_t* sp, store_t* src, store_t* ds
       if (!s || !d) { snprintf(err, sizeof err, "shard store: no buffer for rank %d tensor %u", kp->rank, kp->ti); failed = 1; break; }
       int64_t bpe = sp->t[kp->ti].bpe, n = box_count(&kp->bx) * bpe;
       uint8_t* tmp = (uint8_t*)malloc((size_t)(n ? n : 1));
-      failed = move_rows(s->bytes, s->n, &s->view, &kp->bx, tmp, n, bpe, 0, err, sizeof err) ||
-               move_rows(d->bytes, d->n, &d->view, &kp->bx, tmp, n, bpe, 1, err, sizeof err);
+      failed = move_entry(s, &kp->bx, tmp, n, bpe, 0, err, sizeof err) ||
+               move_entry(d, &kp->bx, tmp, n, bpe, 1, err, sizeof err);
       free(tmp);
     }
     for (int64_t k = it; k < te && !failed; ++k) {
@@ -836,12 +1088,12 @@ static void execute(const plan_t* p, const spec_t* sp, store_t* src, store_t* ds
       for (int64_t c = 0; c < pcs.n && !failed; ++c) {
         int64_t n = box_count(&pcs.v[c]) * bpe;
         uint8_t* tmp = (uint8_t*)malloc((size_t)(n ? n : 1));
-        if (move_rows(s->bytes, s->n, &s->view, &pcs.v[c], tmp, n, bpe, 0, err, sizeof err)) { free(tmp); failed = 1; break; }
+        if (move_entry(s, &pcs.v[c], tmp, n, bpe, 0, err, sizeof err)) { free(tmp); failed = 1; break; }
         if (tk->src == tk->dst) {
           entry_t* d = store_at(dst, tk->dst, tk->ti);
           if (!d) { snprintf(err, sizeof err, "shard store: no buffer for rank %d tensor %u", tk->dst, tk->ti); free(tmp); failed = 1; break; }
           rep->local_copy_bytes += n;
-          if (move_rows(d->bytes, d->n, &d->view, &pcs.v[c], tmp, n, bpe, 1, err, sizeof err)) failed = 1;
+          if (move_entry(d, &pcs.v[c], tmp, n, bpe, 1, err, sizeof err)) failed = 1;
           free(tmp);
         } else {
           if (nq == capq) { capq = capq ? capq * 2 : 64; q = (frame_t*)realloc(q, sizeof(frame_t) * (size_t)capq); }

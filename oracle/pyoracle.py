@@ -32,7 +32,7 @@ class _Config(C.Structure):
     _fields_ = [("gen", C.c_uint64), ("tp", C.c_int32), ("pp", C.c_int32), ("dp", C.c_int32),
                 ("nranks", C.c_int32), ("ranks", C.POINTER(C.c_int32)),
                 ("layer_stage", C.POINTER(C.c_int32)), ("distributed_optimizer", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("bucket_elems", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -67,7 +67,7 @@ def config_struct(cfg, num_layers: int):
         stage = (C.c_int32 * max(1, num_layers))(*cfg.layer_stage)
     s = _Config(cfg.gen, cfg.tp, cfg.pp, cfg.dp, len(cfg.ranks), ranks,
                 C.cast(stage, C.POINTER(C.c_int32)) if stage is not None else None,
-                int(getattr(cfg, "dist_opt", False)), 0)
+                int(getattr(cfg, "dist_opt", 0)), int(getattr(cfg, "bucket_elems", 0)))
     s._keep = (ranks, stage)
     return s
 

@@ -68,8 +68,12 @@ reshard::ParallelConfig to_config(const rs_config* c, int num_layers) {
   std::vector<int> ranks(c->ranks, c->ranks + c->num_ranks);
   std::vector<int> stages = c->layer_stage ? std::vector<int>(c->layer_stage, c->layer_stage + num_layers)
                                            : reshard::ParallelConfig::default_layer_assignment(num_layers, c->pp);
-  return reshard::ParallelConfig(c->generation_id, c->tp, c->pp, c->dp, std::move(ranks), std::move(stages))
-      .with_distributed_optimizer(c->distributed_optimizer != 0);
+  if (c->distributed_optimizer < 0 || c->distributed_optimizer > 2)
+    throw std::invalid_argument("config: distributed_optimizer must be 0 (off), 1 (dim chunks) or 2 (flat buckets)");
+  if (c->dist_opt_bucket_elems < 0) throw std::invalid_argument("config: negative dist_opt_bucket_elems");
+  auto cfg = reshard::ParallelConfig(c->generation_id, c->tp, c->pp, c->dp, std::move(ranks), std::move(stages))
+                 .with_distributed_optimizer(c->distributed_optimizer != 0);
+  return c->distributed_optimizer == 2 ? cfg.with_flat_buckets(c->dist_opt_bucket_elems) : cfg;
 }
 
 // Copies s into buf (truncating); *needed is the full size incl. the NUL.
@@ -114,6 +118,24 @@ int rs_view(const char* model_spec, const rs_config* cfg, int32_t tensor_index, 
         lo[i] = v->dim(i).lo;
         hi[i] = v->dim(i).hi;
       }
+  });
+}
+
+int rs_view_range(const char* model_spec, const rs_config* cfg, int32_t tensor_index, int32_t rank, int64_t* lo,
+                  int64_t* hi, int32_t* flat) {
+  return guarded([&] {
+    if (!lo || !hi || !flat) throw std::invalid_argument("null argument");
+    auto m = reshard::ModelSpec::parse(model_spec ? model_spec : "");
+    if (tensor_index < 0 || tensor_index >= static_cast<int32_t>(m.tensors.size()))
+      throw std::invalid_argument("tensor index out of range");
+    const auto c = to_config(cfg, m.num_layers);
+    const auto ti = static_cast<std::uint32_t>(tensor_index);
+    auto r = reshard::bucket_range(m, ti, c, rank);
+    *flat = r.has_value();
+    *lo = r ? r->first : 0;
+    *hi = r ? r->second : 0;
+    if (!r)
+      if (auto v = reshard::view(m.tensors[ti], c, rank)) *hi = v->element_count();
   });
 }
 

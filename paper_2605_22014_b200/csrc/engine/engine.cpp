@@ -251,6 +251,13 @@ void Engine::layout(int which, const reshard::ModelSpec& model, const reshard::P
       e.slot = rank_slot[static_cast<std::size_t>(cfg.index_of(rank))];
       e.view = v;
       e.nbytes = v.element_count() * model.element_bytes(t);
+      if (auto r = reshard::bucket_range(model, ti, cfg, rank)) {  // flat-bucket distributed optimizer
+        e.flat = true;
+        e.flat_lo = r->first;
+        e.flat_off = r->first * model.element_bytes(t);
+        e.flat_elems = r->second - r->first;
+        e.nbytes = (r->second - r->first) * model.element_bytes(t);
+      }
       // deterministic arena offsets for every slot: peers compute the same
       auto& used = s.arena_bytes[static_cast<std::size_t>(e.slot)];
       e.off = used;
@@ -505,7 +512,17 @@ std::int64_t Engine::pattern_pass(int which, std::uint64_t seed, bool verify, st
       const Entry& e = s.entries[k];
       if (e.slot != dv.slot) continue;
       const auto& t = s.model.tensors[e.ti];
-      append_pattern(descs, addr(e.ptr), t, e.view, s.model.element_bytes(t), e.ti, k, item_bytes);
+      const std::int64_t eb = s.model.element_bytes(t);
+      if (!e.flat) {
+        append_pattern(descs, addr(e.ptr), t, e.view, eb, e.ti, k, item_bytes);
+        continue;
+      }
+      // a flat-bucket shard: one pattern run per contiguous box of its range
+      std::int64_t at = 0;
+      for (const auto& b : reshard::flat_range_boxes(e.view, e.flat_lo, e.flat_lo + e.nbytes / eb)) {
+        append_pattern(descs, addr(e.ptr) + static_cast<std::uint64_t>(at), t, b, eb, e.ti, k, item_bytes);
+        at += b.element_count() * eb;
+      }
     }
     std::vector<std::uint64_t> item0(descs.size());
     std::uint64_t items = 0;
@@ -622,8 +639,8 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
     const int l = local_of(se->slot);
     if (l < 0) return;  // the source's process pushes it
     if (de->slot != se->slot) programs_[static_cast<std::size_t>(l)].peer_stores = true;
-    append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
-                addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
+    append_copy(programs_[static_cast<std::size_t>(l)].local, view_base(se, "source"), se->view,
+                view_base(de, "destination"), de->view, box, eb, static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
   };
 
   for (int layer : plan_layers_) {
@@ -635,8 +652,8 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
           const Entry* se = src.find(k.rank, k.tensor_index);
           const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
           if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
-          if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
-          if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
+          if (!holds(se, k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
+          if (!holds(de, k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
           push(se, de, k.bounds, eb, layer);
           delta.carryover_bytes += k.bounds.element_count() * eb;
@@ -646,12 +663,12 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
         for (const auto& t : it->second) {
           const Entry* se = src.find(t.src_rank, t.tensor_index);
           if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
-          if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
+          if (!holds(se, t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
           const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
           if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
           if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
-          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
+          if (!holds(de, t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
           push(se, de, t.bounds, eb, layer);
           const std::int64_t n = t.bounds.element_count() * eb;
           if (t.is_local()) delta.local_copy_bytes += n;

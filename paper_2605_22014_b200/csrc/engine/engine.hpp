@@ -73,6 +73,11 @@ struct Entry {
   int slot = 0;            // global device slot holding the buffer
   reshard::ShardView view;
   std::int64_t nbytes = 0;
+  // flat-bucket shards (reshard::bucket_range): the buffer holds the element
+  // range [flat_lo, flat_lo + nbytes / eb) of the view's row-major order, so
+  // view-relative addressing starts flat_off = flat_lo * eb bytes before ptr
+  bool flat = false;
+  std::int64_t flat_lo = 0, flat_off = 0, flat_elems = 0;
   std::size_t off = 0;     // offset in the slot's engine arena (rs_store_alloc)
   char* ptr = nullptr;     // local, peer-mapped (IPC) or caller-bound address
 };

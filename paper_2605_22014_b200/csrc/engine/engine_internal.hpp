@@ -53,5 +53,26 @@ inline char* need_ptr(const Entry* e, const char* what) {
   return e->ptr;
 }
 
+// Address of the entry's view origin: shard buffers are addressed row-major
+// over the view; a flat-bucket shard's buffer starts flat_off bytes in.
+inline std::uint64_t view_base(const Entry* e, const char* what) {
+  return addr(need_ptr(e, what)) - static_cast<std::uint64_t>(e->flat_off);
+}
+
+// Does the entry's buffer hold every element of `box`?  (Inside the view,
+// and for a flat-bucket shard its first and last elements -- row-major --
+// inside the held range.)
+inline bool holds(const Entry* e, const reshard::ShardView& box) {
+  if (!e->view.contains(box)) return false;
+  if (!e->flat) return true;
+  std::int64_t first = 0, last = 0;
+  for (std::size_t k = 0; k < box.ndims(); ++k) {
+    const std::int64_t len = e->view.dim(k).length();
+    first = first * len + (box.dim(k).lo - e->view.dim(k).lo);
+    last = last * len + (box.dim(k).hi - 1 - e->view.dim(k).lo);
+  }
+  return first >= e->flat_lo && last < e->flat_lo + e->flat_elems;
+}
+
 }  // namespace detail
 }  // namespace rsb

@@ -382,8 +382,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     auto local_copy = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb) {
       const int l = local_of(se->slot);
       if (l < 0) return;
-      append_copy(programs_[static_cast<std::size_t>(l)].local, addr(need_ptr(se, "source")), se->view,
-                  addr(need_ptr(de, "destination")), de->view, box, eb, static_cast<std::uint32_t>(layer));
+      append_copy(programs_[static_cast<std::size_t>(l)].local, view_base(se, "source"), se->view,
+                  view_base(de, "destination"), de->view, box, eb, static_cast<std::uint32_t>(layer));
     };
     try {
       if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end()) {
@@ -391,8 +391,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           const Entry* se = src.find(k.rank, k.tensor_index);
           const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
           if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
-          if (!se->view.contains(k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
-          if (!de->view.contains(k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
+          if (!holds(se, k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
+          if (!holds(de, k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
           local_copy(se, de, k.bounds, eb);
           delta.carryover_bytes += k.bounds.element_count() * eb;
@@ -403,12 +403,12 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
           const auto& t = it->second[ti];
           const Entry* se = src.find(t.src_rank, t.tensor_index);
           if (!se) throw IntegrityError(no_buffer(t.src_rank, t.tensor_index));
-          if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
+          if (!holds(se, t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
           const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
           if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
           if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
-          if (!de->view.contains(t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
+          if (!holds(de, t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
           if (t.is_local()) {
             local_copy(se, de, t.bounds, eb);
             delta.local_copy_bytes += t.bounds.element_count() * eb;
@@ -506,7 +506,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       for (auto& batch : hb.batches)
         for (auto& f : batch) {
           f.de = dst.find(chain[h], f.se->ti);
-          if (!f.de || !f.de->view.contains(f.region))  // the plan's own task for this hop was checked above
+          if (!f.de || !holds(f.de, f.region))  // the plan's own task for this hop was checked above
             throw IntegrityError("relay: dst rank " + std::to_string(chain[h]) + " has no buffer for a forwarded box");
         }
       hb.dslot = -1;
@@ -635,7 +635,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       Bd.pack0 = static_cast<std::uint32_t>(frames.size());
       if (tx_local[i])
         for (const auto& f : lb.batches[b])
-          append_copy(frames, addr(f.se->ptr), f.se->view, slot_addr + f.off, f.region, f.region, f.eb,
+          append_copy(frames, addr(f.se->ptr) - static_cast<std::uint64_t>(f.se->flat_off), f.se->view, slot_addr + f.off,
+                      f.region, f.region, f.eb,
                       static_cast<std::uint32_t>(f.layer));
       for (const auto& f : lb.batches[b]) {
         const std::uint64_t n = static_cast<std::uint64_t>(f.region.element_count() * f.eb);
@@ -649,7 +650,7 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
       Bd.unpack0 = static_cast<std::uint32_t>(unpack.size());  // rebased below
       if (rx_local[i])
         for (const auto& f : lb.batches[b])
-          append_copy(unpack, slot_addr + f.off, f.region, addr(need_ptr(f.de, "destination")), f.de->view, f.region,
+          append_copy(unpack, slot_addr + f.off, f.region, view_base(f.de, "destination"), f.de->view, f.region,
                       f.eb, static_cast<std::uint32_t>(f.layer));
       Bd.nunpack = static_cast<std::uint32_t>(unpack.size()) - Bd.unpack0;
       Bd.unpack_items = static_cast<std::uint32_t>(assign_items(unpack, Bd.unpack0, 0, frame_item));
@@ -752,8 +753,9 @@ bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
       if (!se || !de) continue;  // an integrity failure: reported by compile_staged
       const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
       scratch.clear();
-      append_copy(scratch, 0, se->view, 0, t.bounds, t.bounds, eb, 0);  // pack: shard -> packed frame
-      append_copy(scratch, 0, t.bounds, 0, de->view, t.bounds, eb, 0);  // unpack: packed frame -> shard
+      // (bases 0 - flat_off: a flat-bucket shard's view origin keeps its alignment)
+      append_copy(scratch, static_cast<std::uint64_t>(-se->flat_off), se->view, 0, t.bounds, t.bounds, eb, 0);
+      append_copy(scratch, 0, t.bounds, static_cast<std::uint64_t>(-de->flat_off), de->view, t.bounds, eb, 0);
       for (const auto& d : scratch)
         if (d.vec_log2 != 4 || d.row_bytes > 16384) return false;
     }

@@ -17,6 +17,7 @@
 
 #include "compile.hpp"
 #include "engine.hpp"
+#include "engine_internal.hpp"
 #include "kernels.h"
 
 namespace rsb {
@@ -97,7 +98,8 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
       if (se->slot == de->slot) {
         if (se->slot != me) return;
         if (!se->ptr || !de->ptr) throw DomainError("xfer: local shard without device memory");
-        append_copy(p.local, addr_of(se->ptr), se->view, addr_of(de->ptr), de->view, box, eb,
+        append_copy(p.local, addr_of(se->ptr) - static_cast<std::uint64_t>(se->flat_off), se->view,
+                    addr_of(de->ptr) - static_cast<std::uint64_t>(de->flat_off), de->view, box, eb,
                     static_cast<std::uint32_t>(layer));
         return;
       }
@@ -131,8 +133,8 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
           const Entry* se = src.find(k.rank, k.tensor_index);
           const Entry* de = se ? dst.find(k.rank, k.tensor_index) : nullptr;
           if (!se || !de) throw IntegrityError(missing(k.rank, k.tensor_index));
-          if (!se->view.contains(k.bounds)) throw IntegrityError(escapes("slice_local", k.bounds, se->view));
-          if (!de->view.contains(k.bounds)) throw IntegrityError(escapes("scatter_local", k.bounds, de->view));
+          if (!detail::holds(se, k.bounds)) throw IntegrityError(escapes("slice_local", k.bounds, se->view));
+          if (!detail::holds(de, k.bounds)) throw IntegrityError(escapes("scatter_local", k.bounds, de->view));
           const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
           route(se, de, k.bounds, eb, k.rank, k.rank);
           delta.carryover_bytes += k.bounds.element_count() * eb;
@@ -141,12 +143,12 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
         for (const auto& t : it->second) {
           const Entry* se = src.find(t.src_rank, t.tensor_index);
           if (!se) throw IntegrityError(missing(t.src_rank, t.tensor_index));
-          if (!se->view.contains(t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
+          if (!detail::holds(se, t.bounds)) throw IntegrityError("integrity: task bounds escape source view");
           const std::int64_t eb = m.element_bytes(m.tensors[t.tensor_index]);
           if (eb > B) throw IntegrityError("chunk_bounds: one element exceeds the staging budget");
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
           if (!de) throw IntegrityError(missing(t.dst_rank, t.tensor_index));
-          if (!de->view.contains(t.bounds)) throw IntegrityError(escapes("scatter_local", t.bounds, de->view));
+          if (!detail::holds(de, t.bounds)) throw IntegrityError(escapes("scatter_local", t.bounds, de->view));
           const std::int64_t n = t.bounds.element_count() * eb;
           if (t.is_local()) delta.local_copy_bytes += n;
           else delta.bytes_moved += n;
@@ -227,9 +229,11 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
         for (const auto& f : l.batches[static_cast<std::size_t>(r)]) {
           const std::uint64_t b = addr_of(x.buf) + f.off;
           if (pass == 0)
-            append_copy(xfer_descs_, addr_of(f.se->ptr), f.se->view, b, f.region, f.region, f.eb, static_cast<std::uint32_t>(r));
+            append_copy(xfer_descs_, addr_of(f.se->ptr) - static_cast<std::uint64_t>(f.se->flat_off), f.se->view, b,
+                        f.region, f.region, f.eb, static_cast<std::uint32_t>(r));
           else
-            append_copy(xfer_descs_, b, f.region, addr_of(f.de->ptr), f.de->view, f.region, f.eb, static_cast<std::uint32_t>(r));
+            append_copy(xfer_descs_, b, f.region, addr_of(f.de->ptr) - static_cast<std::uint64_t>(f.de->flat_off),
+                        f.de->view, f.region, f.eb, static_cast<std::uint32_t>(r));
         }
       }
       const std::uint64_t end = assign_items(xfer_descs_, first, item, item_bytes);

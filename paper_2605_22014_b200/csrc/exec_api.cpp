@@ -68,6 +68,8 @@ void RecordingTransport::on_device_frame(int layer, int src, int dst, std::uint3
 // ------------------------------------------------------------- shard store
 
 ShardStore ShardStore::allocate(const ModelSpec& model, const ParallelConfig& config) {
+  if (config.flat_buckets())  // the reference's store holds whole views (shard_store.hpp:21-24)
+    throw std::invalid_argument("ShardStore: flat-bucket configs hold element ranges; use the rs_* C ABI stores");
   ShardStore s;
   s.model_ = model;
   s.config_ = config;

@@ -12,6 +12,7 @@
 // reference's brute-force oracle (planner.cpp:194-303), but counts coverage on
 // a coordinate-compressed grid of cells instead of per element.
 #include <algorithm>
+#include <map>
 #include <stdexcept>
 
 #include "reshard_b200/reshard.hpp"
@@ -36,6 +37,89 @@ bool same_local_layout(const ShardView& owner_old, const ShardView& owner_new,
     stride_new *= owner_new.dim(k).length();
   }
   return off_old == off_new && strides_match;
+}
+
+// Local layout of a held region: the owner block and the flat offset of its
+// first held element (flat-bucket shards hold a sub-range of the block).
+bool same_local_layout_flat(const ShardView& block_old, std::int64_t lo_old, const ShardView& block_new,
+                            std::int64_t lo_new, const ShardView& region) {
+  return block_old == block_new && lo_old == lo_new && same_local_layout(block_old, block_new, region);
+}
+
+// Extension: a DP-sharded tensor where either config uses
+// Megatron's flat buckets.  What each rank holds is a list of boxes
+// (held_boxes); every destination box is tiled by every source box of the
+// old TP blocks: DP-sharded sources are unique per element, replicated
+// sources come from dp index 0 (the reference's choice, planner.cpp:154-171).
+// Self-held boxes become carryovers when the block and the flat offset are
+// unchanged, local tasks otherwise.
+void plan_flat_buckets(TransferPlan& plan, const ModelSpec& model, std::uint32_t ti, const ParallelConfig& c_old,
+                       const ParallelConfig& c_new, std::int64_t& pairs) {
+  const TensorSpec& t = model.tensors[ti];
+  const std::int64_t ebytes = model.element_bytes(t);
+  const int s_old = c_old.stage_of_layer(t.layer), s_new = c_new.stage_of_layer(t.layer);
+  const bool old_sharded = c_old.distributed_optimizer();
+  auto pos_rank = [](const ParallelConfig& c, int tp_i, int dp_i, int s) {
+    return c.ranks()[static_cast<std::size_t>(tp_i + c.tp() * (dp_i + c.dp() * s))];
+  };
+  auto flat_lo = [&](const ParallelConfig& c, int rank) -> std::int64_t {
+    auto r = bucket_range(model, ti, c, rank);
+    return r ? r->first : 0;
+  };
+  // source holders in (tp, dp) order: every dp index when the old state is
+  // DP-sharded, else dp 0 only.  A tensor without a TP axis is held whole by
+  // every TP index, but each TP index's buckets cut it at different places
+  // (the other tensors' TP-local sizes differ), so it is sourced from TP
+  // index 0's holders only
+  struct Source {
+    int rank, tp_i, dp_i;
+    std::vector<ShardView> boxes;
+  };
+  std::vector<Source> sources;
+  for (int otp = 0; otp < (t.tp_shard_axis ? c_old.tp() : 1); ++otp)
+    for (int odp = 0; odp < (old_sharded ? c_old.dp() : 1); ++odp) {
+      const int r = pos_rank(c_old, otp, odp, s_old);
+      auto boxes = held_boxes(model, ti, c_old, r);
+      if (!boxes.empty()) sources.push_back({r, otp, odp, std::move(boxes)});
+    }
+  for (int dtp = 0; dtp < c_new.tp(); ++dtp)
+    for (int ddp = 0; ddp < c_new.dp(); ++ddp) {
+      const int dst = pos_rank(c_new, dtp, ddp, s_new);
+      const auto dst_boxes = held_boxes(model, ti, c_new, dst);
+      if (dst_boxes.empty()) continue;
+      const auto v_dst = view(t, c_new, dst);
+      const std::int64_t lo_dst = flat_lo(c_new, dst);
+      // the destination's own old holding of this tensor, if any
+      std::optional<ShardView> v_held;
+      int held_tp = -1, held_dp = -1;
+      std::int64_t lo_held = 0;
+      if (c_old.contains(dst)) {
+        const RankCoord oc = c_old.coord_of(dst);
+        if (oc.pp == s_old) {
+          v_held = view(t, c_old, dst);
+          held_tp = oc.tp;
+          held_dp = oc.dp;
+          lo_held = flat_lo(c_old, dst);
+        }
+      }
+      for (const ShardView& db : dst_boxes)
+        for (const Source& src : sources)
+          for (const ShardView& sb : src.boxes) {
+            ++pairs;
+            auto region = intersect(db, sb);
+            if (!region) continue;
+            const std::int64_t bytes = region->element_count() * ebytes;
+            const bool self = v_held && held_tp == src.tp_i && (!old_sharded || held_dp == src.dp_i);
+            if (self) {
+              if (same_local_layout_flat(*v_held, lo_held, *v_dst, lo_dst, *region))
+                plan.carryover_by_layer[t.layer].push_back({ti, t.layer, dst, *region, bytes});
+              else
+                plan.tasks_by_layer[t.layer].push_back({ti, t.layer, dst, dst, *region, bytes});
+              continue;
+            }
+            plan.tasks_by_layer[t.layer].push_back({ti, t.layer, src.rank, dst, *region, bytes});
+          }
+    }
 }
 
 }  // namespace
@@ -88,6 +172,11 @@ TransferPlan compute_transfer_plan(const ParallelConfig& c_old, const ParallelCo
         if (auto b = tp_block(axis_len, tp_old, i)) old_blocks.push_back({i, *b});
     } else {
       old_blocks.push_back({-1, {0, 1}});
+    }
+
+    if (t.dp_shard_axis && (c_old.flat_buckets() || c_new.flat_buckets())) {
+      plan_flat_buckets(plan, model, ti, c_old, c_new, pairs);
+      continue;
     }
 
     // Extension (distributed optimizer): DP-sharded views split the TP block
@@ -284,18 +373,30 @@ std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelCon
     if (to_model[pi] < 0) complain("plan references unknown tensor " + plan.tensor_ids[pi]);
   }
 
-  std::vector<ShardView> marked;
+  // does the union of `held` contain `region` (held boxes are disjoint)?
+  auto inside = [](const std::vector<ShardView>& held, const ShardView& region) {
+    if (held.size() == 1) return held.front().contains(region);
+    std::int64_t n = 0;
+    for (const auto& h : held)
+      if (auto x = intersect(h, region)) n += x->element_count();
+    return n == region.element_count();
+  };
+  std::vector<ShardView> marked, part;
   for (std::size_t mi = 0; mi < model.tensors.size(); ++mi) {
     const TensorSpec& t = model.tensors[mi];
-    const auto dst_views = owners(t, c_new);
-    const auto src_views = owners(t, c_old);
+    const auto ti = static_cast<std::uint32_t>(mi);
+    // what every rank holds: its view, or the boxes of its flat-bucket range
+    std::map<int, std::vector<ShardView>> dst_held, src_held;
+    for (const auto& [r, v] : owners(t, c_new)) dst_held[r] = held_boxes(model, ti, c_new, r);
+    for (const auto& [r, v] : owners(t, c_old)) src_held[r] = held_boxes(model, ti, c_old, r);
     const auto tasks = plan.tasks_by_layer.find(t.layer);
     const auto keeps = plan.carryover_by_layer.find(t.layer);
 
-    for (const auto& [dst, v_dst] : dst_views) {
+    for (const auto& [dst, held] : dst_held) {
+      if (held.empty()) continue;  // an empty flat-bucket range
       marked.clear();
       auto mark = [&](const ShardView& region, const char* what) {
-        if (!v_dst.contains(region)) {
+        if (!inside(held, region)) {
           complain(std::string(what) + " for tensor " + t.tensor_id + " rank " +
                    std::to_string(dst) + " escapes destination view");
           return;
@@ -309,11 +410,11 @@ std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelCon
             complain("empty task for tensor " + t.tensor_id);
             continue;
           }
-          auto s = src_views.find(task.src_rank);
-          if (s == src_views.end())
+          auto s = src_held.find(task.src_rank);
+          if (s == src_held.end() || s->second.empty())
             complain("task source rank " + std::to_string(task.src_rank) + " owns nothing of tensor " +
                      t.tensor_id);
-          else if (!s->second.contains(task.bounds))
+          else if (!inside(s->second, task.bounds))
             complain("task bounds escape source view for tensor " + t.tensor_id + " src " +
                      std::to_string(task.src_rank));
           mark(task.bounds, "task");
@@ -322,14 +423,22 @@ std::vector<std::string> verify_plan(const TransferPlan& plan, const ParallelCon
       if (keeps != plan.carryover_by_layer.end()) {
         for (const auto& k : keeps->second) {
           if (k.rank != dst || to_model.at(k.tensor_index) != static_cast<int>(mi)) continue;
-          auto s = src_views.find(k.rank);
-          if (s == src_views.end() || !s->second.contains(k.bounds))
+          auto s = src_held.find(k.rank);
+          if (s == src_held.end() || !inside(s->second, k.bounds))
             complain("carryover not resident in old view for tensor " + t.tensor_id + " rank " +
                      std::to_string(k.rank));
           mark(k.bounds, "carryover");
         }
       }
-      const auto [gaps, overlaps] = cover_counts(v_dst, marked);
+      std::int64_t gaps = 0, overlaps = 0;
+      for (const auto& h : held) {  // held boxes are disjoint: count each on its own
+        part.clear();
+        for (const auto& m : marked)
+          if (auto x = intersect(h, m)) part.push_back(*x);
+        const auto [g, o] = cover_counts(h, part);
+        gaps += g;
+        overlaps += o;
+      }
       if (gaps)
         complain("coverage gap: tensor " + t.tensor_id + " rank " + std::to_string(dst) + " missing " +
                  std::to_string(gaps) + " elements");

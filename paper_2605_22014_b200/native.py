@@ -20,7 +20,7 @@ RS_MODE_DIRECT, RS_MODE_STAGED, RS_MODE_XFER = 0, 1, 2
 RS_TRAFFIC_RELAY = 1
 
 EXPORTS = [
-    "rs_last_error", "rs_version", "rs_validate_config", "rs_view", "rs_plan_compute",
+    "rs_last_error", "rs_version", "rs_validate_config", "rs_view", "rs_view_range", "rs_plan_compute",
     "rs_plan_read", "rs_plan_write", "rs_plan_summary", "rs_plan_verify", "rs_plan_destroy",
     "rs_chunk_bounds", "rs_engine_create", "rs_engine_destroy", "rs_store_layout",
     "rs_store_alloc", "rs_store_bind", "rs_store_ptr", "rs_store_bytes", "rs_store_entries",
@@ -57,7 +57,7 @@ class Config(C.Structure):
     _fields_ = [("generation_id", C.c_uint64), ("tp", C.c_int32), ("pp", C.c_int32),
                 ("dp", C.c_int32), ("num_ranks", C.c_int32), ("ranks", C.POINTER(C.c_int32)),
                 ("layer_stage", C.POINTER(C.c_int32)), ("distributed_optimizer", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("dist_opt_bucket_elems", C.c_int32)]
 
 
 class PlanOptions(C.Structure):
@@ -156,6 +156,7 @@ def lib() -> C.CDLL:
         L.rs_version.restype = C.c_char_p
         L.rs_validate_config.argtypes = [C.c_char_p, P(Config), C.c_char_p, SZ, P(SZ), P(I32)]
         L.rs_view.argtypes = [C.c_char_p, P(Config), I32, I32, P(I64), P(I64), P(I32)]
+        L.rs_view_range.argtypes = [C.c_char_p, P(Config), I32, I32, P(I64), P(I64), P(I32)]
         L.rs_plan_compute.argtypes = [C.c_char_p, P(Config), P(Config), P(PlanOptions), P(VP)]
         L.rs_plan_read.argtypes = [C.c_char_p, C.c_char_p, P(VP)]
         L.rs_plan_write.argtypes = [VP, C.c_char_p, SZ, P(SZ)]
@@ -215,6 +216,6 @@ def config_struct(cfg, num_layers: int) -> Config:
         stage = (C.c_int32 * max(1, num_layers))(*cfg.layer_stage)
     s = Config(cfg.gen, cfg.tp, cfg.pp, cfg.dp, len(cfg.ranks), ranks,
                C.cast(stage, C.POINTER(C.c_int32)) if stage is not None else None,
-               int(getattr(cfg, "dist_opt", False)), 0)
+               int(getattr(cfg, "dist_opt", 0)), int(getattr(cfg, "bucket_elems", 0)))
     s._keep = (ranks, stage)
     return s

@@ -142,6 +142,15 @@ def view(model: ModelSpec, tensor_index: int, config: ParallelConfig, rank: int)
     return [(lo[i], hi[i]) for i in range(nd)] if present.value else None
 
 
+def view_range(model: ModelSpec, tensor_index: int, config: ParallelConfig, rank: int):
+    """(lo, hi, flat): the element range of the rank's view it holds, row
+    major (flat-bucket distributed optimizer); flat False = the whole view."""
+    lo = C.c_int64(0); hi = C.c_int64(0); flat = C.c_int32(0)
+    N.check(N.lib().rs_view_range(model.to_text().encode(), N.config_struct(config, model.num_layers),
+                                  tensor_index, rank, C.byref(lo), C.byref(hi), C.byref(flat)))
+    return lo.value, hi.value, bool(flat.value)
+
+
 def chunk_bounds(lo: Sequence[int], hi: Sequence[int], max_bytes: int, bpe: int):
     nd = len(lo)
     cap = 1 << 16

@@ -112,7 +112,10 @@ class ParallelConfig:
     dp: int
     ranks: List[int]
     layer_stage: Optional[List[int]] = None  # None: default ceil split
-    dist_opt: bool = False  # extension: DP-shard tensors that declare a dp_axis (ZeRO-1)
+    # extension: DP-shard the tensors that declare a dp_axis (ZeRO-1):
+    # 0/False off, 1/True per-tensor dim chunks, 2 Megatron flat buckets
+    dist_opt: int = 0
+    bucket_elems: int = 0  # flat buckets: bucket size in elements (0: max(40M, 1M x dp))
 
     @property
     def world(self) -> int:
@@ -263,6 +266,10 @@ def baseline_case(name: str):
         # optimizer re-partitioning fp32 master/m/v across the 2 DP ranks (extension)
         c_new = dataclasses.replace(iota_config(2, 4, 1, 2), dist_opt=True)
         return llama("llama3-8b", zero=True), iota_config(1, 8, 1, 1), c_new
+    if name == "c3zb":  # the same with Megatron's flat-bucket distributed optimizer layout:
+        # DP ranks hold contiguous ranges of 40M-element buckets (extension)
+        c_new = dataclasses.replace(iota_config(2, 4, 1, 2), dist_opt=2)
+        return llama("llama3-8b", zero=True), iota_config(1, 8, 1, 1), c_new
     if name == "c4":  # Llama-2-13B TP2PP4 -> TP4PP2 with uneven 21/19 split
         spec = llama("llama2-13b")
         return spec, iota_config(1, 2, 4, 1), iota_config(2, 4, 2, 1, layer_stage=[0] * 21 + [1] * 19)
@@ -279,9 +286,9 @@ def sliced_case(name: str, num_layers: int):
     if name == "c1":
         spec = gpt2_124m(num_layers)
     else:
-        arch = {"c2": "llama2-7b", "c3": "llama3-8b", "c3z": "llama3-8b", "c4": "llama2-13b",
+        arch = {"c2": "llama2-7b", "c3": "llama3-8b", "c3z": "llama3-8b", "c3zb": "llama3-8b", "c4": "llama2-13b",
                 "c5": "llama2-7b", "c5b": "llama2-7b"}[name]
-        spec = llama(arch, num_layers, zero=name == "c3z")
+        spec = llama(arch, num_layers, zero=name in ("c3z", "c3zb"))
     c_old = dataclasses.replace(c_old, layer_stage=None)
     c_new = dataclasses.replace(c_new, layer_stage=None)
     if name == "c4" and num_layers >= 3:
@@ -379,3 +386,21 @@ def random_zero_case(seed: int):
 def iter_random_zero_cases(n: int, base_seed: int = 31337) -> Iterable[tuple]:
     for i in range(n):
         yield (base_seed + i,) + random_zero_case(base_seed + i)
+
+
+def random_flat_case(seed: int):
+    """A random pair where either config may use the Megatron flat-bucket
+    distributed optimizer (dist_opt 2) with a small random bucket size, so
+    buckets close mid-stage and DP ranges cut tensors mid-row (extension)."""
+    spec, c_old, c_new = random_zero_case(seed)
+    rng = random.Random(seed ^ 0xF1A7)
+    modes = (0, 1, 2, 2)
+    c_old = dataclasses.replace(c_old, dist_opt=rng.choice(modes), bucket_elems=rng.choice((0, 64, 200, 777, 5000)))
+    c_new = dataclasses.replace(c_new, dist_opt=rng.choice(modes[1:]) if c_old.dist_opt != 2 else rng.choice(modes),
+                                bucket_elems=rng.choice((0, 64, 200, 777, 5000)))
+    return spec, c_old, c_new
+
+
+def iter_random_flat_cases(n: int, base_seed: int = 4242) -> Iterable[tuple]:
+    for i in range(n):
+        yield (base_seed + i,) + random_flat_case(base_seed + i)

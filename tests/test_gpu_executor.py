@@ -8,6 +8,8 @@ and (b) the analytic gather-reslice pattern via the verify kernel.  Bit-exact:
 the tolerance is zero mismatched bytes.
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -710,6 +712,57 @@ def test_stream_lane_kernels_bitexact(ring_kernel, stages, slot_kib, golden, ora
     plan = R.compute_transfer_plan(co, cn, sp)
     rep = R.execute_plan(plan, eng)
     assert rep["ok"] and rep["ring_kernel"] == ring_kernel, rep
+    _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 20)
+    for (ti, rank), arr in want.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)
+    eng.close()
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged", "xfer-free"])
+def test_flat_bucket_distributed_optimizer_bitexact(mode, oracle_c):
+    """Megatron flat-bucket distributed optimizer on the device (extension,
+    SURVEY §8(f)1): flat-bucket shards hold element ranges of their TP block,
+    addressed through the block's strides from an offset origin.  Random
+    pairs (small buckets: ranges cut mid-row) vs the C oracle's bytes; a
+    4-layer slice of BASELINE config 3 with Megatron's layout (c3zb, TP8 ->
+    TP4DP2, the default 40M-element buckets) vs the analytic pattern, and its
+    16 B-aligned mini version through the STAGED stream lanes."""
+    kw = {"lanes_per_link": 1}
+    m = "direct" if mode == "xfer-free" else mode
+    if mode == "xfer-free":
+        kw["copy_kernel"] = 15  # the LDG8 warp copy over flat shards
+    n = 0
+    for seed, sp, co, cn in specs.iter_random_flat_cases(60):
+        if co.dist_opt != 2 and cn.dist_opt != 2:
+            continue
+        eng = make_engine(sp, co, cn, m, 1 << 16, **kw)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        rep = R.execute_plan(plan, eng)
+        orep, ostore = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 16)
+        assert rep["ok"] and orep["ok"], (seed, rep["error"])
+        assert rep["bytes_moved"] == orep["bytes_moved"], seed
+        for (ti, rank), want in ostore.entries.items():
+            assert np.array_equal(eng.read(RS_DST, rank, ti), want), (seed, ti, rank)
+        assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+        eng.close()
+        n += 1
+    assert n >= 20
+    sp, co, cn = specs.sliced_case("c3zb", 4)
+    eng = make_engine(sp, co, cn, m, 256 << 20, **({} if mode == "xfer-free" else {}))
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and eng.verify_pattern(RS_DST, SEED)[0] == 0
+    assert eng.verify_pattern(RS_SRC, SEED)[0] == 0  # the source is untouched
+    eng.close()
+    sp = specs.llama("llama-mini-a16", 4, zero=True)
+    co = dataclasses.replace(specs.iota_config(1, 2, 2, 2), dist_opt=2, bucket_elems=100_000)
+    cn = dataclasses.replace(specs.iota_config(2, 4, 1, 2), dist_opt=2, bucket_elems=250_000)
+    eng = make_engine(sp, co, cn, m, 1 << 20, **kw)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"], rep
+    if mode == "staged":
+        assert rep["ring_kernel"] == 2, rep  # aligned flat shards run the TMA stream lanes
     _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 20)
     for (ti, rank), arr in want.entries.items():
         assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)

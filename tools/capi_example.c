@@ -33,7 +33,7 @@ static rs_config iota(uint64_t gen, int tp, int pp, int dp, int32_t* ranks) {
   c.ranks = ranks;
   c.layer_stage = NULL;
   c.distributed_optimizer = 0;
-  c.reserved = 0;
+  c.dist_opt_bucket_elems = 0;
   return c;
 }
 

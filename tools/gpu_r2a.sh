@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 session A: GPU suite, smoke, default bench (N=1, DIRECT + STAGED sub-object), launch list.
-OUT=gpurun_out/r2a
+OUT=gpurun_out/${1:-r2a}
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt 2>&1
 nproc >> $OUT/gpu.txt
