@@ -413,6 +413,16 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
         staging = int(t[0])
     total = plan.summary()["total_bytes"]
     roof = roofline(traffic, step_ms, pk["hbm_gbs"], pk["nvlink_gbs"])
+    traffic_note = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if world == 1 and not args.profile_layers and os.path.exists(tp):
+        with open(tp) as f:  # ncu single-pass DRAM bytes of this launch (same kernel, same plan)
+            st = json.load(f).get("staged", {})
+        if st.get("kernel") == kernel_name("staged", rep) and st.get("remote_bytes") == plan.summary()["remote_bytes"]:
+            traffic_note = {"lane_kernel_dram_bytes": st["lane_kernel_dram_read_bytes"] + st["lane_kernel_dram_write_bytes"],
+                            "lane_kernel_algorithmic_bytes": st["lane_algorithmic_bytes_per_launch"],
+                            "local_copy_dram_bytes": st["local_copy_dram_bytes"],
+                            "source": "profiles/r2/launches_c2_full.csv (ncu, single pass)"}
     out = {"ms_per_step": round(step_ms, 4), "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
            "frac": roof["frac"], "bound": roof["bound"], "roofline_ms": roof["roofline_ms"],
            "peak_staging_bytes": staging, "staging_budget_bytes": args.staging_bytes,
@@ -420,6 +430,8 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
            "ring_same_slot": rep["ring_same_slot"], "relay": bool(relay), "relay_routes": rep["relay_routes"],
            "gpu_launches": launches, "clocks": clocks,
            "wall_s": round(wall, 3), "dst_pattern_mismatches": int(bad)}
+    if traffic_note:
+        out["traffic"] = traffic_note
     eng.close()
     return out
 
