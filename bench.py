@@ -600,12 +600,19 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     """Same handoff through rs_execute_host with HOST shard stores: every step
     copies all (this process's) source shards H2D from pinned memory and all
     destination shards D2H, layer-pipelined.  Host RAM cannot hold a second
-    94 GB store next to the pinned source (196 GB box), so destination shards
-    land in a 4 GiB pinned window that successive shards overwrite; every
-    byte still crosses PCIe.  On this box H2D and D2H each run ~55 GB/s and
-    ~96 GB/s combined when the engine merges back-to-back shards into large
-    copies (tools/e2e_probe2.py): the e2e step is host-transfer bound, the
-    reshard kernel is ~1.5 % of it."""
+    94 GB store next to the pinned source (196 GB box), so the last
+    destination shards in store order (up to 4 GiB) get their own pinned
+    region and every other destination shard lands in a 4 GiB pinned window
+    that successive shards overwrite; every byte still crosses PCIe.  After
+    the timed steps the dedicated host region is compared byte for byte with
+    the device destination, which is pattern-verified (the host copy of the
+    last layers is checked at full size, not just the device side).  On this
+    box H2D and D2H each run ~55 GB/s and ~96 GB/s combined when the engine
+    merges back-to-back shards into large copies (tools/e2e_probe2.py): the
+    e2e step is host-transfer bound, the reshard kernel is ~1.5 % of it."""
+    import ctypes
+
+    import numpy as np
     import torch
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
     from paper_2605_22014_b200.reshard import PinnedBuffer
@@ -618,6 +625,7 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     d2h = sum(n for (_, _, n), l in zip(dst, dst_local) if l)
     host_src = PinnedBuffer(max(h2d, 1))
     window = PinnedBuffer(4 << 30)
+    keep_cap = 4 << 30
     # the host source store holds the device source state, so the e2e output
     # is checkable against the analytic pattern afterwards
     off, src_ptrs = 0, []
@@ -628,10 +636,26 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
         src_ptrs.append(host_src.ptr + off)
         eng.read_to(RS_SRC, r, ti, host_src.ptr + off, n)
         off += n
-    dst_ptrs, woff = [], 0
-    for (_, _, n), l in zip(dst, dst_local):
+    # the last destination shards in store order (up to keep_cap bytes) keep
+    # their own host region: unique addresses, whatever order the copies run in
+    kept, kept_bytes = set(), 0
+    for k in range(len(dst) - 1, -1, -1):
+        if not dst_local[k]:
+            continue
+        if kept_bytes + dst[k][2] > keep_cap:
+            break
+        kept.add(k)
+        kept_bytes += dst[k][2]
+    keep = PinnedBuffer(max(kept_bytes, 1))
+    dst_ptrs, woff, koff, checks = [], 0, 0, []
+    for k, ((ti, r, n), l) in enumerate(zip(dst, dst_local)):
         if not l:
             dst_ptrs.append(0)
+            continue
+        if k in kept:
+            dst_ptrs.append(keep.ptr + koff)
+            checks.append((ti, r, n, keep.ptr + koff))
+            koff += n
             continue
         if woff + n > window.nbytes:
             woff = 0
@@ -650,20 +674,29 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
         times.append(time.perf_counter() - t0)
         ok &= rep["ok"]
     bad = eng.verify_pattern(RS_DST, SEED)[0]
+    host_bad = host_checked = 0
+    for ti, r, n, ptr in checks:  # host bytes of the kept layers == the (pattern-verified) device bytes
+        host = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), shape=(n,))
+        dev = eng.read(RS_DST, r, ti)
+        host_bad += int(np.count_nonzero(host != dev))
+        host_checked += n
     host_src.free()
     window.free()
+    keep.free()
     mean = statistics.mean(times)
     if world > 1:
-        t = torch.tensor([float(h2d), float(d2h), float(bad)], dtype=torch.float64)
+        t = torch.tensor([float(h2d), float(d2h), float(bad), float(host_bad), float(host_checked)],
+                         dtype=torch.float64)
         torch.distributed.all_reduce(t)
-        h2d, d2h, bad = int(t[0]), int(t[1]), int(t[2])
+        h2d, d2h, bad, host_bad, host_checked = (int(x) for x in t)
     return {"value": round(total / mean / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(mean, 4),
             "path": "rs_execute_host (C ABI, host shard stores)",
+            "host_dst_checked_bytes": host_checked, "host_dst_mismatches": host_bad,
             "bound": ("host<->device transfer: 188.7 GB per step over PCIe; measured ceiling "
                       "H2D 55.5 + D2H 55.2 GB/s alone, ~96 GB/s combined concurrent with merged copies "
                       "(profiles/r1/e2e_probe2.json)"),
-            "ok": bool(ok and bad == 0)}
+            "ok": bool(ok and bad == 0 and host_bad == 0)}
 
 
 def main() -> None:
@@ -680,7 +713,7 @@ def main() -> None:
     ap.add_argument("--placement", default="iota", choices=["iota", "searched"],
                     help="destination rank list: BASELINE iota, or rs_plan_placement's choice")
     ap.add_argument("--ring-slot-kib", type=int, default=0, help="STAGED ring slot cap (0: default, -1: none)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-staged", action="store_true", help="skip the STAGED sub-object of a DIRECT run")

@@ -65,11 +65,13 @@ def run(case, mode, layers=None):
             "ms": round(mean, 3), "reshard_GBps": round(s["total_bytes"] / mean / 1e6, 1),
             "hbm_frac": round(algo / (mean / 1e3) / 1e9 / HBM, 4),
             "hbm_frac_vs_dram_ring": round(ring / (mean / 1e3) / 1e9 / HBM, 4) if mode == "staged" else None,
-            "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad}
+            "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad,
+            "kernel": ({2: "rs_stream_lane_kernel", 3: "rs_stream_ws_kernel"}.get(rep.get("ring_kernel"), "rs_exchange_kernel")
+                       if mode == "staged" else f"RS_COPY {rep.get('copy_kernel')}")}
 
 
 def main():
-    for case in ("c1", "c2", "c3", "c3z", "c4", "c5", "c5b"):
+    for case in ("c1", "c2", "c3", "c3z", "c3zb", "c4", "c5", "c5b"):
         for mode in ("direct", "staged"):
             r = None
             for layers in (None, 16, 8):
