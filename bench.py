@@ -413,6 +413,20 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
         staging = int(t[0])
     total = plan.summary()["total_bytes"]
     roof = roofline(traffic, step_ms, pk["hbm_gbs"], pk["nvlink_gbs"])
+    # One-GPU ring bound from measured transfer shapes (profiles/r2/l2_probe.jsonl,
+    # tools/l2_probe.py: 1-warp CTAs, 2 x 16 KB TMA stages, 6 per SM): a remote
+    # byte is one sender transfer (HBM -> L2 slot, 9011 GB/s of read + write)
+    # plus one receiver transfer (L2 slot -> HBM, 9653 GB/s) on the same GPU;
+    # local bytes are one DIRECT copy (6929 GB/s, the TMA copy kernel's rate in
+    # this bench).  Additive: both halves share one memory system.
+    ring_bound = None
+    if world == 1:
+        summ_ = plan.summary()
+        ring_bound_s = (2 * summ_["remote_bytes"] / 9010.7e9 + 2 * summ_["remote_bytes"] / 9652.9e9
+                        + 2 * (summ_["local_bytes"] + summ_["carryover_bytes"]) / 6928.9e9)
+        ring_bound = {"ms": round(ring_bound_s * 1e3, 3), "frac": round(ring_bound_s * 1e3 / step_ms, 4),
+                      "source": "profiles/r2/l2_probe.jsonl (sender HBM->L2 9011 GB/s, receiver L2->HBM 9653 GB/s, "
+                                "r+w bytes, 6 CTAs/SM) + the DIRECT copy rate for local bytes"}
     traffic_note = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if world == 1 and not args.profile_layers and os.path.exists(tp):
@@ -432,6 +446,8 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
            "wall_s": round(wall, 3), "dst_pattern_mismatches": int(bad)}
     if traffic_note:
         out["traffic"] = traffic_note
+    if ring_bound:
+        out["one_gpu_ring_bound"] = ring_bound
     eng.close()
     return out
 
