@@ -170,15 +170,26 @@ def dist_env():
     return rank, world, local
 
 
-def workload(n_gpus: int, layers: int = 0):
+CASES = {  # BASELINE.json configs (specs.baseline_case); c2 is the headline workload
+    "c1": "c1: GPT-2 124M fp32 p + m + v, TP2.PP2.DP2 -> TP4.PP2.DP1 (8 ranks)",
+    "c2": "c2: Llama-2-7B bf16 params + fp32 master/m/v, TP4.PP2.DP1 (8 ranks) -> TP2.PP2.DP1 (4 ranks)",
+    "c3": "c3: Llama-3-8B TP8 -> TP4.DP2 (replicated DP state)",
+    "c3z": "c3z: Llama-3-8B TP8 -> TP4.DP2, distributed optimizer (per-tensor DP chunks)",
+    "c3zb": "c3zb: Llama-3-8B TP8 -> TP4.DP2, distributed optimizer (Megatron flat buckets)",
+    "c4": "c4: Llama-2-13B TP2.PP4 -> TP4.PP2, uneven 21/19 stage migration",
+    "c5": "c5: Llama-2-7B scale-out TP2.PP2 (4) -> TP4.PP2 (8)",
+    "c5b": "c5b: Llama-2-7B DP scale-out TP2.PP2 (4) -> TP2.PP2.DP2 (8)",
+}
+
+
+def workload(n_gpus: int, layers: int = 0, case: str = "c2"):
     from paper_2605_22014_b200 import specs
-    if layers:  # profiling-only slice (never a bench value)
-        sp, co, cn = specs.sliced_case("c2", layers)
-        return sp, co, cn, f"c2 PROFILING SLICE ({layers} layers)"
-    sp, co, cn = specs.baseline_case("c2")
-    desc = ("c2: Llama-2-7B bf16 params + fp32 master/m/v, TP4.PP2.DP1 (8 ranks) -> "
-            "TP2.PP2.DP1 (4 ranks), all logical ranks on one B200 (intra-device relayout)")
-    return sp, co, cn, desc
+    if layers:  # profiling / dry-run slice (never the headline value)
+        sp, co, cn = specs.sliced_case(case, layers)
+        return sp, co, cn, (f"{case} SLICE ({layers} layers): " + CASES[case].split(": ", 1)[1]
+                            + ", all logical ranks on one B200 (intra-device relayout)")
+    sp, co, cn = specs.baseline_case(case)
+    return sp, co, cn, CASES[case] + ", all logical ranks on one B200 (intra-device relayout)"
 
 
 def cpu_sample(layers: int):
@@ -469,7 +480,7 @@ def ours(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    sp, co, cn, desc = workload(args.gpus, args.profile_layers)
+    sp, co, cn, desc = workload(args.gpus, args.profile_layers, args.case)
     if args.placement == "searched":
         # placement-aware destination rank list (rs_plan_placement); changes the
         # plan (more self-held bytes), so it is a different workload: labelled
@@ -557,7 +568,8 @@ def ours(args) -> None:
                 roof["traffic"] = t.get("rs_copy_kernel_dram_bytes_per_launch")
                 roof["traffic_source"] = t.get("source")
 
-    line = {"metric": METRIC, "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
+    metric = METRIC if args.case == "c2" else f"reshard GB/s ({CASES[args.case].split(':')[0]} handoff; not the headline)"
+    line = {"metric": metric, "value": round(total / (step_ms / 1e3) / 1e9, 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(step_ms, 4), "handoff_ms": round(step_ms, 4),
             "higher_is_better": HIGH_IS_GOOD, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
@@ -589,7 +601,7 @@ def ours(args) -> None:
                                      "processes are never co-resident; set RS_BENCH_STAGED=1 to run it anyway"
                           if same_device else "--no-staged"}
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.case == "c2":
         cpu_layers = int(os.environ.get("RS_BENCH_CPU_SAMPLE_LAYERS", "4"))  # ~12 s of single-thread work
         res = run_reference_cpu(1, cpu_layers, 1, 0, args.staging_bytes)
         if res is not None:
@@ -734,6 +746,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-staged", action="store_true", help="skip the STAGED sub-object of a DIRECT run")
     ap.add_argument("--profile-layers", type=int, default=0, help="profiling slice (not a bench value)")
+    ap.add_argument("--case", default="c2", choices=sorted(CASES),
+                    help="BASELINE config (default c2, the metric's config); others for dry runs / scaling studies")
     args = ap.parse_args()
     if args.strict and args.mode == "xfer":
         ap.error("--strict applies to --mode direct / staged (xfer rounds are host-driven)")

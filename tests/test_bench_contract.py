@@ -106,3 +106,33 @@ def test_bench_multi_process_line(n):
         assert st["dst_pattern_mismatches"] == 0 and st["within_budget"] and st["kernel"] in ("rs_exchange_kernel", "rs_stream_lane_kernel")
     else:
         assert "skipped" in st
+
+
+@pytest.mark.gpu
+def test_bench_relay_line_c5b_slice():
+    """--case c5b --mode staged at N=4 (four processes on this GPU, a 4-layer
+    slice): the DP scale-out runs relay chains (relay_routes > 0), the
+    roofline is computed from the relay traffic, and every destination byte
+    checks out."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = {**os.environ, "RS_BENCH_SAME_DEVICE": "1"}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", "29644", os.path.join(ROOT, "bench.py"),
+           "--gpus", "4", "--steps", "2", "--warmup", "3", "--profile-layers", "4", "--case", "c5b",
+           "--mode", "staged", "--no-e2e", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-4000:])
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    assert d["correct"]["dst_pattern_mismatches"] == 0
+    assert d["config"]["relay"] is True and d["config"]["relay_routes"] > 0
+    from paper_2605_22014_b200 import reshard as R
+    from paper_2605_22014_b200 import specs
+    sp, co, cn = specs.sliced_case("c5b", 4)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    so = [r * 4 // 8 for r in co.ranks]
+    sn = [r * 4 // 8 for r in cn.ranks]
+    relay = R.plan_traffic(plan, co, so, cn, sn, 4, relay=True)
+    assert [g["out_GB"] for g in d["roofline"]["per_gpu"]] == [round(t[0] / 1e9, 3) for t in relay]
+    assert max(t[0] for t in relay) < max(t[0] for t in R.plan_traffic(plan, co, so, cn, sn, 4))
