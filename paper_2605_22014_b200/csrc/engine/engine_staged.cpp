@@ -96,7 +96,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   std::map<std::pair<int, std::vector<int>>, int> route_id;
   if (opts_.relay && nslots_ > 1) {
     if (!geo.stream)
-      throw DomainError("relay: needs stream lanes (16 B aligned plans, ring_kernel != 1, strict_layers off)");
+      throw DomainError("relay: needs stream lanes (16 B aligned plans, ring_kernel 0 or 2)");
     const auto chains = reshard::relay_chains(
         plan, [&](int r) { return slot_in(src_slot, r); }, [&](int r) { return slot_in(dst_slot, r); });
     for (const auto& ch : chains) {
@@ -174,7 +174,10 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
     // stream lanes: the local copies run as their own launch beside the lane
     // kernel, so the lanes may take (almost) every co-resident CTA slot
-    double frac = geo.stream ? 0.98 : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
+    // (strict: the local copies run inside the lane launch -- leave them the
+    // remote : local byte share of the CTAs)
+    double frac = geo.stream ? (opts_.strict_layers ? 0.98 * std::clamp(1.0 / (1.0 + r), 0.5, 0.95) : 0.98)
+                             : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
     if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
     const int capacity = static_cast<int>(lane_capacity(0, geo.stream) * frac);
     int max_lanes = 64;  // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than 32)
@@ -721,15 +724,22 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
     // stream lanes need every frame this device touches to be bulk-copyable:
     // 16 B aligned runs of <= one 16 KB stage (the slot-side layout and the
     // flag protocol are the same for both lane kernels, so processes may differ)
-    p.stream_lanes = stream && !p.lanes.empty();
-    if (p.stream_lanes)
-      for (const auto& f : p.frames)
-        if (f.vec_log2 != 4 || f.row_bytes > 16384 || f.rows_per_item * f.row_bytes > 16384)
-          // the plan was bulk-copy eligible (stream_lanes_for), so only a
-          // caller-bound shard buffer off a 16 B boundary gets here; every
-          // process must run the geometry it computed, so this cannot fall back
-          throw DomainError("staged: stream lanes need 16 B aligned shard buffers (rs_store_bind); "
-                            "use ring_kernel = 1 (classic lanes) for this job");
+    // (strict: every slot launches -- its CTAs meet every layer barrier, and
+    // its local copies run inside the lane launch)
+    p.stream_lanes = stream && (!p.lanes.empty() || opts_.strict_layers);
+    auto bulk_ok = [](const rs_copy_desc& f) {
+      return f.vec_log2 == 4 && f.row_bytes <= 16384 && f.rows_per_item * f.row_bytes <= 16384;
+    };
+    // the plan was bulk-copy eligible (stream_lanes_for), so only a
+    // caller-bound shard buffer off a 16 B boundary fails here; every process
+    // must run the geometry it computed, so this cannot fall back
+    const bool frames_ok = std::all_of(p.frames.begin(), p.frames.end(), bulk_ok);
+    const bool local_ok = !opts_.strict_layers || std::all_of(p.local.begin(), p.local.end(), [](const rs_copy_desc& f) {
+      return f.vec_log2 == 4 && f.row_bytes <= 16384;  // (items are assigned at upload: 16 KB)
+    });
+    if (p.stream_lanes && !(frames_ok && local_ok))
+      throw DomainError("staged: stream lanes need 16 B aligned shard buffers (rs_store_bind); "
+                        "use ring_kernel = 1 (classic lanes) for this job");
   }
 }
 
@@ -740,7 +750,8 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
 // a job makes the same choice (the ring geometry depends on it).
 bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
   if (opts_.mode != RS_MODE_STAGED || opts_.ring_kernel == 1) return false;
-  if (opts_.strict_layers || (opts_.ring_discard & 8)) return false;  // barriers / warp-specialised: classic only
+  if (opts_.ring_discard & 8) return false;  // the warp-specialised control-warp design is classic only
+  if (opts_.strict_layers && opts_.ring_kernel == 3) return false;  // layer barriers: one-warp stream lanes only
   const Store& src = stores_[RS_SRC];
   const Store& dst = stores_[RS_DST];
   const auto& m = src.model;
@@ -759,6 +770,27 @@ bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
       for (const auto& d : scratch)
         if (d.vec_log2 != 4 || d.row_bytes > 16384) return false;
     }
+  if (opts_.strict_layers) {
+    // strict: the lane launch also runs the local tasks + carryovers through
+    // its shared-memory stages, so they must be bulk-copyable too
+    auto local_ok = [&](std::uint32_t ti, int src_rank, int dst_rank, const reshard::ShardView& box) {
+      const Entry* se = src.find(src_rank, ti);
+      const Entry* de = dst.find(dst_rank, ti);
+      if (!se || !de) return true;  // an integrity failure: reported by compile_staged
+      scratch.clear();
+      append_copy(scratch, static_cast<std::uint64_t>(-se->flat_off), se->view,
+                  static_cast<std::uint64_t>(-de->flat_off), de->view, box, m.element_bytes(m.tensors[ti]), 0);
+      for (const auto& d : scratch)
+        if (d.vec_log2 != 4 || d.row_bytes > 16384) return false;
+      return true;
+    };
+    for (const auto& kv : plan.tasks_by_layer)
+      for (const auto& t : kv.second)
+        if (!ringed(t) && !local_ok(t.tensor_index, t.src_rank, t.dst_rank, t.bounds)) return false;
+    for (const auto& kv : plan.carryover_by_layer)
+      for (const auto& k : kv.second)
+        if (!local_ok(k.tensor_index, k.rank, k.rank, k.bounds)) return false;
+  }
   return true;
 }
 
@@ -779,9 +811,10 @@ int Engine::run_stream_lanes(std::size_t d) {
   DeviceProgram& p = programs_[d];
   Device& dv = devices_[d];
   const int cap = lane_capacity(static_cast<int>(d), true);
-  if (p.ntx + p.nrx > cap)
+  if (p.ntx + p.nrx > cap || (opts_.strict_layers && p.ntx + p.nrx >= cap))
     throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) + " stream lanes exceed the co-resident CTA capacity " +
-                      std::to_string(cap) + "; lower lanes_per_link");
+                      std::to_string(cap) + (opts_.strict_layers ? " (strict: one CTA must stay for the local copies)" : "") +
+                      "; lower lanes_per_link");
   DeviceGuard g(dv.ordinal);
   int launches = 0;
   if (opts_.trace && p.d_trace.size())
@@ -797,7 +830,13 @@ int Engine::run_stream_lanes(std::size_t d) {
     prof = DeviceBuffer(dv.ordinal, 64ull * static_cast<std::size_t>(p.ntx + p.nrx));
     cuda_check(cudaMemsetAsync(prof.data(), 0, prof.size(), dv.stream), "memset");
   }
-  if (p.ntx + p.nrx) {
+  const bool strict = opts_.strict_layers != 0;
+  rs_layer_sync sync{};
+  if (strict) {  // zero the launch's arrival counter; the barrier flags are epoch-valued
+    sync = p.layer_sync;
+    cuda_check(cudaMemsetAsync(sync.arrive, 0, sizeof(unsigned long long), dv.stream), "memset");
+  }
+  if (p.ntx + p.nrx || strict) {
     const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
     cuda_check(rs_launch_stream_exchange(lanes, static_cast<std::uint32_t>(p.ntx), lanes + p.ntx,
                                          static_cast<std::uint32_t>(p.nrx),
@@ -810,7 +849,10 @@ int Engine::run_stream_lanes(std::size_t d) {
                                          opts_.ring_stages,
                                          opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
                                          prof.size() ? reinterpret_cast<unsigned long long*>(prof.data()) : nullptr,
-                                         dv.stream),
+                                         reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
+                                         reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
+                                         static_cast<std::uint32_t>(p.local.size()), cap - p.ntx - p.nrx,
+                                         strict ? &sync : nullptr, dv.stream),
                "stream lane kernel launch");
     ++launches;
     if (prof.size() && stream_ws()) {  // diagnostic: per role and warp, mean cycles and idle polls
@@ -861,6 +903,7 @@ int Engine::run_stream_lanes(std::size_t d) {
     const char* e = std::getenv("RS_STREAM_LOCAL_AFTER");
     return e ? std::atoi(e) : 0;
   }();
+  if (strict) return launches;  // the local copies ran inside the lane launch
   if (p.local_items && local_after) {
     cuda_check(rs_launch_copy(reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                               reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),

@@ -4,6 +4,8 @@
 // return a credit (bounded staging, proj/src/executor.cpp:183-206); spare
 // CTAs run the local copies.  Integer / byte movement only.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "desc.h"
@@ -729,7 +731,8 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
     uint32_t nrx, const rs_batch_desc* __restrict__ batches, const rs_copy_desc* __restrict__ frames,
     uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace,
-    unsigned long long* __restrict__ prof) {
+    unsigned long long* __restrict__ prof, const rs_copy_desc* __restrict__ local_descs,
+    const uint64_t* __restrict__ local_item0, uint32_t nlocal, rs_layer_sync sync) {
   extern __shared__ __align__(128) unsigned char stages[];
   __shared__ __align__(8) uint64_t bar[kStages];
   using DR = DescRing<kStages>;
@@ -738,7 +741,44 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   __shared__ __align__(8) uint64_t desc_bar[2 * DR::kNB];
   const int lane = threadIdx.x;
   const bool sender = blockIdx.x < ntx;
-  if (blockIdx.x >= ntx + nrx) return;
+  if (blockIdx.x >= ntx + nrx) {
+    // Strict layers (sync.nlayers > 0): the launch's remaining CTAs copy the
+    // local tasks + carryovers layer by layer through two shared-memory
+    // stages and meet every layer barrier with the lanes.
+    if (!sync.nlayers) return;
+    if (lane == 0) {
+      for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint64_t pol = policy_evict_first();
+    const uint64_t wid = blockIdx.x - ntx - nrx, nw = gridDim.x - ntx - nrx;
+    uint64_t n = 0, begin = 0;
+    for (uint32_t li = 0; li < sync.nlayers; ++li) {
+      const uint64_t end = sync.local_layer_end[li];
+      for (uint64_t item = begin + wid; item < end; item += nw, ++n) {
+        const uint32_t s = static_cast<uint32_t>(n % kStages);
+        if (n >= static_cast<uint64_t>(kStages)) bulk_wait_read_dyn(kStages - 1);  // item n - kStages left stage s
+        __syncwarp();
+        const rs_copy_desc D = local_descs[find_desc(local_item0, nlocal, item)];
+        const uint64_t k = item - D.item0;
+        const uint64_t r0 = k * D.rows_per_item;
+        const uint32_t bytes = static_cast<uint32_t>((min(r0 + D.rows_per_item, D.rows) - r0) * D.row_bytes);
+        unsigned char* stage = stages + static_cast<size_t>(s) * kStreamStageBytes;
+        if (lane == 0) mbar_expect_tx(&bar[s], bytes);
+        __syncwarp();
+        stream_item_load(D, side_contiguous(D, true), k, stage, &bar[s], pol, lane);
+        mbar_wait(&bar[s], static_cast<uint32_t>((n / kStages) & 1));
+        stream_item_store(D, side_contiguous(D, false), k, stage, pol, lane);
+      }
+      begin = end;
+      bulk_wait_all();  // this layer's stores are written before the barrier's release
+      fence_proxy_async_global();
+      __syncwarp();
+      if (!layer_barrier(sync, li, epoch, error_flag, spin_limit)) return;
+    }
+    return;
+  }
   if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
   const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
   const bool peer = (L.flags & RS_LANE_PEER) != 0;
@@ -761,6 +801,16 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   ItemCursor ld, st;
   cursor_start(ld, ring, sender, true, lane);
   cursor_start(st, ring, sender, false, lane);
+  // strict layers: barriers passed so far; a lane end meets barrier l as soon
+  // as its own layer-<=l batches are done (before that, at its first batch,
+  // the barriers of the layers it has no part in)
+  uint32_t barriers = 0;
+  auto pass_to = [&](uint32_t target) -> bool {
+    for (; barriers < target; ++barriers)
+      if (!layer_barrier(sync, barriers, epoch, error_flag, spin_limit)) return false;
+    return true;
+  };
+  if (sync.nlayers && !pass_to(L.nbatches ? ring.batch(0).layer_idx : sync.nlayers)) return;
   uint64_t g_ld = 0, g_st = 0;       // items loaded (issued) / stored (issued)
   uint32_t ready_b = 0xffffffffu;    // receiver: batch whose ready flag was acquired last
   uint32_t credit_b = 0xffffffffu;   // sender: batch whose slot credit was acquired last
@@ -876,6 +926,19 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
         if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
       }
       if (trace && lane == 0) record_batch(trace, L, batches[L.batch0 + b], b, sender ? 0 : 1, t_open[b % kStages]);
+      if (sync.nlayers) {
+        // strict: this lane end's batches of the layers before the next
+        // batch's are done (a receiver's shard stores written) -> barriers
+        if (!sender) {
+          bulk_wait_all();
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        if (!pass_to(st.b < L.nbatches ? ring.batch(st.b).layer_idx : sync.nlayers)) {
+          bulk_wait_all();
+          return;
+        }
+      }
     }
     if (progress) {
       idle = 0;
@@ -1151,8 +1214,11 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
                                       uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
                                       uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags,
                                       int stages, rs_trace_record* trace, unsigned long long* prof,
-                                      cudaStream_t stream) {
-  const int grid = static_cast<int>(ntx + nrx);
+                                      const rs_copy_desc* local_descs, const uint64_t* local_item0, uint32_t nlocal,
+                                      int local_ctas, const rs_layer_sync* sync_in, cudaStream_t stream) {
+  rs_layer_sync sync{};
+  if (sync_in) sync = *sync_in;
+  const int grid = static_cast<int>(ntx + nrx) + (sync.nlayers ? std::max(local_ctas, 1) : 0);
   if (grid == 0) return cudaSuccess;
   const int smem = stages * static_cast<int>(kStreamStageBytes);
   if (flags & kExStreamWS) {  // warp-specialised lane ends (load warp + store warp)
@@ -1178,7 +1244,8 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
                                          smem);                                                                \
     if (e != cudaSuccess) return e;                                                                            \
     rs_stream_lane_kernel<S><<<grid, 32, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, epoch, \
-                                                         error_flag, spin_limit, flags, trace, prof);          \
+                                                         error_flag, spin_limit, flags, trace, prof,           \
+                                                         local_descs, local_item0, nlocal, sync);              \
   } while (0)
   switch (stages) {
     case 1: RS_STREAM_LAUNCH(1); break;

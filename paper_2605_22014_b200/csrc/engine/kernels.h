@@ -32,11 +32,14 @@ cudaError_t rs_launch_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx,
 
 // TMA-pipelined ring lanes (one 1-warp CTA per lane end, `stages` x 16 KB of
 // shared memory); the local copies run as a separate copy launch.
+// sync (strict layers, nlayers > 0): `local_ctas` more CTAs copy the local
+// descriptors layer by layer and every CTA meets a barrier after each layer
 cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx, const rs_lane_desc* lanes_rx,
                                       uint32_t nrx, const rs_batch_desc* batches, const rs_copy_desc* frames,
                                       uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags,
                                       int stages, rs_trace_record* trace, unsigned long long* prof,
-                                      cudaStream_t stream);
+                                      const rs_copy_desc* local_descs, const uint64_t* local_item0, uint32_t nlocal,
+                                      int local_ctas, const rs_layer_sync* sync, cudaStream_t stream);
 int stream_max_blocks_per_sm(int stages);
 int stream_ws_max_blocks_per_sm(int stages);  // warp-specialised stream lanes (flags bit 512)
 

@@ -45,7 +45,8 @@ def ipc_reshard(rank, world, mode):
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
     dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
     torch.cuda.set_device(dev)
-    sp = specs.llama("llama-mini", 4)
+    sp = specs.llama("llama-mini-a16" if mode.endswith("-a16") else "llama-mini", 4)
+    mode = mode.replace("-a16", "")
     co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
     so = [i * world // co.world for i in range(co.world)]
     sn = [(i + 1) * world // cn.world % world for i in range(cn.world)]  # shifted placement

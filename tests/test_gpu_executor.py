@@ -553,6 +553,42 @@ def test_strict_layers_staged_global_layer_order(golden, oracle_c):
         eng.close()
 
 
+@pytest.mark.parametrize("ring_kernel", [2, 1])
+def test_strict_layers_stream_lanes(ring_kernel, golden, oracle_c):
+    """strict_layers on the TMA stream lanes (16 B-aligned plans): the lane
+    launch also runs the local copies and every CTA meets a barrier after
+    each layer, so the trace shows the global layer order; bytes equal the C
+    oracle's (mixed-dtype Llama) and the reference's digest (full GPT-2 C1).
+    ring_kernel 1 forces the classic lanes on the same plans."""
+    sp = specs.llama("llama-mini-a16", 4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 1)
+    eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=2, ring_slot_kib=16, trace=True,
+                      strict_layers=True, ring_kernel=ring_kernel)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["ring_kernel"] == ring_kernel, rep
+    _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 20)
+    for (ti, rank), arr in want.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)
+    tr = [r for r in eng.trace(0) if r["t_end"]]
+    layers = sorted({r["layer"] for r in tr})
+    assert len(layers) == 4
+    for a, b in zip(layers, layers[1:]):
+        end_a = max(r["t_end"] for r in tr if r["layer"] == a)
+        begin_b = min(r["t_begin"] for r in tr if r["layer"] == b)
+        assert begin_b >= end_a - 1000, (a, b, end_a, begin_b)
+    for _ in range(3):  # epoch-valued barrier flags, fresh arrival counter per launch
+        assert eng.run()["ok"]
+    assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
+    sp, co, cn = specs.baseline_case("c1")
+    eng = make_engine(sp, co, cn, "staged", 256 << 20, strict_layers=True, ring_kernel=ring_kernel)
+    rep = R.execute_plan(R.compute_transfer_plan(co, cn, sp), eng)
+    assert rep["ok"] and rep["ring_kernel"] == ring_kernel, rep
+    assert engine_store_digest(eng, RS_DST, sp, dst_owners(oracle_c, sp, cn)) == golden["c1_exec"]["1073741824"]["dst_sha"]
+    eng.close()
+
+
 def test_transport_trace_layer_order_and_causality():
     """STAGED transport trace (rs_trace_read, the reference's RecordingTransport
     on the device): every remote byte appears once per role; each lane

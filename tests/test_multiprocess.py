@@ -57,7 +57,8 @@ def test_plan_agreement_and_partition():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["direct", "direct-tma", "staged", "staged-strict", "xfer"])
+@pytest.mark.parametrize("mode", ["direct", "direct-tma", "staged", "staged-strict", "xfer", "staged-a16",
+                                  "staged-strict-a16"])
 def test_two_processes_one_gpu_ipc(mode):
     import torch
     if not torch.cuda.is_available():
