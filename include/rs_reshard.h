@@ -92,8 +92,9 @@ typedef struct {
   int32_t mode;             /* RS_MODE_* */
   int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 2), STAGED */
   int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
-  int32_t strict_layers;    /* 1: layer barriers (DIRECT: one launch per layer; STAGED: classic lanes
-                               meet a device-wide barrier after each layer), 0: fused */
+  int32_t strict_layers;    /* 1: layer barriers (DIRECT: one launch per layer; STAGED: every lane
+                               CTA meets a device-wide barrier after each layer, the local copies
+                               run inside the lane launch), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
   int32_t blocks_per_sm;    /* 0: occupancy maximum */
   int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
@@ -113,8 +114,9 @@ typedef struct {
   int32_t ring_same_slot;   /* STAGED, cross-rank tasks whose ranks share a GPU: 0 = auto (rings
                                on a one-slot engine -- the transport is what runs -- and direct
                                copies in a multi-slot job), 1 = always rings, 2 = always direct */
-  int32_t ring_kernel;      /* STAGED lane kernel: 0 = auto (TMA stream lanes when every frame is
-                               16 B aligned and strict_layers is off, else classic), 1 = classic
+  int32_t ring_kernel;      /* STAGED lane kernel: 0 = auto (TMA stream lanes when every frame --
+                               and under strict_layers every local copy -- is 16 B aligned with
+                               runs <= 16 KB, else classic), 1 = classic
                                register lanes (rs_exchange_kernel), 2 = TMA stream lanes
                                (rs_stream_lane_kernel; falls back to classic when ineligible),
                                3 = warp-specialised stream lanes (rs_stream_ws_kernel: a load warp
