@@ -328,7 +328,7 @@ def xfer_one_gpu(args) -> None:
 def kernel_name(mode: str, rep: dict) -> str:
     """The kernel that moved the bytes, from the run's own report."""
     if mode == "staged":
-        return {2: "rs_stream_lane_kernel", 3: "rs_stream_ws_kernel"}.get(rep.get("ring_kernel"), "rs_exchange_kernel")
+        return "rs_stream_lane_kernel" if rep.get("ring_kernel") == 2 else "rs_exchange_kernel"
     if mode == "xfer":
         return "rs_copy_kernel pack/unpack + NCCL"
     return COPY_KERNEL_NAMES.get(rep.get("copy_kernel", -1), f"RS_COPY variant {rep.get('copy_kernel')}")

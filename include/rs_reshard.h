@@ -118,9 +118,7 @@ typedef struct {
                                and under strict_layers every local copy -- is 16 B aligned with
                                runs <= 16 KB, else classic), 1 = classic
                                register lanes (rs_exchange_kernel), 2 = TMA stream lanes
-                               (rs_stream_lane_kernel; falls back to classic when ineligible),
-                               3 = warp-specialised stream lanes (rs_stream_ws_kernel: a load warp
-                               and a store warp per lane end; measured 6 % slower on full C2) */
+                               (rs_stream_lane_kernel; falls back to classic when ineligible) */
   int32_t ring_stages;      /* stream lanes: 16 KB shared-memory stages per lane end (0: default 2;
                                1, 2, 3, 4, 6, 8, 10 or 13) */
   int32_t relay;            /* STAGED, multi-slot jobs: 1 = relay chains for DP broadcasts (a box
@@ -166,8 +164,7 @@ typedef struct {
   int32_t copy_kernel;
   int32_t ring_same_slot;
   int32_t ring_kernel;        /* STAGED lane kernel of device 0: 1 classic (rs_exchange_kernel),
-                                 2 TMA stream lanes (rs_stream_lane_kernel), 3 warp-specialised
-                                 stream lanes (rs_stream_ws_kernel), 0 n/a */
+                                 2 TMA stream lanes (rs_stream_lane_kernel), 0 n/a */
   int32_t relay_routes;       /* STAGED relay: distinct (source, destination chain) routes forwarded */
 } rs_exec_report;
 

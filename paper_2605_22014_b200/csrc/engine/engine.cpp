@@ -149,8 +149,8 @@ Engine::Engine(const rs_engine_options& opts) : opts_(opts) {
     throw DomainError("engine: unknown mode");
   if (opts.ring_same_slot < 0 || opts.ring_same_slot > 2)
     throw DomainError("engine: ring_same_slot must be 0 (auto), 1 (rings) or 2 (direct)");
-  if (opts.ring_kernel < 0 || opts.ring_kernel > 3)
-    throw DomainError("engine: ring_kernel must be 0 (auto), 1 (classic), 2 (stream) or 3 (warp-specialised stream)");
+  if (opts.ring_kernel < 0 || opts.ring_kernel > 2)
+    throw DomainError("engine: ring_kernel must be 0 (auto), 1 (classic) or 2 (stream)");
   // stream lanes: 2 x 16 KB stages -> 7 lane CTAs per SM; more lanes beat
   // deeper lanes (profiles/r2/stream_sweep.jsonl)
   if (opts_.ring_stages == 0) opts_.ring_stages = 2;
@@ -953,7 +953,7 @@ void Engine::describe_run(rs_exec_report& rep) const {
   rep.ring_same_slot = opts_.mode == RS_MODE_STAGED ? same_slot_policy() : 0;
   rep.ring_kernel = 0;
   if (opts_.mode == RS_MODE_STAGED && !programs_.empty())
-    rep.ring_kernel = programs_[0].stream_lanes ? (stream_ws() ? 3 : 2) : (programs_[0].ntx + programs_[0].nrx ? 1 : 0);
+    rep.ring_kernel = programs_[0].stream_lanes ? 2 : (programs_[0].ntx + programs_[0].nrx ? 1 : 0);
   rep.relay_routes = relay_routes_;
 }
 

@@ -227,7 +227,6 @@ class Engine {
   int same_slot_policy() const;  // resolved ring_same_slot: 1 rings, 2 direct copies
   bool stream_lanes_for(const reshard::TransferPlan& plan) const;  // STAGED: TMA stream lanes run this plan
   int lane_capacity(int dev, bool stream) const;  // co-resident lane CTAs of the lane kernel
-  bool stream_ws() const;  // stream lanes run warp-specialised (rs_stream_ws_kernel)
   int run_stream_lanes(std::size_t dev);  // enqueue the stream-lane launch + local copies; returns launches
   void describe_run(rs_exec_report& rep) const;  // which kernels / policy the run used
   void upload_layer_sync(std::size_t dev);         // STAGED strict layers: barrier state of a device

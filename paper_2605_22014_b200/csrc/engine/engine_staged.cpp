@@ -751,7 +751,6 @@ void Engine::compile_staged(const reshard::TransferPlan& plan) {
 bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
   if (opts_.mode != RS_MODE_STAGED || opts_.ring_kernel == 1) return false;
   if (opts_.ring_discard & 8) return false;  // the warp-specialised control-warp design is classic only
-  if (opts_.strict_layers && opts_.ring_kernel == 3) return false;  // layer barriers: one-warp stream lanes only
   const Store& src = stores_[RS_SRC];
   const Store& dst = stores_[RS_DST];
   const auto& m = src.model;
@@ -794,13 +793,10 @@ bool Engine::stream_lanes_for(const reshard::TransferPlan& plan) const {
   return true;
 }
 
-bool Engine::stream_ws() const { return opts_.ring_kernel == 3; }
-
 int Engine::lane_capacity(int dev, bool stream) const {
   if (stream)
     return devices_[static_cast<std::size_t>(dev)].sms *
-           std::max(1, stream_ws() ? stream_ws_max_blocks_per_sm(opts_.ring_stages)
-                                   : stream_max_blocks_per_sm(opts_.ring_stages));
+           std::max(1, stream_max_blocks_per_sm(opts_.ring_stages));
   return grid_for(dev, exchange_kernel_id());
 }
 
@@ -844,8 +840,7 @@ int Engine::run_stream_lanes(std::size_t d) {
                                          reinterpret_cast<const rs_copy_desc*>(p.d_frames.data()), epoch_,
                                          reinterpret_cast<unsigned int*>(p.d_error.data()),
                                          opts_.spin_limit > 0 ? static_cast<std::uint64_t>(opts_.spin_limit) : kSpinLimit,
-                                         (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | stream_flags |
-                                             (stream_ws() ? 512 : 0),
+                                         (opts_.fault_inject == 1 ? 1 : 0) | (ring_l2 & 1 ? 2 : 0) | stream_flags,
                                          opts_.ring_stages,
                                          opts_.trace ? reinterpret_cast<rs_trace_record*>(p.d_trace.data()) : nullptr,
                                          prof.size() ? reinterpret_cast<unsigned long long*>(prof.data()) : nullptr,
@@ -855,27 +850,7 @@ int Engine::run_stream_lanes(std::size_t d) {
                                          strict ? &sync : nullptr, dv.stream),
                "stream lane kernel launch");
     ++launches;
-    if (prof.size() && stream_ws()) {  // diagnostic: per role and warp, mean cycles and idle polls
-      std::vector<unsigned long long> h(prof.size() / 8);
-      cuda_check(cudaMemcpyAsync(h.data(), prof.data(), prof.size(), cudaMemcpyDeviceToHost, dv.stream), "prof");
-      cuda_check(cudaStreamSynchronize(dv.stream), "prof");
-      double acc[2][2][2] = {};
-      int n[2] = {0, 0};
-      for (std::size_t i = 0; i < h.size() / 8; ++i) {
-        const int role = h[8 * i + 2] ? 0 : 1;
-        ++n[role];
-        for (int w = 0; w < 2; ++w) {
-          acc[role][w][0] += static_cast<double>(h[8 * i + 4 * w]);
-          acc[role][w][1] += static_cast<double>(h[8 * i + 4 * w + 1]);
-        }
-      }
-      for (int role = 0; role < 2; ++role)
-        if (n[role])
-          std::fprintf(stderr, "[stream ws prof] %s lanes=%d load warp: cycles=%.0f idle_polls=%.0f  store warp: "
-                       "cycles=%.0f idle_polls=%.0f (mean per lane)\n", role ? "rx" : "tx", n[role],
-                       acc[role][0][0] / n[role], acc[role][0][1] / n[role], acc[role][1][0] / n[role],
-                       acc[role][1][1] / n[role]);
-    } else if (prof.size()) {  // diagnostic summary on stderr: mean cycles per phase, senders / receivers
+    if (prof.size()) {  // diagnostic summary on stderr: mean cycles per phase, senders / receivers
       std::vector<unsigned long long> h(prof.size() / 8);
       cuda_check(cudaMemcpyAsync(h.data(), prof.data(), prof.size(), cudaMemcpyDeviceToHost, dv.stream), "prof");
       cuda_check(cudaStreamSynchronize(dv.stream), "prof");

@@ -520,20 +520,33 @@ struct DescRing {
   const rs_batch_desc* batches;
   uint32_t f0, nf;  // this role's frames in the global table
   uint32_t b0, nb;  // the lane's batches
+  bool whole_cta;   // the calling warp is the whole CTA (one-warp lanes): order with bar.sync
 
+  // every lane's earlier generic reads of a buffer before the bulk write that
+  // refills it: a barrier over the readers (the CTA is the lane's one warp),
+  // then a generic -> async proxy fence
+  __device__ __forceinline__ void before_refill() const {
+    if (whole_cta) __syncthreads();
+    else __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+
+  // (warp-uniform calls)
   __device__ __forceinline__ void load_frames(uint32_t j, int lane) const {
-    if (j * kCF >= nf || lane != 0) return;
+    if (j * kCF >= nf) return;
+    before_refill();
+    if (lane != 0) return;
     const uint32_t n = min(kCF, nf - j * kCF);
     const uint32_t buf = j % kNB;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
     mbar_expect_tx(&fbar[buf], n * static_cast<uint32_t>(sizeof(rs_copy_desc)));
     bulk_load(fbuf + buf * kCF, frames + f0 + j * kCF, n * static_cast<uint32_t>(sizeof(rs_copy_desc)), &fbar[buf]);
   }
   __device__ __forceinline__ void load_batches(uint32_t j, int lane) const {
-    if (j * kCB >= nb || lane != 0) return;
+    if (j * kCB >= nb) return;
+    before_refill();
+    if (lane != 0) return;
     const uint32_t n = min(kCB, nb - j * kCB);
     const uint32_t buf = j % kNB;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bbar[buf], n * static_cast<uint32_t>(sizeof(rs_batch_desc)));
     bulk_load(bbuf + buf * kCB, batches + b0 + j * kCB, n * static_cast<uint32_t>(sizeof(rs_batch_desc)), &bbar[buf]);
   }
@@ -797,7 +810,8 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   const uint64_t ld_pol = pol_first, st_pol = sender ? pol_last : pol_first;
 
   const DR ring{desc_frames, desc_batches, desc_bar, desc_bar + DR::kNB, frames, batches,
-                sender ? L.tx_frame0 : L.rx_frame0, sender ? L.tx_nframes : L.rx_nframes, L.batch0, L.nbatches};
+                sender ? L.tx_frame0 : L.rx_frame0, sender ? L.tx_nframes : L.rx_nframes, L.batch0, L.nbatches,
+                true};
   ItemCursor ld, st;
   cursor_start(ld, ring, sender, true, lane);
   cursor_start(st, ring, sender, false, lane);
@@ -975,201 +989,6 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
 }
 
 
-// ------------------------------------------------------- warp-specialised stream lanes
-//
-// Same ring protocol and shared-memory stages as rs_stream_lane_kernel, with
-// the lane end split over two warps (64 threads): a load warp (descriptor
-// chunks, the receiver's ready-flag acquire, bulk loads into free stages) and
-// a store warp (bulk stores out of landed stages, the sender's credit
-// acquire, batch publishes / credits).  Stages pass between them through
-// full / empty mbarriers.  In the one-warp lane every latency -- a release
-// fence at each batch end, a flag poll, a descriptor chunk -- stalled both
-// directions of the pipeline (profiles/r2 ncu source pages); here a store-side
-// fence no longer holds back the next loads and vice versa.
-constexpr int kExStreamWS = 512;
-
-// bounded mbarrier wait of a whole warp (lane 0 polls, the warp agrees, every
-// lane then observes the phase); false = the job aborted
-__device__ __forceinline__ bool warp_mbar_wait(uint64_t* bar, uint32_t parity, unsigned int* error_flag,
-                                               uint64_t spin_limit, int lane, uint64_t& idle) {
-  uint64_t spins = 0;
-  while (true) {
-    int st = 0;  // 1 landed, 2 abort
-    if (lane == 0) {
-      if (mbar_test(bar, parity)) st = 1;
-      else if (*reinterpret_cast<volatile unsigned int*>(error_flag)) st = 2;
-      else if (++spins > spin_limit) {
-        atomicExch(error_flag, 1u);
-        st = 2;
-      } else {
-        __nanosleep(20);
-      }
-    }
-    st = __shfl_sync(0xffffffffu, st, 0);
-    if (st == 1) break;
-    if (st == 2) return false;
-    ++idle;
-  }
-  mbar_wait(bar, parity);
-  return true;
-}
-
-// bounded ring-flag wait of a whole warp (relaxed polls, one acquire)
-__device__ __forceinline__ bool warp_flag_wait(const uint64_t* flag, uint64_t want, bool peer,
-                                               unsigned int* error_flag, uint64_t spin_limit, int lane,
-                                               uint64_t& idle) {
-  uint64_t spins = 0;
-  while (true) {
-    int st = 0;
-    if (lane == 0) {
-      if (flag_reached(flag, want, peer)) st = 1;
-      else if (*reinterpret_cast<volatile unsigned int*>(error_flag)) st = 2;
-      else if (++spins > spin_limit) {
-        atomicExch(error_flag, 1u);
-        st = 2;
-      } else {
-        __nanosleep(32);
-      }
-    }
-    st = __shfl_sync(0xffffffffu, st, 0);
-    if (st == 1) return true;
-    if (st == 2) return false;
-    ++idle;
-  }
-}
-
-template <int kStages>
-__global__ void __launch_bounds__(64, 6) rs_stream_ws_kernel(
-    const rs_lane_desc* __restrict__ lanes_tx, uint32_t ntx, const rs_lane_desc* __restrict__ lanes_rx,
-    uint32_t nrx, const rs_batch_desc* __restrict__ batches, const rs_copy_desc* __restrict__ frames,
-    uint64_t epoch, unsigned int* error_flag, uint64_t spin_limit, int flags, rs_trace_record* __restrict__ trace,
-    unsigned long long* __restrict__ prof) {
-  extern __shared__ __align__(128) unsigned char stages[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  using DR = DescRing<kStages>;
-  __shared__ __align__(128) rs_copy_desc desc_frames[DR::kNB * DR::kCF];
-  __shared__ __align__(128) rs_batch_desc desc_batches[DR::kNB * DR::kCB];
-  __shared__ __align__(8) uint64_t desc_bar[2 * DR::kNB];
-  __shared__ uint64_t t_open[kStages];  // trace: the receiver's ready-flag acquire time per open batch
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool sender = blockIdx.x < ntx;
-  if (blockIdx.x >= ntx + nrx) return;
-  if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
-  const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
-  const bool peer = (L.flags & RS_LANE_PEER) != 0;
-  const bool fwd = !sender && L.fwd_slot_base != 0;  // relay forwarder
-  const bool fpeer = (L.fwd_flags & RS_LANE_PEER) != 0;
-  const int64_t fwd_delta = static_cast<int64_t>(L.fwd_slot_base - L.slot_base_rx);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 * static_cast<int>(DR::kNB); ++i) mbar_init(&desc_bar[i], 1);
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const DR ring{desc_frames, desc_batches, desc_bar, desc_bar + DR::kNB, frames, batches,
-                sender ? L.tx_frame0 : L.rx_frame0, sender ? L.tx_nframes : L.rx_nframes, L.batch0, L.nbatches};
-  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-  uint64_t idle = 0;
-  const uint64_t t0 = clock64();
-  ItemCursor c;
-  cursor_start(c, ring, sender, warp == 0, lane);
-
-  if (warp == 0) {
-    // ---------------- load warp: stages in item order, up to kStages ahead of the store warp
-    uint64_t item = 0;
-    uint32_t ready_b = 0xffffffffu;
-    while (c.b < L.nbatches) {
-      const uint32_t s = static_cast<uint32_t>(item % kStages);
-      if (item >= static_cast<uint64_t>(kStages) &&
-          !warp_mbar_wait(&empty[s], static_cast<uint32_t>((item / kStages - 1) & 1), error_flag, spin_limit, lane,
-                          idle))
-        return;
-      if (!sender && c.first_of_batch && ready_b != c.b) {
-        if (!warp_flag_wait(reinterpret_cast<const uint64_t*>(L.ready_flags_rx) + c.b % L.slots, epoch + c.b + 1, peer,
-                            error_flag, spin_limit, lane, idle))
-          return;
-        ready_b = c.b;
-        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_open[c.b % kStages]));
-        fence_proxy_async_global();  // the slot bytes were published through the generic proxy
-      }
-      const uint64_t r0 = c.k * c.D.rows_per_item;
-      const uint32_t bytes = static_cast<uint32_t>((min(r0 + c.D.rows_per_item, c.D.rows) - r0) * c.D.row_bytes);
-      if (lane == 0) mbar_expect_tx(&full[s], bytes);
-      __syncwarp();
-      stream_item_load(c.D, c.src_contig, c.k, stages + static_cast<size_t>(s) * kStreamStageBytes, &full[s], pol_first,
-                       lane);
-      cursor_next(c, ring, sender, true, lane);
-      ++item;
-    }
-  } else {
-    // ---------------- store warp: landed stages in item order, batch publishes / credits
-    const uint64_t st_pol = sender ? pol_last : pol_first;
-    uint64_t item = 0;
-    uint32_t credit_b = 0xffffffffu;
-    uint64_t t_credit = 0;
-    while (c.b < L.nbatches) {
-      const uint32_t s = static_cast<uint32_t>(item % kStages);
-      if (!warp_mbar_wait(&full[s], static_cast<uint32_t>((item / kStages) & 1), error_flag, spin_limit, lane, idle))
-        break;
-      if ((sender || fwd) && c.first_of_batch && credit_b != c.b) {
-        const uint64_t* f = reinterpret_cast<const uint64_t*>(sender ? L.credit_flags_tx : L.fwd_credit_flags) +
-                            c.b % L.slots;
-        if (c.b >= L.slots &&
-            !warp_flag_wait(f, epoch + c.b - L.slots + 1, sender ? peer : fpeer, error_flag, spin_limit, lane, idle))
-          break;
-        credit_b = c.b;
-        if (trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_credit));
-      }
-      const uint32_t b = c.b;
-      const uint64_t extent = c.extent;
-      stream_item_store(c.D, c.dst_contig, c.k, stages + static_cast<size_t>(s) * kStreamStageBytes, st_pol, lane, fwd,
-                        c.src_contig, fwd_delta, pol_last);
-      bulk_wait_read<0>();  // this stage's bytes are out of shared memory: hand it back
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      const bool last = cursor_next(c, ring, sender, false, lane);
-      ++item;
-      if (!last) continue;
-      const uint32_t slot = b % L.slots;
-      if (sender) {
-        // the batch's slot writes complete, then one release publishes them
-        bulk_wait_all();
-        fence_proxy_async_global();
-        __syncwarp();
-        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.ready_flags) + slot, epoch + b + 1, peer);
-      } else {
-        if (fwd) {  // relay: the batch's bytes are in the next hop's slot -> publish it there
-          bulk_wait_all();
-          fence_proxy_async_global();
-          __syncwarp();
-          if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.fwd_ready_flags) + slot, epoch + b + 1, fpeer);
-        }
-        // every slot byte of batch b has landed in shared memory: drop the
-        // slot's lines from L2 and hand the slot back
-        if ((flags & kExDiscard) && extent && ((L.slot_base_rx | L.slot_bytes) & 127) == 0) {
-          const uint64_t base = L.slot_base_rx + static_cast<uint64_t>(slot) * L.slot_bytes;
-          const uint64_t lines = (extent + 127) >> 7;
-          for (uint64_t i = lane; i < lines; i += 32) discard_l2_line(base + (i << 7));
-        }
-        __syncwarp();
-        if (lane == 0) publish_release(reinterpret_cast<uint64_t*>(L.credit_flags) + slot, epoch + b + 1, peer);
-      }
-      if (trace && lane == 0)
-        record_batch(trace, L, batches[L.batch0 + b], b, sender ? 0 : 1, sender ? t_credit : t_open[b % kStages]);
-    }
-    bulk_wait_all();  // shared memory stays valid until every store has read it
-  }
-  if (prof && lane == 0) {  // diagnostic: cycles and idle polls per warp
-    unsigned long long* p = prof + 8ull * blockIdx.x + 4 * warp;
-    p[0] = clock64() - t0;
-    p[1] = idle;
-    p[2] = sender;
-    p[3] = warp;
-  }
-}
 
 }  // namespace
 
@@ -1221,23 +1040,6 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
   const int grid = static_cast<int>(ntx + nrx) + (sync.nlayers ? std::max(local_ctas, 1) : 0);
   if (grid == 0) return cudaSuccess;
   const int smem = stages * static_cast<int>(kStreamStageBytes);
-  if (flags & kExStreamWS) {  // warp-specialised lane ends (load warp + store warp)
-#define RS_WS_LAUNCH(S)                                                                                     \
-  do {                                                                                                      \
-    cudaError_t e = cudaFuncSetAttribute(rs_stream_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-    if (e != cudaSuccess) return e;                                                                         \
-    rs_stream_ws_kernel<S><<<grid, 64, smem, stream>>>(lanes_tx, ntx, lanes_rx, nrx, batches, frames, epoch,  \
-                                                       error_flag, spin_limit, flags, trace, prof);         \
-  } while (0)
-    switch (stages) {
-      case 1: RS_WS_LAUNCH(1); break;
-      case 3: RS_WS_LAUNCH(3); break;
-      case 4: RS_WS_LAUNCH(4); break;
-      default: RS_WS_LAUNCH(2); break;
-    }
-#undef RS_WS_LAUNCH
-    return cudaGetLastError();
-  }
 #define RS_STREAM_LAUNCH(S)                                                                                    \
   do {                                                                                                         \
     cudaError_t e = cudaFuncSetAttribute(rs_stream_lane_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1259,22 +1061,6 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
   }
 #undef RS_STREAM_LAUNCH
   return cudaGetLastError();
-}
-
-int stream_ws_max_blocks_per_sm(int stages) {
-  int n = 0;
-  const int smem = stages * static_cast<int>(kStreamStageBytes);
-#define RS_WS_OCC(S)                                                                                         \
-  cudaFuncSetAttribute(rs_stream_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);           \
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, rs_stream_ws_kernel<S>, 64, smem)
-  switch (stages) {
-    case 1: RS_WS_OCC(1); break;
-    case 3: RS_WS_OCC(3); break;
-    case 4: RS_WS_OCC(4); break;
-    default: RS_WS_OCC(2); break;
-  }
-#undef RS_WS_OCC
-  return n;
 }
 
 int stream_max_blocks_per_sm(int stages) {

@@ -41,7 +41,6 @@ cudaError_t rs_launch_stream_exchange(const rs_lane_desc* lanes_tx, uint32_t ntx
                                       const rs_copy_desc* local_descs, const uint64_t* local_item0, uint32_t nlocal,
                                       int local_ctas, const rs_layer_sync* sync, cudaStream_t stream);
 int stream_max_blocks_per_sm(int stages);
-int stream_ws_max_blocks_per_sm(int stages);  // warp-specialised stream lanes (flags bit 512)
 
 // which: 0 LDG4, 3 LDG8, 5 LDG16, 6 CTA8, 4 bulk, 1 pattern, 2/7/8 exchange 256/512/1024 threads
 int rs_kernel_max_blocks_per_sm(int which);

@@ -723,11 +723,9 @@ def test_c4_uneven_stage_migration_on_device(mode):
     eng.close()
 
 
-@pytest.mark.parametrize("ring_kernel,stages,slot_kib", [(2, 2, 64), (2, 1, 32), (3, 2, 64), (3, 1, 16), (3, 3, 128),
-                                                         (3, 4, 0)])
+@pytest.mark.parametrize("ring_kernel,stages,slot_kib", [(2, 2, 64), (2, 1, 32), (2, 3, 128), (2, 4, 0), (2, 2, 16)])
 def test_stream_lane_kernels_bitexact(ring_kernel, stages, slot_kib, golden, oracle_c):
-    """The TMA stream lanes -- one warp per lane end (2) or a load warp + a
-    store warp (3) -- over stage counts and slot caps: full GPT-2 C1 equals the
+    """The TMA stream lanes over stage counts and slot caps: full GPT-2 C1 equals the
     reference's digest (twice: epochs advance), and a 16 B-aligned mixed-dtype
     Llama resize equals the C oracle's bytes.  Descriptor chunks are staged in
     shared memory, so long lanes cross many chunk boundaries."""

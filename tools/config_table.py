@@ -66,7 +66,7 @@ def run(case, mode, layers=None):
             "hbm_frac": round(algo / (mean / 1e3) / 1e9 / HBM, 4),
             "hbm_frac_vs_dram_ring": round(ring / (mean / 1e3) / 1e9 / HBM, 4) if mode == "staged" else None,
             "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad,
-            "kernel": ({2: "rs_stream_lane_kernel", 3: "rs_stream_ws_kernel"}.get(rep.get("ring_kernel"), "rs_exchange_kernel")
+            "kernel": (("rs_stream_lane_kernel" if rep.get("ring_kernel") == 2 else "rs_exchange_kernel")
                        if mode == "staged" else f"RS_COPY {rep.get('copy_kernel')}")}
 
 
