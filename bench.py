@@ -652,8 +652,10 @@ def e2e(eng, plan, total, args, world=1, local_entry=None) -> dict:
     h2d = sum(n for (_, _, n), l in zip(src, src_local) if l)
     d2h = sum(n for (_, _, n), l in zip(dst, dst_local) if l)
     host_src = PinnedBuffer(max(h2d, 1))
-    window = PinnedBuffer(4 << 30)
-    keep_cap = 4 << 30
+    # the destination window and the verified region split 8 GiB of pinned
+    # memory over the job's processes (one host's RAM holds every rank's)
+    window = PinnedBuffer(max(512 << 20, (4 << 30) // world))
+    keep_cap = max(512 << 20, (4 << 30) // world)
     # the host source store holds the device source state, so the e2e output
     # is checkable against the analytic pattern afterwards
     off, src_ptrs = 0, []
