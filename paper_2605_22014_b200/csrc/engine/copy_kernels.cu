@@ -269,6 +269,9 @@ __global__ void __launch_bounds__(32) rs_copy_tma_np_kernel(const rs_copy_desc* 
     int64_t so, dof;
     row_offsets(D, static_cast<uint32_t>(r), so, dof);
     bulk_store(reinterpret_cast<void*>(D.dst + dof), buf + off, static_cast<uint32_t>(D.row_bytes));
+    // DP broadcast: the second destination from the same shared-memory copy
+    if (D.dst2_delta)
+      bulk_store(reinterpret_cast<void*>(D.dst + dof + D.dst2_delta), buf + off, static_cast<uint32_t>(D.row_bytes));
     off += static_cast<uint32_t>(D.row_bytes);
   }
   bulk_commit();

@@ -28,7 +28,11 @@ typedef struct {
   uint32_t nouter;
   uint32_t vec_log2;      // access width: 1 << vec_log2 bytes (0..4)
   uint32_t tag;           // layer (diagnostics)
-  uint64_t reserved;      // pads the descriptor to 160 B: tables stay bulk-copyable (16 B granules)
+  // DP broadcast (DIRECT copy kernels): every row is also stored at
+  // dst + dst2_delta -- a second destination with the same layout, written
+  // from the same load (0: none).  Keeps the descriptor 160 B: tables stay
+  // bulk-copyable in 16 B granules.
+  int64_t dst2_delta;
 } rs_copy_desc;
 
 // Synthetic-state descriptor: one shard buffer (row-major over its view),

@@ -87,7 +87,7 @@ __device__ __forceinline__ uint4 load16(const uint4* p, uint64_t pol) {
 // issued before their stores.
 template <typename T, bool kReadOnly, int U = kUnroll, bool kStream = false, int kLd = 0>
 __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64_t nbytes,
-                                              int lane) {
+                                              int lane, int64_t dst2 = 0) {
   const T* s = reinterpret_cast<const T*>(src);
   T* d = reinterpret_cast<T*>(dst);
   const uint64_t n = nbytes / sizeof(T);
@@ -108,19 +108,28 @@ __device__ __forceinline__ void warp_copy_run(const char* src, char* dst, uint64
       if constexpr (kStream && sizeof(T) == 16) store_cs(reinterpret_cast<uint4*>(d + i + 32 * u), v[u]);
       else store<T>(d + i + 32 * u, v[u]);
     }
+    if (dst2) {  // DP broadcast: the same registers to the second destination
+      T* d2 = reinterpret_cast<T*>(dst + dst2);
+#pragma unroll
+      for (int u = 0; u < U; ++u) store<T>(d2 + i + 32 * u, v[u]);
+    }
   }
-  for (; i < n; i += 32) store<T>(d + i, load<T, kReadOnly>(s + i));
+  for (; i < n; i += 32) {
+    const T v = load<T, kReadOnly>(s + i);
+    store<T>(d + i, v);
+    if (dst2) store<T>(reinterpret_cast<T*>(dst + dst2) + i, v);
+  }
 }
 
 template <bool kReadOnly, int U = kUnroll, bool kStream = false, int kLd = 0>
 __device__ __forceinline__ void warp_copy_any(const char* src, char* dst, uint64_t nbytes,
-                                              uint32_t vec_log2, int lane) {
+                                              uint32_t vec_log2, int lane, int64_t dst2 = 0) {
   switch (vec_log2) {
-    case 4: warp_copy_run<uint4, kReadOnly, U, kStream, kLd>(src, dst, nbytes, lane); break;
-    case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane); break;
-    case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane); break;
-    case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane); break;
-    default: warp_copy_run<uint8_t, kReadOnly>(src, dst, nbytes, lane); break;
+    case 4: warp_copy_run<uint4, kReadOnly, U, kStream, kLd>(src, dst, nbytes, lane, dst2); break;
+    case 3: warp_copy_run<uint2, kReadOnly>(src, dst, nbytes, lane, dst2); break;
+    case 2: warp_copy_run<uint32_t, kReadOnly>(src, dst, nbytes, lane, dst2); break;
+    case 1: warp_copy_run<uint16_t, kReadOnly>(src, dst, nbytes, lane, dst2); break;
+    default: warp_copy_run<uint8_t, kReadOnly>(src, dst, nbytes, lane, dst2); break;
   }
 }
 
@@ -167,7 +176,7 @@ __device__ __forceinline__ void warp_copy_item(const rs_copy_desc& D, uint64_t l
   for (uint64_t r = r0; r < r1; ++r) {
     int64_t so, dof;
     row_offsets(D, static_cast<uint32_t>(r), so, dof);
-    warp_copy_any<kReadOnly, U, kStream, kLd>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane);
+    warp_copy_any<kReadOnly, U, kStream, kLd>(src + so, dst + dof, D.row_bytes, D.vec_log2, lane, D.dst2_delta);
   }
 }
 

@@ -22,6 +22,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <tuple>
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
@@ -635,18 +636,52 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
   const std::int64_t B = opts_.staging_bytes;
   std::vector<std::size_t> mark(devices_.size());
 
-  auto push = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb, int layer) {
+  // de2 (DP broadcast): a second destination with de's layout, written from
+  // the same load (rs_copy_desc.dst2_delta)
+  auto push = [&](const Entry* se, const Entry* de, const reshard::ShardView& box, std::int64_t eb, int layer,
+                  const Entry* de2 = nullptr) {
     const int l = local_of(se->slot);
     if (l < 0) return;  // the source's process pushes it
-    if (de->slot != se->slot) programs_[static_cast<std::size_t>(l)].peer_stores = true;
-    append_copy(programs_[static_cast<std::size_t>(l)].local, view_base(se, "source"), se->view,
-                view_base(de, "destination"), de->view, box, eb, static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
+    auto& prog = programs_[static_cast<std::size_t>(l)];
+    if (de->slot != se->slot || (de2 && de2->slot != se->slot)) prog.peer_stores = true;
+    const std::size_t first = prog.local.size();
+    append_copy(prog.local, view_base(se, "source"), se->view, view_base(de, "destination"), de->view, box, eb,
+                static_cast<std::uint32_t>(layer), opts_.copy_kernel != RS_COPY_CE);
+    if (!de2) return;
+    const auto delta = static_cast<std::int64_t>(view_base(de2, "destination") - view_base(de, "destination"));
+    for (std::size_t k = first; k < prog.local.size(); ++k) {
+      rs_copy_desc& d = prog.local[k];
+      d.dst2_delta = delta;
+      while (d.vec_log2 > 0 && (static_cast<std::uint64_t>(delta) & ((1ull << d.vec_log2) - 1))) --d.vec_log2;
+    }
   };
+  // DP broadcasts: a layer's copies with one source rank, tensor and box into
+  // destinations of identical layout (DP replicas) are paired so one load
+  // feeds both stores -- 3 instead of 4 bytes of HBM traffic per byte pair.
+  // Only the copy kernels that honour dst2_delta (LDG warp engine, TMA-NP).
+  static const bool bcast_off = [] {  // diagnostic A/B knob: RS_DIRECT_BCAST=0
+    const char* e = std::getenv("RS_DIRECT_BCAST");
+    return e && std::atoi(e) == 0;
+  }();
+  const bool bcast = !bcast_off && opts_.copy_kernel != RS_COPY_CE && opts_.copy_kernel != RS_COPY_CTA8 &&
+                     opts_.copy_kernel != RS_COPY_BULK && (opts_.copy_kernel < RS_COPY_BULK_MW ||
+                                                          opts_.copy_kernel > RS_COPY_BULK_MW + 4);
+  struct Copy {
+    int src_rank, dst_rank;
+    std::uint32_t ti;
+    const reshard::ShardView* box;
+    bool keep;
+  };
+  std::vector<Copy> copies;
+  std::vector<int> partner;
 
   for (int layer : plan_layers_) {
     for (std::size_t d = 0; d < devices_.size(); ++d) mark[d] = programs_[d].local.size();
     rs_exec_report delta{};
     try {
+      // validate every copy of the layer (the reference's checks and
+      // messages), then pair DP broadcasts, then emit
+      copies.clear();
       if (auto it = plan.carryover_by_layer.find(layer); it != plan.carryover_by_layer.end()) {
         for (const auto& k : it->second) {
           const Entry* se = src.find(k.rank, k.tensor_index);
@@ -654,9 +689,8 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
           if (!se || !de) throw IntegrityError(no_buffer(k.rank, k.tensor_index));
           if (!holds(se, k.bounds)) throw IntegrityError(escape_msg("slice_local", k.bounds, se->view));
           if (!holds(de, k.bounds)) throw IntegrityError(escape_msg("scatter_local", k.bounds, de->view));
-          const std::int64_t eb = m.element_bytes(m.tensors[k.tensor_index]);
-          push(se, de, k.bounds, eb, layer);
-          delta.carryover_bytes += k.bounds.element_count() * eb;
+          copies.push_back({k.rank, k.rank, k.tensor_index, &k.bounds, true});
+          delta.carryover_bytes += k.bounds.element_count() * m.element_bytes(m.tensors[k.tensor_index]);
         }
       }
       if (auto it = plan.tasks_by_layer.find(layer); it != plan.tasks_by_layer.end()) {
@@ -669,11 +703,48 @@ void Engine::compile_direct(const reshard::TransferPlan& plan) {
           const Entry* de = dst.find(t.dst_rank, t.tensor_index);
           if (!de) throw IntegrityError(no_buffer(t.dst_rank, t.tensor_index));
           if (!holds(de, t.bounds)) throw IntegrityError(escape_msg("scatter_local", t.bounds, de->view));
-          push(se, de, t.bounds, eb, layer);
+          copies.push_back({t.src_rank, t.dst_rank, t.tensor_index, &t.bounds, false});
           const std::int64_t n = t.bounds.element_count() * eb;
           if (t.is_local()) delta.local_copy_bytes += n;
           else delta.bytes_moved += n;
         }
+      }
+      partner.assign(copies.size(), -1);  // -1 alone, >= 0 the paired copy, -2 emitted by its partner
+      if (bcast && copies.size() > 1) {
+        std::map<std::tuple<int, std::uint32_t, std::vector<std::int64_t>>, std::vector<std::size_t>> groups;
+        for (std::size_t i = 0; i < copies.size(); ++i) {
+          std::vector<std::int64_t> b;
+          for (std::size_t d = 0; d < copies[i].box->ndims(); ++d) {
+            b.push_back(copies[i].box->dim(d).lo);
+            b.push_back(copies[i].box->dim(d).hi);
+          }
+          groups[{copies[i].src_rank, copies[i].ti, std::move(b)}].push_back(i);
+        }
+        for (const auto& kv : groups) {
+          const auto& g = kv.second;
+          for (std::size_t a = 0; a < g.size(); ++a) {
+            if (partner[g[a]] != -1) continue;
+            const Entry* da = dst.find(copies[g[a]].dst_rank, copies[g[a]].ti);
+            for (std::size_t b = a + 1; b < g.size(); ++b) {
+              if (partner[g[b]] != -1) continue;
+              const Entry* db = dst.find(copies[g[b]].dst_rank, copies[g[b]].ti);
+              if (da->view == db->view && da->flat == db->flat && da->flat_lo == db->flat_lo) {
+                partner[g[a]] = static_cast<int>(g[b]);
+                partner[g[b]] = -2;
+                break;
+              }
+            }
+          }
+        }
+      }
+      for (std::size_t i = 0; i < copies.size(); ++i) {
+        if (partner[i] == -2) continue;
+        const Copy& c = copies[i];
+        const Entry* se = src.find(c.src_rank, c.ti);
+        const Entry* de = dst.find(c.dst_rank, c.ti);
+        const Entry* de2 = partner[i] >= 0 ? dst.find(copies[static_cast<std::size_t>(partner[i])].dst_rank, c.ti)
+                                           : nullptr;
+        push(se, de, *c.box, m.element_bytes(m.tensors[c.ti]), layer, de2);
       }
     } catch (const IntegrityError& e) {
       for (std::size_t d = 0; d < devices_.size(); ++d) programs_[d].local.resize(mark[d]);
