@@ -70,6 +70,23 @@ def test_two_processes_one_gpu_ipc(mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["direct-a16", "staged-a16", "staged-strict-a16"])
+def test_eight_processes_one_gpu_ipc(mode):
+    """The 8-GPU process layout on one B200: eight processes, one slot each,
+    every peer arena CUDA-IPC mapped into every process, the new ranks
+    shifted one slot so every cross-rank byte crosses a process boundary
+    (DIRECT peer stores incl. paired DP broadcasts, STAGED stream lanes with
+    .sys handshakes, strict layer barriers over eight slots' done flags)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    outs = launch(mode, world=8, timeout=900)
+    for o in outs:
+        assert o["result"]["ok"], o
+        assert o["result"]["mismatches"] == 0, o
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["direct", "staged"])
 def test_two_processes_live_handoff_chain(mode):
     """Runtime hook across processes: three generations through LiveHandoff
