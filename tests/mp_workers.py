@@ -103,7 +103,8 @@ def relay_reshard(rank, world):
     so = [r % world for r in co.ranks] if "slot_old" not in case else case["slot_old"]
     sn = case["slot_new"]
     eng = R.Engine([dev], staging_bytes=case.get("staging", 1 << 20), mode="staged", lanes_per_link=case.get("lanes", 1),
-                   world_slots=world, first_local_slot=rank, relay=case.get("relay", True))
+                   world_slots=world, first_local_slot=rank, relay=case.get("relay", True),
+                   strict_layers=case.get("strict", False))
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
     eng.alloc(RS_SRC)
