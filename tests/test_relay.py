@@ -76,6 +76,35 @@ def _dp_scaleout_cases():
     return out
 
 
+def _random_relay_cases(n=6, seed=7):
+    """Random DP scale-outs of the aligned mini Llama (either dtype group)
+    over 3-4 slots with random rank placements, kept when relay chains
+    change the traffic (so every case forwards)."""
+    import random
+    rng = random.Random(seed)
+    out = []
+    while len(out) < n:
+        tp0, pp0 = rng.choice([1, 2, 4]), rng.choice([1, 2])
+        dpn, tpn, ppn = rng.choice([2, 3, 4]), rng.choice([1, 2]), rng.choice([1, 2])
+        wo, wn = tp0 * pp0, tpn * ppn * dpn
+        if wn > 8:
+            continue
+        w, layers, bpe = rng.choice([3, 4]), rng.choice([2, 3, 4]), rng.choice([2, 4])
+        so = [rng.randrange(w) for _ in range(wo)]
+        sn = [rng.randrange(w) for _ in range(wn)]
+        if len(set(so) | set(sn)) < w:
+            continue
+        sp = specs.group_spec(specs.llama("llama-mini-a16", layers), bpe)
+        co, cn = specs.iota_config(1, tp0, pp0, 1), specs.iota_config(2, tpn, ppn, dpn)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        if R.plan_traffic(plan, co, so, cn, sn, w, relay=True) == R.plan_traffic(plan, co, so, cn, sn, w):
+            continue
+        out.append({"name": f"rand{len(out)}", "layers": layers, "bpe": bpe, "old": [tp0, pp0, 1],
+                    "new": [tpn, ppn, dpn], "slot_old": so, "slot_new": sn, "world": w,
+                    "lanes": rng.choice([1, 2])})
+    return out
+
+
 @pytest.mark.parametrize("case", _dp_scaleout_cases(), ids=lambda c: c["name"])
 def test_mini_cases_have_relay_chains(case):
     """CPU: the test placements do exercise relays (chains exist and the hot
@@ -90,7 +119,7 @@ def test_mini_cases_have_relay_chains(case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", _dp_scaleout_cases(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("case", _dp_scaleout_cases() + _random_relay_cases(), ids=lambda c: c["name"])
 def test_relay_staged_bitexact_vs_reference(case, oracle_ref):
     import torch
     if not torch.cuda.is_available():
