@@ -801,3 +801,42 @@ def test_flat_bucket_distributed_optimizer_bitexact(mode, oracle_c):
     for (ti, rank), arr in want.entries.items():
         assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)
     eng.close()
+
+
+def _random_aligned_resizes(n=10, seed=11):
+    """Random TP/PP/DP resizes of the 16 B-aligned mini Llama (mixed bf16 /
+    fp32 state), uneven stage splits included: every one runs on the TMA
+    stream lanes."""
+    import random
+    rng = random.Random(seed)
+    out = []
+    while len(out) < n:
+        layers = rng.choice([2, 3, 4, 5])
+        shapes = []
+        for gen in (1, 2):
+            tp, pp, dp = rng.choice([1, 2, 4]), rng.choice([1, 2]), rng.choice([1, 2])
+            if tp * pp * dp > 8:
+                break
+            stages = None
+            if pp == 2 and rng.random() < 0.5:
+                first = rng.randrange(1, layers)
+                stages = [0] * first + [1] * (layers - first)
+            shapes.append(specs.iota_config(gen, tp, pp, dp, layer_stage=stages))
+        if len(shapes) == 2:
+            out.append((layers, shapes[0], shapes[1]))
+    return out
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_stream_lanes_random_aligned_resizes(strict, oracle_c):
+    for layers, co, cn in _random_aligned_resizes():
+        sp = specs.llama("llama-mini-a16", layers)
+        eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=2, ring_slot_kib=16, strict_layers=strict)
+        plan = R.compute_transfer_plan(co, cn, sp)
+        rep = R.execute_plan(plan, eng)
+        assert rep["ok"], (co, cn, rep)
+        assert rep["ring_kernel"] == (2 if rep["bytes_moved"] or strict else 0), (co, cn, rep)
+        _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 1 << 20)
+        for (ti, rank), arr in want.entries.items():
+            assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (co, cn, ti, rank)
+        eng.close()
