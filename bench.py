@@ -370,6 +370,18 @@ def timed_steps(one_step, steps: int, world: int, barrier, device: int):
     return dev_ms, launches, wall, clk.summary(), rep
 
 
+def guarded(leg: str, fn) -> dict:
+    """Run a secondary leg (STAGED sub-object, e2e) so that its failure is
+    reported inside the headline line instead of discarding the DIRECT
+    number already measured; the traceback goes to stderr."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001 -- reported, never swallowed silently
+        import traceback
+        traceback.print_exc(file=sys.stderr)
+        return {"ok": False, "error": f"{leg}: {type(e).__name__}: {e}"[:600]}
+
+
 def reduce_ranks(world: int, step_ms: float, counts):
     """max over ranks of the step time, sum over ranks of the counters."""
     if world == 1:
@@ -595,7 +607,8 @@ def ours(args) -> None:
     run_staged = args.mode == "direct" and not args.no_staged and (
         not same_device or world == 1 or os.environ.get("RS_BENCH_STAGED"))
     if run_staged:
-        line["staged"] = staged_leg(eng, sp, co, so, cn, sn, plan, traffic, args, world, rank, device, barrier, pk)
+        line["staged"] = guarded("staged", lambda: staged_leg(eng, sp, co, so, cn, sn, plan, traffic, args, world,
+                                                              rank, device, barrier, pk))
     elif args.mode == "direct":
         line["staged"] = {"skipped": "processes time-share one GPU (RS_BENCH_SAME_DEVICE): ring lanes of different "
                                      "processes are never co-resident; set RS_BENCH_STAGED=1 to run it anyway"
@@ -616,7 +629,7 @@ def ours(args) -> None:
 
         def local_entry(which, r):
             return (so[pos_old[r]] if which == RS_SRC else sn[pos_new[r]]) == rank
-        line["e2e"] = e2e(eng, plan, total, args, world, local_entry)
+        line["e2e"] = guarded("e2e", lambda: e2e(eng, plan, total, args, world, local_entry))
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
