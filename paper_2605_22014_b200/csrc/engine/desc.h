@@ -104,10 +104,21 @@ typedef struct {
 // GPU count in `arrive`; the last one publishes this slot's `done_self` flag
 // and, in a multi-GPU job, waits for every slot's flag (peer-mapped,
 // system scope) before releasing its GPU's CTAs through `release`.
+//
+// Stream lanes run layer-scoped roles: a CTA takes a role by ticket (roles
+// sorted by first layer, so the CTAs of the earliest layers are resident
+// first), meets only the barriers of its lane's layer range, and layer l's
+// barrier waits for expect[l] arrivals -- the CTAs active in l.  Lanes of
+// links that never share a layer (the PP stages) then reuse the same CTA
+// slots instead of idling through each other's layers.  Classic lanes:
+// expect == roles == null, every CTA arrives at every barrier (cumulative).
 typedef struct {
   uint32_t nlayers;                 // 0: no barriers (fused layers)
   uint32_t nslots;                  // slots whose flags `done_all` lists (1: this GPU only)
-  unsigned long long* arrive;       // per-launch arrival counter (zeroed before the launch)
+  unsigned long long* arrive;       // arrival counters (zeroed before the launch): one, or one per layer with expect
+  const uint32_t* expect;           // arrivals that complete barrier l (CTAs active in layer l), or null
+  const uint32_t* roles;            // ticket -> CTA role (the blockIdx the role stands for), or null
+  unsigned long long* tickets;      // role ticket counter (zeroed with `arrive`)
   uint64_t* release;                // this GPU's release flag (epoch + layer + 1)
   uint64_t* done_self;              // this slot's layer-done flag (in its comm arena)
   const uint64_t* const* done_all;  // every slot's layer-done flag as mapped here (device array)

@@ -964,7 +964,8 @@ rs_exec_report Engine::run() {
       rs_layer_sync sync{};
       if (opts_.strict_layers) {
         sync = p.layer_sync;
-        cuda_check(cudaMemsetAsync(sync.arrive, 0, sizeof(unsigned long long), devices_[d].stream), "memset");
+        cuda_check(cudaMemsetAsync(sync.arrive, 0, (sync.nlayers + 1ull) * sizeof(unsigned long long), devices_[d].stream),
+                   "memset");
       }
       // ring slots in L2: 0 = default (discard + policies), else bit flags (2 = neither)
       const int ring_l2 = opts_.ring_discard == 0 ? 5 : opts_.ring_discard;

@@ -113,9 +113,12 @@ struct DeviceProgram {
   std::vector<rs_batch_desc> batches;
   std::vector<rs_copy_desc> frames;
   DeviceBuffer d_local, d_item0, d_lanes, d_batches, d_frames, d_error, d_trace;
-  // STAGED strict layers: [arrival counter][release flag][done_all: nslots ptrs][layer item ends]
+  // STAGED strict layers: [arrival counters: nlayers][role ticket][release flag][done_all: nslots ptrs]
+  // [layer item ends][stream lanes: per-layer expected arrivals, role table (u32)]
   DeviceBuffer d_sync;
   rs_layer_sync layer_sync{};
+  int strict_local_ctas = 0;   // stream lanes, strict: local-copy CTAs of the lane launch
+  int strict_max_active = 0;   // stream lanes, strict: most lane CTAs active in one layer
   std::uint64_t local_bytes = 0;
   bool all_aligned = true;  // every local descriptor is 16 B aligned (bulk-copy eligible)
   std::uint64_t launch_bytes = 0;  // bytes of the largest single copy launch (grid / item sizing)

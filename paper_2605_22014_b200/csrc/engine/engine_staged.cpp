@@ -119,7 +119,10 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     std::uint64_t bytes = 0;
     int tx_slot = 0;
     std::vector<int> rx_ranks;
+    int first = -1, last = -1;  // plan-layer index range of its tasks
   };
+  std::map<int, int> layer_index;
+  for (std::size_t i = 0; i < plan_layers_.size(); ++i) layer_index[plan_layers_[i]] = static_cast<int>(i);
   std::map<LaneKey, Link> links;
   for (const auto& [layer, tasks] : plan.tasks_by_layer)
     for (std::size_t i = 0; i < tasks.size(); ++i) {
@@ -137,6 +140,9 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
                                            : geo.route_chain[static_cast<std::size_t>(std::get<2>(key))];
       }
       lk.bytes += static_cast<std::uint64_t>(t.byte_size);
+      const int li = layer_index.count(layer) ? layer_index.at(layer) : 0;
+      lk.first = lk.first < 0 ? li : std::min(lk.first, li);
+      lk.last = std::max(lk.last, li);
     }
   std::map<int, std::set<LaneKey>> inbound;  // dst rank -> links with a receiver there
   for (const auto& [key, lk] : links)
@@ -155,12 +161,10 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   if (opts_.lanes_per_link > 0) {
     for (const auto& kv : links) lanes_of[kv.first] = opts_.lanes_per_link;
   } else if (!links.empty()) {
-    std::vector<std::uint64_t> slot_bytes(static_cast<std::size_t>(nslots_), 0);
     auto touches = [&](const Link& lk, auto&& fn) {  // every CTA-hosting slot of a link, once per CTA
       fn(lk.tx_slot);
       for (int r : lk.rx_ranks) fn(slot_in(dst_slot, r));
     };
-    for (const auto& [key, lk] : links) touches(lk, [&](int sl) { slot_bytes[static_cast<std::size_t>(sl)] += lk.bytes; });
     // Share of the co-resident CTAs given to ring lanes; the rest run the
     // local copies (local tasks + carryovers) in the same launch.  Balanced so
     // both finish together: a lane pair (2 CTAs) streams ~10 GB/s of payload,
@@ -174,31 +178,54 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     const double r = remote_total ? static_cast<double>(local_total) / static_cast<double>(remote_total) : 0.0;
     // stream lanes: the local copies run as their own launch beside the lane
     // kernel, so the lanes may take (almost) every co-resident CTA slot
-    // (strict: the local copies run inside the lane launch -- leave them the
-    // remote : local byte share of the CTAs)
-    double frac = geo.stream ? (opts_.strict_layers ? 0.98 * std::clamp(1.0 / (1.0 + r), 0.5, 0.95) : 0.98)
+    // (strict: the local copies run inside the lane launch, in 1-warp CTAs
+    // that move ~2/3 of a lane end's bytes each -- leave them a 1.5 r share:
+    // full C2 strict 49.0 ms at 1 / (1 + r), 47.4 ms at this share,
+    // profiles/r2/strict_scoped/strict_sweep2.jsonl)
+    double frac = geo.stream ? (opts_.strict_layers ? 0.98 * std::clamp(1.0 / (1.0 + 1.5 * r), 0.5, 0.95) : 0.98)
                              : std::clamp(1.94 / (2.0 + 0.5 * r), 0.5, 0.97);
     if (const char* env = std::getenv("RS_RING_CAPACITY_FRAC")) frac = std::atof(env);
     const int capacity = static_cast<int>(lane_capacity(0, geo.stream) * frac);
-    int max_lanes = 64;  // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than 32)
+    // per link (few-link plans, e.g. GPT-2 C1 with 4 links, need more than
+    // 32; strict stream lanes give one PP stage's few links the whole share)
+    int max_lanes = geo.stream && opts_.strict_layers ? 128 : 64;
     if (const char* env = std::getenv("RS_RING_MAX_LANES")) max_lanes = std::atoi(env);
-    const double busiest = static_cast<double>(*std::max_element(slot_bytes.begin(), slot_bytes.end()));
+    // The capacity constraint is per slot; under strict layers it is per
+    // (layer, slot): the lane kernel runs layer-scoped roles (a lane end's
+    // CTA is needed only over its link's layer range, upload_layer_sync), so
+    // links that never share a layer -- the PP stages -- each get the whole
+    // lane share instead of splitting it.  Fused, every lane is live at once:
+    // one "layer" spanning the plan.
+    const bool scoped = geo.stream && opts_.strict_layers;
+    const std::size_t nl = scoped ? std::max<std::size_t>(plan_layers_.size(), 1) : 1;
+    auto span = [&](const Link& lk, auto&& fn) {  // the layers (rows) a link's lanes are live in
+      if (!scoped) return fn(std::size_t{0});
+      for (int li = std::max(lk.first, 0); li <= lk.last; ++li) fn(static_cast<std::size_t>(li));
+    };
+    const std::size_t ns = static_cast<std::size_t>(nslots_);
+    std::vector<double> live_bytes(nl * ns, 0.0);
+    for (const auto& [key, lk] : links)
+      span(lk, [&](std::size_t li) { touches(lk, [&](int sl) { live_bytes[li * ns + static_cast<std::size_t>(sl)] += static_cast<double>(lk.bytes); }); });
+    const double busiest = *std::max_element(live_bytes.begin(), live_bytes.end());
     const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
-    std::vector<int> slot_lanes(static_cast<std::size_t>(nslots_), 0);
+    std::vector<int> live_lanes(nl * ns, 0);
     for (const auto& [key, lk] : links) {
       const int n = std::clamp(static_cast<int>(scale * static_cast<double>(lk.bytes)), 1, max_lanes);
       lanes_of[key] = n;
-      touches(lk, [&](int sl) { slot_lanes[static_cast<std::size_t>(sl)] += n; });
+      span(lk, [&](std::size_t li) { touches(lk, [&](int sl) { live_lanes[li * ns + static_cast<std::size_t>(sl)] += n; }); });
     }
     // the max(1, .) floor can overshoot a slot with many light links: trim
-    // the widest links touching it
-    for (int sl = 0; sl < nslots_; ++sl)
-      while (slot_lanes[static_cast<std::size_t>(sl)] > capacity) {
+    // the widest links live there
+    for (std::size_t row = 0; row < nl * ns; ++row)
+      while (live_lanes[row] > capacity) {
+        const std::size_t li = row / ns;
+        const int sl = static_cast<int>(row % ns);
         const LaneKey* widest = nullptr;
         int w = 1;
         for (const auto& [key, lk] : links) {
           bool hit = false;
           touches(lk, [&](int x) { hit = hit || x == sl; });
+          if (scoped) hit = hit && static_cast<int>(li) >= lk.first && static_cast<int>(li) <= lk.last;
           if (hit && lanes_of[key] > w) {
             w = lanes_of[key];
             widest = &key;
@@ -206,7 +233,8 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
         }
         if (!widest) break;  // every link at one lane: the launch check reports it
         --lanes_of[*widest];
-        touches(links.at(*widest), [&](int x) { --slot_lanes[static_cast<std::size_t>(x)]; });
+        const Link& wl = links.at(*widest);
+        span(wl, [&](std::size_t l2) { touches(wl, [&](int x) { --live_lanes[l2 * ns + static_cast<std::size_t>(x)]; }); });
       }
   }
   // Ring slot size per dst rank: B split over its inbound lanes, capped at
@@ -807,8 +835,12 @@ int Engine::run_stream_lanes(std::size_t d) {
   DeviceProgram& p = programs_[d];
   Device& dv = devices_[d];
   const int cap = lane_capacity(static_cast<int>(d), true);
-  if (p.ntx + p.nrx > cap || (opts_.strict_layers && p.ntx + p.nrx >= cap))
-    throw DomainError("staged: " + std::to_string(p.ntx + p.nrx) + " stream lanes exceed the co-resident CTA capacity " +
+  // strict: layer-scoped roles, so only the lane CTAs active in one layer
+  // (plus one local-copy CTA) must be co-resident
+  const int resident = opts_.strict_layers ? p.strict_max_active : p.ntx + p.nrx;
+  if (resident > cap || (opts_.strict_layers && resident >= cap))
+    throw DomainError("staged: " + std::to_string(resident) + " stream lanes" +
+                      (opts_.strict_layers ? " active in one layer" : "") + " exceed the co-resident CTA capacity " +
                       std::to_string(cap) + (opts_.strict_layers ? " (strict: one CTA must stay for the local copies)" : "") +
                       "; lower lanes_per_link");
   DeviceGuard g(dv.ordinal);
@@ -830,7 +862,8 @@ int Engine::run_stream_lanes(std::size_t d) {
   rs_layer_sync sync{};
   if (strict) {  // zero the launch's arrival counter; the barrier flags are epoch-valued
     sync = p.layer_sync;
-    cuda_check(cudaMemsetAsync(sync.arrive, 0, sizeof(unsigned long long), dv.stream), "memset");
+    cuda_check(cudaMemsetAsync(sync.arrive, 0, (sync.nlayers + 1ull) * sizeof(unsigned long long), dv.stream),
+               "memset");
   }
   if (p.ntx + p.nrx || strict) {
     const auto* lanes = reinterpret_cast<const rs_lane_desc*>(p.d_lanes.data());
@@ -846,7 +879,8 @@ int Engine::run_stream_lanes(std::size_t d) {
                                          prof.size() ? reinterpret_cast<unsigned long long*>(prof.data()) : nullptr,
                                          reinterpret_cast<const rs_copy_desc*>(p.d_local.data()),
                                          reinterpret_cast<const std::uint64_t*>(p.d_item0.data()),
-                                         static_cast<std::uint32_t>(p.local.size()), cap - p.ntx - p.nrx,
+                                         static_cast<std::uint32_t>(p.local.size()),
+                                         strict ? p.strict_local_ctas : cap - p.ntx - p.nrx,
                                          strict ? &sync : nullptr, dv.stream),
                "stream lane kernel launch");
     ++launches;
@@ -906,23 +940,72 @@ char* Engine::layer_done_flag(int slot) const {
   return b ? b + comm_bytes(slot) - kSyncFlagBytes : nullptr;
 }
 
-// STAGED strict layers: the barrier state of one local device -- an arrival
-// counter, a release flag, the address (as mapped in this process) of every
-// slot's layer-done flag, and the local-copy item end of every plan layer.
+// STAGED strict layers: the barrier state of one local device -- arrival
+// counters (one per layer) and the role ticket, a release flag, the address
+// (as mapped in this process) of every slot's layer-done flag, the local-copy
+// item end of every plan layer, and for stream lanes the layer-scoped roles:
+// each lane end is active from its first batch's layer to its last's; roles
+// are dealt by ticket in that order after the local-copy CTAs (active in
+// every layer), and barrier l expects the CTAs active in l.  Deadlock-free
+// when the lane ends active in any one layer plus the local-copy CTAs fit the
+// co-resident capacity: a role starts only after every role of an earlier
+// first layer has started, and a role whose last layer is done exits.
 void Engine::upload_layer_sync(std::size_t d) {
   DeviceProgram& p = programs_[d];
   const Device& dv = devices_[d];
   const std::size_t nl = p.layers.size();
   const std::size_t ns = nslots_ > 1 ? static_cast<std::size_t>(nslots_) : 0;
-  std::vector<std::uint64_t> words(2 + ns + nl, 0);
+  const bool scoped = p.stream_lanes;
+  std::vector<std::uint32_t> expect, roles;
+  p.strict_max_active = 0;
+  p.strict_local_ctas = 0;
+  if (scoped) {
+    const int nlanes = p.ntx + p.nrx;
+    std::vector<int> first(static_cast<std::size_t>(nlanes), -1), last(static_cast<std::size_t>(nlanes), -1);
+    std::vector<int> active(nl + 1, 0);
+    for (int i = 0; i < nlanes; ++i) {
+      const rs_lane_desc& L = p.lanes[static_cast<std::size_t>(i)];
+      if (!L.nbatches) continue;  // exits at once: never arrives
+      int lo = static_cast<int>(nl), hi = -1;
+      for (std::uint32_t b = 0; b < L.nbatches; ++b) {
+        const int li = static_cast<int>(p.batches[L.batch0 + b].layer_idx);
+        lo = std::min(lo, li);
+        hi = std::max(hi, li);
+      }
+      if (static_cast<int>(p.batches[L.batch0].layer_idx) != lo)
+        throw IntegrityError("staged strict: a lane's batches are not in layer order");
+      first[static_cast<std::size_t>(i)] = lo;
+      last[static_cast<std::size_t>(i)] = hi;
+      for (int li = lo; li <= hi; ++li) ++active[static_cast<std::size_t>(li)];
+    }
+    p.strict_max_active = *std::max_element(active.begin(), active.end());
+    const int cap = lane_capacity(static_cast<int>(d), true);
+    p.strict_local_ctas = std::max(1, cap - p.strict_max_active);
+    expect.resize(nl);
+    for (std::size_t li = 0; li < nl; ++li)
+      expect[li] = static_cast<std::uint32_t>(active[li] + p.strict_local_ctas);
+    for (int k = 0; k < p.strict_local_ctas; ++k) roles.push_back(static_cast<std::uint32_t>(nlanes + k));
+    std::vector<int> order(static_cast<std::size_t>(nlanes));
+    for (int i = 0; i < nlanes; ++i) order[static_cast<std::size_t>(i)] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const int fa = first[static_cast<std::size_t>(a)], fb = first[static_cast<std::size_t>(b)];
+      return (fa < 0 ? 1 << 30 : fa) < (fb < 0 ? 1 << 30 : fb);
+    });
+    for (int i : order) roles.push_back(static_cast<std::uint32_t>(i));
+  }
+  const std::size_t n32 = expect.size() + roles.size();
+  std::vector<std::uint64_t> words(nl + 2 + ns + nl + (n32 + 1) / 2, 0);
   for (std::size_t s = 0; s < ns; ++s) {
     char* f = layer_done_flag(static_cast<int>(s));
     if (!f)
       throw DomainError("staged strict_layers: comm arena of slot " + std::to_string(s) +
                         " not mapped in this process (rs_arena_import RS_COMM on every process)");
-    words[2 + s] = addr(f);
+    words[nl + 2 + s] = addr(f);
   }
-  for (std::size_t li = 0; li < nl; ++li) words[2 + ns + li] = p.layers[li].item_end;
+  for (std::size_t li = 0; li < nl; ++li) words[nl + 2 + ns + li] = p.layers[li].item_end;
+  auto* tail = reinterpret_cast<std::uint32_t*>(words.data() + nl + 2 + ns + nl);
+  std::copy(expect.begin(), expect.end(), tail);
+  std::copy(roles.begin(), roles.end(), tail + expect.size());
   DeviceGuard g(dv.ordinal);
   p.d_sync = DeviceBuffer(dv.ordinal, words.size() * sizeof(std::uint64_t));
   p.d_sync.upload(words.data(), words.size() * sizeof(std::uint64_t), dv.stream);
@@ -931,10 +1014,14 @@ void Engine::upload_layer_sync(std::size_t d) {
   p.layer_sync.nlayers = static_cast<std::uint32_t>(nl);
   p.layer_sync.nslots = static_cast<std::uint32_t>(ns);
   p.layer_sync.arrive = reinterpret_cast<unsigned long long*>(base);
-  p.layer_sync.release = base + 1;
+  p.layer_sync.tickets = reinterpret_cast<unsigned long long*>(base + nl);
+  p.layer_sync.release = base + nl + 1;
   p.layer_sync.done_self = ns ? reinterpret_cast<std::uint64_t*>(layer_done_flag(dv.slot)) : nullptr;
-  p.layer_sync.done_all = reinterpret_cast<const std::uint64_t* const*>(base + 2);
-  p.layer_sync.local_layer_end = base + 2 + ns;
+  p.layer_sync.done_all = reinterpret_cast<const std::uint64_t* const*>(base + nl + 2);
+  p.layer_sync.local_layer_end = base + nl + 2 + ns;
+  const auto* tail_dev = reinterpret_cast<const std::uint32_t*>(base + nl + 2 + ns + nl);
+  p.layer_sync.expect = scoped ? tail_dev : nullptr;
+  p.layer_sync.roles = scoped ? tail_dev + expect.size() : nullptr;
 }
 
 }  // namespace rsb

@@ -96,26 +96,44 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* flag, uint64_t want,
 // layer.  The GPU's last arriver publishes the slot's layer-done flag, waits
 // for every slot's (peer-mapped, system scope) and releases its GPU.
 // Bounded like every ring wait: false = abort (error flag raised).
+//
+// Layer-scoped roles (S.expect): barrier li has its own counter and completes
+// at expect[li] arrivals; `wait` = false arrives without waiting (a role's
+// last barrier -- it exits and frees its CTA slot).  The GPU's last arriver
+// always completes the barrier (cross-slot flags, release) itself.
 __device__ __noinline__ bool layer_barrier(const rs_layer_sync& S, uint32_t li, uint64_t epoch,
-                                           unsigned int* error_flag, uint64_t spin_limit) {
+                                           unsigned int* error_flag, uint64_t spin_limit, bool wait = true) {
   __shared__ int passed;
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint64_t want = epoch + li + 1;
     bool ok = true;
     __threadfence_system();  // this CTA's layer-li stores (peer rings / shards) before its arrival
-    const unsigned long long n = atomicAdd(S.arrive, 1ull) + 1ull;
-    if (n == static_cast<unsigned long long>(li + 1) * gridDim.x) {
+    const unsigned long long n = atomicAdd(S.expect ? S.arrive + li : S.arrive, 1ull) + 1ull;
+    const unsigned long long full =
+        S.expect ? static_cast<unsigned long long>(S.expect[li]) : static_cast<unsigned long long>(li + 1) * gridDim.x;
+    if (n == full) {
       if (S.nslots) {
         st_release_sys(S.done_self, want);
         for (uint32_t s = 0; ok && s < S.nslots; ++s) ok = wait_geq(S.done_all[s], want, error_flag, spin_limit, true);
       }
       if (ok) st_release_gpu(S.release, want);
-    } else {
+    } else if (wait) {
       ok = wait_geq(S.release, want, error_flag, spin_limit, false);
     }
     passed = ok;
   }
+  __syncthreads();
+  return passed != 0;
+}
+
+// Wait (without arriving) until barrier li has completed: a layer-scoped
+// role's entry into its first layer li + 1.
+__device__ __noinline__ bool layer_wait(const rs_layer_sync& S, uint32_t li, uint64_t epoch,
+                                        unsigned int* error_flag, uint64_t spin_limit) {
+  __shared__ int passed;
+  __syncthreads();
+  if (threadIdx.x == 0) passed = wait_geq(S.release, epoch + li + 1, error_flag, spin_limit, false);
   __syncthreads();
   return passed != 0;
 }
@@ -753,8 +771,15 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   __shared__ __align__(128) rs_batch_desc desc_batches[DR::kNB * DR::kCB];
   __shared__ __align__(8) uint64_t desc_bar[2 * DR::kNB];
   const int lane = threadIdx.x;
-  const bool sender = blockIdx.x < ntx;
-  if (blockIdx.x >= ntx + nrx) {
+  uint32_t vb = blockIdx.x;  // the CTA's role: sender lane, receiver lane or local-copy CTA
+  if (sync.roles) {          // strict, layer-scoped roles: dealt by ticket in first-layer order
+    __shared__ uint32_t role;
+    if (lane == 0) role = sync.roles[atomicAdd(sync.tickets, 1ull)];
+    __syncwarp();
+    vb = role;
+  }
+  const bool sender = vb < ntx;
+  if (vb >= ntx + nrx) {
     // Strict layers (sync.nlayers > 0): the launch's remaining CTAs copy the
     // local tasks + carryovers layer by layer through two shared-memory
     // stages and meet every layer barrier with the lanes.
@@ -765,7 +790,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     }
     __syncwarp();
     const uint64_t pol = policy_evict_first();
-    const uint64_t wid = blockIdx.x - ntx - nrx, nw = gridDim.x - ntx - nrx;
+    const uint64_t wid = vb - ntx - nrx, nw = gridDim.x - ntx - nrx;
     uint64_t n = 0, begin = 0;
     for (uint32_t li = 0; li < sync.nlayers; ++li) {
       const uint64_t end = sync.local_layer_end[li];
@@ -793,11 +818,13 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     return;
   }
   if ((flags & kExFaultRx) && !sender) return;  // test hook: the receiving peer is gone
-  const rs_lane_desc L = sender ? lanes_tx[blockIdx.x] : lanes_rx[blockIdx.x - ntx];
+  const rs_lane_desc L = sender ? lanes_tx[vb] : lanes_rx[vb - ntx];
   const bool peer = (L.flags & RS_LANE_PEER) != 0;
   const bool fwd = !sender && L.fwd_slot_base != 0;  // relay forwarder
   const bool fpeer = (L.fwd_flags & RS_LANE_PEER) != 0;
   const int64_t fwd_delta = static_cast<int64_t>(L.fwd_slot_base - L.slot_base_rx);
+  const bool scoped = sync.nlayers && sync.expect;  // meets only its own layers' barriers
+  if (scoped && !L.nbatches) return;                // never counted in expect
   if (lane == 0) {
     for (int i = 0; i < 2 * static_cast<int>(DR::kNB); ++i) mbar_init(&desc_bar[i], 1);
     for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
@@ -818,13 +845,22 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   // strict layers: barriers passed so far; a lane end meets barrier l as soon
   // as its own layer-<=l batches are done (before that, at its first batch,
   // the barriers of the layers it has no part in)
+  // (layer-scoped: a lane end enters at its first batch's layer once the
+  // barrier before it completed, arrives at every barrier up to its last
+  // batch's layer, and arrives at that last one without waiting)
   uint32_t barriers = 0;
-  auto pass_to = [&](uint32_t target) -> bool {
+  auto pass_to = [&](uint32_t target, bool final_arrive) -> bool {
     for (; barriers < target; ++barriers)
-      if (!layer_barrier(sync, barriers, epoch, error_flag, spin_limit)) return false;
+      if (!layer_barrier(sync, barriers, epoch, error_flag, spin_limit, !(final_arrive && barriers + 1 == target)))
+        return false;
     return true;
   };
-  if (sync.nlayers && !pass_to(L.nbatches ? ring.batch(0).layer_idx : sync.nlayers)) return;
+  if (scoped) {
+    barriers = ring.batch(0).layer_idx;
+    if (barriers && !layer_wait(sync, barriers - 1, epoch, error_flag, spin_limit)) return;
+  } else if (sync.nlayers && !pass_to(L.nbatches ? ring.batch(0).layer_idx : sync.nlayers, false)) {
+    return;
+  }
   uint64_t g_ld = 0, g_st = 0;       // items loaded (issued) / stored (issued)
   uint32_t ready_b = 0xffffffffu;    // receiver: batch whose ready flag was acquired last
   uint32_t credit_b = 0xffffffffu;   // sender: batch whose slot credit was acquired last
@@ -948,7 +984,8 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
           fence_proxy_async_global();
         }
         __syncwarp();
-        if (!pass_to(st.b < L.nbatches ? ring.batch(st.b).layer_idx : sync.nlayers)) {
+        const bool done = st.b >= L.nbatches;
+        if (!pass_to(!done ? ring.batch(st.b).layer_idx : (scoped ? barriers + 1 : sync.nlayers), done && scoped)) {
           bulk_wait_all();
           return;
         }
@@ -974,7 +1011,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   }
   bulk_wait_all();  // shared memory stays valid until every store has read it
   if (prof && lane == 0) {  // diagnostic: cycles per phase, per lane end
-    unsigned long long* p = prof + 8ull * blockIdx.x;
+    unsigned long long* p = prof + 8ull * vb;
     p[0] = clock64() - prof_t0;
     p[1] = prof_reuse;
     p[2] = prof_store;
