@@ -128,12 +128,31 @@ __device__ __noinline__ bool layer_barrier(const rs_layer_sync& S, uint32_t li, 
 }
 
 // Wait (without arriving) until barrier li has completed: a layer-scoped
-// role's entry into its first layer li + 1.
+// role's entry into its first layer li + 1.  A role resident early may wait
+// through many layers, so the spin budget restarts whenever a barrier
+// completes (bounded per layer, like every other wait, not per handoff).
 __device__ __noinline__ bool layer_wait(const rs_layer_sync& S, uint32_t li, uint64_t epoch,
                                         unsigned int* error_flag, uint64_t spin_limit) {
   __shared__ int passed;
   __syncthreads();
-  if (threadIdx.x == 0) passed = wait_geq(S.release, epoch + li + 1, error_flag, spin_limit, false);
+  if (threadIdx.x == 0) {
+    const uint64_t want = epoch + li + 1;
+    uint64_t seen = 0, spins = 0;
+    int ok = 1;
+    for (uint64_t v; (v = ld_acquire_gpu(S.release)) < want;) {
+      if (v != seen) {
+        seen = v;
+        spins = 0;
+      }
+      if (*reinterpret_cast<volatile unsigned int*>(error_flag) || ++spins > spin_limit) {
+        atomicExch(error_flag, 1u);
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+    passed = ok;
+  }
   __syncthreads();
   return passed != 0;
 }

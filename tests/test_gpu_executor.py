@@ -589,6 +589,40 @@ def test_strict_layers_stream_lanes(ring_kernel, golden, oracle_c):
     eng.close()
 
 
+def test_strict_scoped_roles_beyond_co_resident_capacity(oracle_c):
+    """strict_layers on the stream lanes deals CTA roles by ticket in
+    first-layer order and counts each barrier over the CTAs live in its
+    layer, so a launch may hold more lane ends than can be co-resident as
+    long as one layer's fit: here 96 lanes per link (PP2: the two stages'
+    links never share a layer) give more lane CTAs than the device holds.
+    The run must neither deadlock nor reorder layers, and lands the C
+    oracle's bytes; repeated runs reuse the epoch-valued flags."""
+    import torch
+    sp = specs.llama("llama-mini-a16", 4)
+    co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 1)
+    eng = make_engine(sp, co, cn, "staged", 64 << 20, lanes_per_link=96, ring_slot_kib=16, trace=True,
+                      strict_layers=True)
+    plan = R.compute_transfer_plan(co, cn, sp)
+    rep = R.execute_plan(plan, eng)
+    assert rep["ok"] and rep["ring_kernel"] == 2, rep
+    _, want = oracle_c.execute(sp, co, cn, plan.text(), SEED, 64 << 20)
+    for (ti, rank), arr in want.entries.items():
+        assert np.array_equal(eng.read(RS_DST, rank, ti), arr), (ti, rank)
+    tr = [r for r in eng.trace(0) if r["t_end"]]
+    lane_ends = 2 * len({r["lane"] for r in tr if r["role"] == 0})
+    assert lane_ends > 6 * torch.cuda.get_device_properties(0).multi_processor_count, lane_ends
+    layers = sorted({r["layer"] for r in tr})
+    for a, b in zip(layers, layers[1:]):
+        end_a = max(r["t_end"] for r in tr if r["layer"] == a)
+        begin_b = min(r["t_begin"] for r in tr if r["layer"] == b)
+        assert begin_b >= end_a - 1000, (a, b, end_a, begin_b)
+    for _ in range(3):
+        eng.fill_pattern(RS_DST, SEED ^ 0xBEEF)
+        assert eng.run()["ok"]
+        assert eng.verify_pattern(RS_DST, SEED)[0] == 0
+    eng.close()
+
+
 def test_transport_trace_layer_order_and_causality():
     """STAGED transport trace (rs_trace_read, the reference's RecordingTransport
     on the device): every remote byte appears once per role; each lane
