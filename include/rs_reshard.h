@@ -92,9 +92,10 @@ typedef struct {
   int32_t mode;             /* RS_MODE_* */
   int32_t slots_per_link;   /* ring depth K (>= 2; 0: default 2), STAGED */
   int32_t lanes_per_link;   /* parallel rings per (src,dst) link, STAGED */
-  int32_t strict_layers;    /* 1: layer barriers (DIRECT: one launch per layer; STAGED: every lane
-                               CTA meets a device-wide barrier after each layer, the local copies
-                               run inside the lane launch), 0: fused */
+  int32_t strict_layers;    /* 1: layer barriers (DIRECT: one launch per layer; STAGED: a device-wide
+                               barrier after each layer, the local copies run inside the lane
+                               launch; stream-lane CTAs meet only the barriers of their lane's
+                               layer range), 0: fused */
   int64_t item_bytes;       /* work-item granularity of the copy engine (0: default) */
   int32_t blocks_per_sm;    /* 0: occupancy maximum */
   int32_t copy_kernel;      /* RS_COPY_*: LDG/STG warp engine or TMA bulk-copy ring */
