@@ -9,6 +9,7 @@
 #include <exception>
 #include <thread>
 #include <map>
+#include <queue>
 #include <set>
 
 #include "engine.hpp"
@@ -121,8 +122,15 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     std::vector<int> rx_ranks;
     int first = -1, last = -1;  // plan-layer index range of its tasks
   };
+  // plan-layer index of every layer (the order prepare executes them in);
+  // from the plan itself: rs_comm_alloc_plan sizes the rings before prepare
   std::map<int, int> layer_index;
-  for (std::size_t i = 0; i < plan_layers_.size(); ++i) layer_index[plan_layers_[i]] = static_cast<int>(i);
+  for (const auto& kv : plan.tasks_by_layer) layer_index.emplace(kv.first, 0);
+  for (const auto& kv : plan.carryover_by_layer) layer_index.emplace(kv.first, 0);
+  {
+    int i = 0;
+    for (auto& kv : layer_index) kv.second = i++;
+  }
   std::map<LaneKey, Link> links;
   for (const auto& [layer, tasks] : plan.tasks_by_layer)
     for (std::size_t i = 0; i < tasks.size(); ++i) {
@@ -197,7 +205,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     // lane share instead of splitting it.  Fused, every lane is live at once:
     // one "layer" spanning the plan.
     const bool scoped = geo.stream && opts_.strict_layers;
-    const std::size_t nl = scoped ? std::max<std::size_t>(plan_layers_.size(), 1) : 1;
+    const std::size_t nl = scoped ? std::max<std::size_t>(layer_index.size(), 1) : 1;
     auto span = [&](const Link& lk, auto&& fn) {  // the layers (rows) a link's lanes are live in
       if (!scoped) return fn(std::size_t{0});
       for (int li = std::max(lk.first, 0); li <= lk.last; ++li) fn(static_cast<std::size_t>(li));
@@ -236,6 +244,36 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
         const Link& wl = links.at(*widest);
         span(wl, [&](std::size_t l2) { touches(wl, [&](int x) { --live_lanes[l2 * ns + static_cast<std::size_t>(x)]; }); });
       }
+    // Flooring leaves up to one lane per link unused: hand the spare CTA
+    // slots out one lane at a time to the link with the most bytes per lane
+    // whose rows all have room, so the per-lane bytes -- and the lanes'
+    // finish times -- come out as even as the capacity allows.
+    // (ties go to the smaller link key: every process computes the same
+    // geometry, and comm_alloc_plan and prepare agree)
+    using Cand = std::pair<double, const LaneKey*>;
+    auto later = [](const Cand& a, const Cand& b) {
+      return a.first != b.first ? a.first < b.first : *b.second < *a.second;
+    };
+    std::priority_queue<Cand, std::vector<Cand>, decltype(later)> grow(later);
+    const char* no_grow = std::getenv("RS_RING_NO_GROW");  // diagnostic: proportional lanes only
+    for (const auto& [key, lk] : links)
+      if (lanes_of[key] < max_lanes && !(no_grow && *no_grow == '1'))
+        grow.push({static_cast<double>(lk.bytes) / lanes_of[key], &key});
+    while (!grow.empty()) {
+      const LaneKey* kp = grow.top().second;
+      grow.pop();
+      const Link& lk = links.at(*kp);
+      std::map<int, int> per_slot;  // CTAs one more lane adds to each slot (both ends may share one)
+      touches(lk, [&](int sl) { ++per_slot[sl]; });
+      bool room = true;
+      span(lk, [&](std::size_t li) {
+        for (const auto& [sl, c] : per_slot) room = room && live_lanes[li * ns + static_cast<std::size_t>(sl)] + c <= capacity;
+      });
+      if (!room) continue;  // rows only fill up: this link cannot grow again
+      const int n = ++lanes_of[*kp];
+      span(lk, [&](std::size_t li) { touches(lk, [&](int sl) { ++live_lanes[li * ns + static_cast<std::size_t>(sl)]; }); });
+      if (n < max_lanes) grow.push({static_cast<double>(lk.bytes) / n, kp});
+    }
   }
   // Ring slot size per dst rank: B split over its inbound lanes, capped at
   // 128 KiB by default -- B is the budget, not the target footprint.  At

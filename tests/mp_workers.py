@@ -45,6 +45,8 @@ def ipc_reshard(rank, world, mode):
     from paper_2605_22014_b200.native import RS_DST, RS_SRC
     dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
     torch.cuda.set_device(dev)
+    auto_lanes = mode.endswith("-auto")  # the engine's own lane allocation (rings sized before prepare)
+    mode = mode.replace("-auto", "")
     sp = specs.llama("llama-mini-a16" if mode.endswith("-a16") else "llama-mini", 4)
     mode = mode.replace("-a16", "")
     co, cn = specs.iota_config(1, 4, 2, 1), specs.iota_config(2, 2, 2, 2)
@@ -55,7 +57,7 @@ def ipc_reshard(rank, world, mode):
         mode, copy_kernel = "direct", 17
     if mode == "staged-strict":  # layer barriers across the two slots (peer-mapped done flags)
         mode, strict = "staged", True
-    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
+    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=0 if auto_lanes else 1, world_slots=world,
                    first_local_slot=rank, copy_kernel=copy_kernel, strict_layers=strict)
     eng.layout(RS_SRC, sp, co, so)
     eng.layout(RS_DST, sp, cn, sn)
@@ -178,7 +180,7 @@ def handoff_chain(rank, world, mode):
     dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
     torch.cuda.set_device(dev)
     sp = specs.llama("llama-mini", 4)
-    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
+    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=0 if auto_lanes else 1, world_slots=world,
                    first_local_slot=rank)
 
     def placement(cfg):  # alternate between blocked and shifted placements

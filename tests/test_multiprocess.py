@@ -58,7 +58,7 @@ def test_plan_agreement_and_partition():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["direct", "direct-tma", "staged", "staged-strict", "xfer", "staged-a16",
-                                  "staged-strict-a16"])
+                                  "staged-strict-a16", "staged-a16-auto", "staged-strict-a16-auto"])
 def test_two_processes_one_gpu_ipc(mode):
     import torch
     if not torch.cuda.is_available():
