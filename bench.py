@@ -436,7 +436,7 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
         staging = int(t[0])
     total = plan.summary()["total_bytes"]
     roof = roofline(traffic, step_ms, pk["hbm_gbs"], pk["nvlink_gbs"])
-    # One-GPU ring bound from measured transfer shapes (profiles/r2/l2_probe.jsonl,
+    # One-GPU ring model from measured transfer shapes (profiles/r2/l2_probe.jsonl,
     # tools/l2_probe.py: 1-warp CTAs, 2 x 16 KB TMA stages, 6 per SM): a remote
     # byte is one sender transfer (HBM -> L2 slot, 9011 GB/s of read + write)
     # plus one receiver transfer (L2 slot -> HBM, 9653 GB/s) on the same GPU;
@@ -470,7 +470,7 @@ def staged_leg(eng_direct, sp, co, so, cn, sn, plan, traffic, args, world, rank,
     if traffic_note:
         out["traffic"] = traffic_note
     if ring_bound:
-        out["one_gpu_ring_bound"] = ring_bound
+        out["one_gpu_ring_model"] = ring_bound
     eng.close()
     return out
 
