@@ -3,7 +3,8 @@
 
 Full size where source + destination state fit in HBM, else a 16-layer slice
 of the same resize.  DIRECT (copy engine) and STAGED (rings, B = 256 MiB per
-destination rank, automatic lanes).  Prints one JSON line per (config, mode)
+destination rank, automatic lanes); RS_TABLE_MODES adds "direct-strict" /
+"staged-strict" (the reference's barrier after every layer).  Prints one JSON line per (config, mode)
 with the 1-GPU HBM roofline fraction (2 x (plan + carryover) bytes over the
 measured copy peak) and the analytic-pattern check of every destination byte.
 """
@@ -36,11 +37,12 @@ def run(case, mode, layers=None):
     sp, co, cn = specs.sliced_case(case, layers) if layers else specs.baseline_case(case)
     plan = R.compute_transfer_plan(co, cn, sp)
     s = plan.summary()
-    eng = R.Engine([0], staging_bytes=256 << 20, mode=mode)
+    strict = mode.endswith("-strict")  # the reference's barrier after every layer
+    eng = R.Engine([0], staging_bytes=256 << 20, mode=mode.replace("-strict", ""), strict_layers=strict)
     eng.layout(RS_SRC, sp, co)
     eng.layout(RS_DST, sp, cn)
     need = eng.store_bytes(RS_SRC) + eng.store_bytes(RS_DST)
-    if mode == "staged":  # plan-sized rings (rs_comm_alloc_plan): tens of MiB per destination rank
+    if mode.startswith("staged"):  # plan-sized rings (rs_comm_alloc_plan): tens of MiB per destination rank
         need += (64 << 20) * len(set(cn.ranks))
     free, _ = torch.cuda.mem_get_info()
     if need + (1 << 30) > free:
@@ -64,15 +66,15 @@ def run(case, mode, layers=None):
             "carry_GB": round(s["carryover_bytes"] / 1e9, 2), "state_GB": round(need / 1e9, 1),
             "ms": round(mean, 3), "reshard_GBps": round(s["total_bytes"] / mean / 1e6, 1),
             "hbm_frac": round(algo / (mean / 1e3) / 1e9 / HBM, 4),
-            "hbm_frac_vs_dram_ring": round(ring / (mean / 1e3) / 1e9 / HBM, 4) if mode == "staged" else None,
+            "hbm_frac_vs_dram_ring": round(ring / (mean / 1e3) / 1e9 / HBM, 4) if mode.startswith("staged") else None,
             "peak_staging_MiB": rep["peak_staging_bytes"] >> 20, "mismatches": bad,
             "kernel": (("rs_stream_lane_kernel" if rep.get("ring_kernel") == 2 else "rs_exchange_kernel")
-                       if mode == "staged" else f"RS_COPY {rep.get('copy_kernel')}")}
+                       if mode.startswith("staged") else f"RS_COPY {rep.get('copy_kernel')}")}
 
 
 def main():
     for case in ("c1", "c2", "c3", "c3z", "c3zb", "c4", "c5", "c5b"):
-        for mode in ("direct", "staged"):
+        for mode in os.environ.get("RS_TABLE_MODES", "direct,staged").split(","):
             r = None
             for layers in (None, 16, 8):
                 try:
