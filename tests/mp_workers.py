@@ -180,7 +180,7 @@ def handoff_chain(rank, world, mode):
     dev = int(os.environ.get("RS_TEST_DEVICE", "0"))
     torch.cuda.set_device(dev)
     sp = specs.llama("llama-mini", 4)
-    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=0 if auto_lanes else 1, world_slots=world,
+    eng = R.Engine([dev], staging_bytes=1 << 20, mode=mode, lanes_per_link=1, world_slots=world,
                    first_local_slot=rank)
 
     def placement(cfg):  # alternate between blocked and shifted placements
