@@ -117,7 +117,10 @@ typedef struct {
   uint32_t nslots;                  // slots whose flags `done_all` lists (1: this GPU only)
   unsigned long long* arrive;       // arrival counters (zeroed before the launch): one, or one per layer with expect
   const uint32_t* expect;           // arrivals that complete barrier l (CTAs active in layer l), or null
+  const uint32_t* local_n;          // local-copy roles sharing layer l's local items, or null (all of them)
   const uint32_t* roles;            // ticket -> CTA role (the blockIdx the role stands for), or null
+  const uint32_t* local_roles;      // local role q: [2q] = its share index in every layer of its run,
+                                    // [2q + 1] = first layer | last layer << 16 (with local_n)
   unsigned long long* tickets;      // role ticket counter (zeroed with `arrive`)
   uint64_t* release;                // this GPU's release flag (epoch + layer + 1)
   uint64_t* done_self;              // this slot's layer-done flag (in its comm arena)

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <exception>
 #include <thread>
+#include <limits>
 #include <map>
 #include <queue>
 #include <set>
@@ -121,6 +122,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     int tx_slot = 0;
     std::vector<int> rx_ranks;
     int first = -1, last = -1;  // plan-layer index range of its tasks
+    std::map<int, std::uint64_t> layer_bytes;  // plan-layer index -> its bytes there
   };
   // plan-layer index of every layer (the order prepare executes them in);
   // from the plan itself: rs_comm_alloc_plan sizes the rings before prepare
@@ -151,6 +153,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       const int li = layer_index.count(layer) ? layer_index.at(layer) : 0;
       lk.first = lk.first < 0 ? li : std::min(lk.first, li);
       lk.last = std::max(lk.last, li);
+      lk.layer_bytes[li] += static_cast<std::uint64_t>(t.byte_size);
     }
   std::map<int, std::set<LaneKey>> inbound;  // dst rank -> links with a receiver there
   for (const auto& [key, lk] : links)
@@ -211,11 +214,47 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       for (int li = std::max(lk.first, 0); li <= lk.last; ++li) fn(static_cast<std::size_t>(li));
     };
     const std::size_t ns = static_cast<std::size_t>(nslots_);
+    // per-row lane capacity.  Fused: the share above.  Strict: each (layer,
+    // slot) splits the launch's CTAs between lane ends and in-launch local
+    // copies by that layer's bytes (ring bytes per lane end, local bytes
+    // weighted by RS_STRICT_LOCAL_WEIGHT), so a layer without local work
+    // (C2's second PP stage) gives the lanes everything; the local-copy
+    // roles take what the lanes leave (upload_layer_sync)
+    std::vector<int> cap_row(nl * ns, capacity);
+    if (scoped) {
+      // a local byte weighs 1.5 ring bytes per lane end (strict sweep,
+      // profiles/r2/strict_scoped/local_sweep.jsonl: best for C2, C4, C5b)
+      double w = 1.5;
+      if (const char* env = std::getenv("RS_STRICT_LOCAL_WEIGHT")) w = std::atof(env);
+      std::vector<double> ring_row(nl * ns, 0.0), local_row(nl * ns, 0.0);
+      for (const auto& [key, lk] : links)
+        for (const auto& [li, b] : lk.layer_bytes)
+          touches(lk, [&](int sl) { ring_row[static_cast<std::size_t>(li) * ns + static_cast<std::size_t>(sl)] += static_cast<double>(b); });
+      auto add_local = [&](int layer, int rank, std::int64_t bytes) {
+        const int sl = slot_in(src_slot, rank);
+        if (sl < 0 || !layer_index.count(layer)) return;
+        local_row[static_cast<std::size_t>(layer_index.at(layer)) * ns + static_cast<std::size_t>(sl)] += static_cast<double>(bytes);
+      };
+      for (const auto& [layer, tasks] : plan.tasks_by_layer)
+        for (const auto& t : tasks)
+          if (!ringed(t)) add_local(layer, t.src_rank, t.byte_size);
+      for (const auto& [layer, keeps] : plan.carryover_by_layer)
+        for (const auto& k : keeps) add_local(layer, k.rank, k.byte_size);
+      const double total = 0.98 * lane_capacity(0, geo.stream);
+      for (std::size_t row = 0; row < nl * ns; ++row)
+        cap_row[row] = ring_row[row] > 0
+                           ? std::max(1, static_cast<int>(total * ring_row[row] / (ring_row[row] + w * local_row[row])))
+                           : std::numeric_limits<int>::max();  // lanes idle here: no constraint from this row
+      if (std::getenv("RS_RING_CAPACITY_FRAC")) std::fill(cap_row.begin(), cap_row.end(), capacity);
+    }
     std::vector<double> live_bytes(nl * ns, 0.0);
     for (const auto& [key, lk] : links)
       span(lk, [&](std::size_t li) { touches(lk, [&](int sl) { live_bytes[li * ns + static_cast<std::size_t>(sl)] += static_cast<double>(lk.bytes); }); });
-    const double busiest = *std::max_element(live_bytes.begin(), live_bytes.end());
-    const double scale = busiest > 0 ? capacity / busiest : 0.0;  // lanes per byte
+    double scale = std::numeric_limits<double>::max();  // lanes per byte: the tightest row decides
+    for (std::size_t row = 0; row < nl * ns; ++row)
+      if (live_bytes[row] > 0 && cap_row[row] < std::numeric_limits<int>::max())
+        scale = std::min(scale, cap_row[row] / live_bytes[row]);
+    if (scale == std::numeric_limits<double>::max()) scale = 0.0;
     std::vector<int> live_lanes(nl * ns, 0);
     for (const auto& [key, lk] : links) {
       const int n = std::clamp(static_cast<int>(scale * static_cast<double>(lk.bytes)), 1, max_lanes);
@@ -225,7 +264,7 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
     // the max(1, .) floor can overshoot a slot with many light links: trim
     // the widest links live there
     for (std::size_t row = 0; row < nl * ns; ++row)
-      while (live_lanes[row] > capacity) {
+      while (live_lanes[row] > cap_row[row]) {
         const std::size_t li = row / ns;
         const int sl = static_cast<int>(row % ns);
         const LaneKey* widest = nullptr;
@@ -267,7 +306,10 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       touches(lk, [&](int sl) { ++per_slot[sl]; });
       bool room = true;
       span(lk, [&](std::size_t li) {
-        for (const auto& [sl, c] : per_slot) room = room && live_lanes[li * ns + static_cast<std::size_t>(sl)] + c <= capacity;
+        for (const auto& [sl, c] : per_slot) {
+          const std::size_t row = li * ns + static_cast<std::size_t>(sl);
+          room = room && static_cast<long long>(live_lanes[row]) + c <= cap_row[row];
+        }
       });
       if (!room) continue;  // rows only fill up: this link cannot grow again
       const int n = ++lanes_of[*kp];
@@ -994,7 +1036,7 @@ void Engine::upload_layer_sync(std::size_t d) {
   const std::size_t nl = p.layers.size();
   const std::size_t ns = nslots_ > 1 ? static_cast<std::size_t>(nslots_) : 0;
   const bool scoped = p.stream_lanes;
-  std::vector<std::uint32_t> expect, roles;
+  std::vector<std::uint32_t> expect, local_n, roles, local_roles;
   p.strict_max_active = 0;
   p.strict_local_ctas = 0;
   if (scoped) {
@@ -1018,20 +1060,46 @@ void Engine::upload_layer_sync(std::size_t d) {
     }
     p.strict_max_active = *std::max_element(active.begin(), active.end());
     const int cap = lane_capacity(static_cast<int>(d), true);
-    p.strict_local_ctas = std::max(1, cap - p.strict_max_active);
+    // Local-copy roles: layer l's local items are shared by n[l] CTAs --
+    // every CTA slot its lane ends leave (at least one, so each barrier has
+    // an arrival on this GPU).  Local slot j works in the layers with
+    // n > j; each maximal run of such layers is one role (a CTA that exits
+    // after the run), so exactly n[l] local roles are live in layer l and
+    // lanes + local roles never exceed the co-resident capacity.
+    std::vector<std::uint32_t> n(nl);
+    for (std::size_t li = 0; li < nl; ++li) n[li] = static_cast<std::uint32_t>(std::max(1, cap - active[li]));
+    if (std::getenv("RS_STRICT_UNIFORM_LOCAL"))  // diagnostic: one count for every layer
+      std::fill(n.begin(), n.end(), static_cast<std::uint32_t>(std::max(1, cap - p.strict_max_active)));
+    std::vector<std::pair<int, std::uint32_t>> order_all;  // (sort key, role)
+    const std::uint32_t m = *std::max_element(n.begin(), n.end());
+    for (std::uint32_t jj = 0; jj < m; ++jj)
+      for (std::size_t li = 0; li < nl;) {
+        if (n[li] <= jj) {
+          ++li;
+          continue;
+        }
+        std::size_t l1 = li;
+        while (l1 + 1 < nl && n[l1 + 1] > jj) ++l1;
+        const auto q = static_cast<std::uint32_t>(local_roles.size() / 2);
+        local_roles.push_back(jj);
+        local_roles.push_back(static_cast<std::uint32_t>(li) | static_cast<std::uint32_t>(l1) << 16);
+        order_all.push_back({2 * static_cast<int>(li), static_cast<std::uint32_t>(nlanes) + q});
+        li = l1 + 1;
+      }
+    p.strict_local_ctas = static_cast<int>(local_roles.size() / 2);
     expect.resize(nl);
-    for (std::size_t li = 0; li < nl; ++li)
-      expect[li] = static_cast<std::uint32_t>(active[li] + p.strict_local_ctas);
-    for (int k = 0; k < p.strict_local_ctas; ++k) roles.push_back(static_cast<std::uint32_t>(nlanes + k));
-    std::vector<int> order(static_cast<std::size_t>(nlanes));
-    for (int i = 0; i < nlanes; ++i) order[static_cast<std::size_t>(i)] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      const int fa = first[static_cast<std::size_t>(a)], fb = first[static_cast<std::size_t>(b)];
-      return (fa < 0 ? 1 << 30 : fa) < (fb < 0 ? 1 << 30 : fb);
-    });
-    for (int i : order) roles.push_back(static_cast<std::uint32_t>(i));
+    for (std::size_t li = 0; li < nl; ++li) expect[li] = static_cast<std::uint32_t>(active[li]) + n[li];
+    local_n = n;
+    // local roles and lane ends in first-layer order (local first on ties)
+    for (int i = 0; i < nlanes; ++i) {
+      const int f = first[static_cast<std::size_t>(i)];
+      order_all.push_back({f < 0 ? 1 << 30 : 2 * f + 1, static_cast<std::uint32_t>(i)});
+    }
+    std::stable_sort(order_all.begin(), order_all.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& [k, role] : order_all) roles.push_back(role);
   }
-  const std::size_t n32 = expect.size() + roles.size();
+  const std::size_t n32 = expect.size() + local_n.size() + roles.size() + local_roles.size();
   std::vector<std::uint64_t> words(nl + 2 + ns + nl + (n32 + 1) / 2, 0);
   for (std::size_t s = 0; s < ns; ++s) {
     char* f = layer_done_flag(static_cast<int>(s));
@@ -1043,7 +1111,9 @@ void Engine::upload_layer_sync(std::size_t d) {
   for (std::size_t li = 0; li < nl; ++li) words[nl + 2 + ns + li] = p.layers[li].item_end;
   auto* tail = reinterpret_cast<std::uint32_t*>(words.data() + nl + 2 + ns + nl);
   std::copy(expect.begin(), expect.end(), tail);
-  std::copy(roles.begin(), roles.end(), tail + expect.size());
+  std::copy(local_n.begin(), local_n.end(), tail + expect.size());
+  std::copy(roles.begin(), roles.end(), tail + expect.size() + local_n.size());
+  std::copy(local_roles.begin(), local_roles.end(), tail + expect.size() + local_n.size() + roles.size());
   DeviceGuard g(dv.ordinal);
   p.d_sync = DeviceBuffer(dv.ordinal, words.size() * sizeof(std::uint64_t));
   p.d_sync.upload(words.data(), words.size() * sizeof(std::uint64_t), dv.stream);
@@ -1059,7 +1129,9 @@ void Engine::upload_layer_sync(std::size_t d) {
   p.layer_sync.local_layer_end = base + nl + 2 + ns;
   const auto* tail_dev = reinterpret_cast<const std::uint32_t*>(base + nl + 2 + ns + nl);
   p.layer_sync.expect = scoped ? tail_dev : nullptr;
-  p.layer_sync.roles = scoped ? tail_dev + expect.size() : nullptr;
+  p.layer_sync.local_n = scoped ? tail_dev + expect.size() : nullptr;
+  p.layer_sync.roles = scoped ? tail_dev + expect.size() + local_n.size() : nullptr;
+  p.layer_sync.local_roles = scoped ? tail_dev + expect.size() + local_n.size() + roles.size() : nullptr;
 }
 
 }  // namespace rsb

@@ -809,11 +809,23 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
     }
     __syncwarp();
     const uint64_t pol = policy_evict_first();
-    const uint64_t wid = vb - ntx - nrx, nw = gridDim.x - ntx - nrx;
-    uint64_t n = 0, begin = 0;
-    for (uint32_t li = 0; li < sync.nlayers; ++li) {
+    uint64_t wid = vb - ntx - nrx;
+    // layer-scoped local roles (sync.local_n): layer li's items are shared by
+    // local_n[li] CTAs; this role is share `wid` in every layer of its run
+    // [l0, l1] and meets only those barriers
+    uint32_t l0 = 0, l1 = sync.nlayers - 1;
+    if (sync.local_n) {
+      const uint32_t q = static_cast<uint32_t>(wid);
+      wid = sync.local_roles[2 * q];
+      l0 = sync.local_roles[2 * q + 1] & 0xffffu;
+      l1 = sync.local_roles[2 * q + 1] >> 16;
+      if (l0 && !layer_wait(sync, l0 - 1, epoch, error_flag, spin_limit)) return;
+    }
+    uint64_t n = 0, begin = l0 ? sync.local_layer_end[l0 - 1] : 0;
+    for (uint32_t li = l0; li <= l1; ++li) {
       const uint64_t end = sync.local_layer_end[li];
-      for (uint64_t item = begin + wid; item < end; item += nw, ++n) {
+      const uint64_t nw = sync.local_n ? sync.local_n[li] : gridDim.x - ntx - nrx;
+      for (uint64_t item = begin + wid; item < end && wid < nw; item += nw, ++n) {
         const uint32_t s = static_cast<uint32_t>(n % kStages);
         if (n >= static_cast<uint64_t>(kStages)) bulk_wait_read_dyn(kStages - 1);  // item n - kStages left stage s
         __syncwarp();
@@ -832,7 +844,7 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
       bulk_wait_all();  // this layer's stores are written before the barrier's release
       fence_proxy_async_global();
       __syncwarp();
-      if (!layer_barrier(sync, li, epoch, error_flag, spin_limit)) return;
+      if (!layer_barrier(sync, li, epoch, error_flag, spin_limit, !(sync.local_n && li == l1))) return;
     }
     return;
   }
