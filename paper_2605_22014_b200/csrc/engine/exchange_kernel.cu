@@ -799,9 +799,9 @@ __global__ void __launch_bounds__(32) rs_stream_lane_kernel(
   }
   const bool sender = vb < ntx;
   if (vb >= ntx + nrx) {
-    // Strict layers (sync.nlayers > 0): the launch's remaining CTAs copy the
-    // local tasks + carryovers layer by layer through two shared-memory
-    // stages and meet every layer barrier with the lanes.
+    // Strict layers (sync.nlayers > 0): the launch's local-copy roles copy
+    // the local tasks + carryovers layer by layer through the shared-memory
+    // stages and meet the barriers of their layers with the lanes.
     if (!sync.nlayers) return;
     if (lane == 0) {
       for (int i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
