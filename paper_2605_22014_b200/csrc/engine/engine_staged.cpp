@@ -294,10 +294,8 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
       return a.first != b.first ? a.first < b.first : *b.second < *a.second;
     };
     std::priority_queue<Cand, std::vector<Cand>, decltype(later)> grow(later);
-    const char* no_grow = std::getenv("RS_RING_NO_GROW");  // diagnostic: proportional lanes only
     for (const auto& [key, lk] : links)
-      if (lanes_of[key] < max_lanes && !(no_grow && *no_grow == '1'))
-        grow.push({static_cast<double>(lk.bytes) / lanes_of[key], &key});
+      if (lanes_of[key] < max_lanes) grow.push({static_cast<double>(lk.bytes) / lanes_of[key], &key});
     while (!grow.empty()) {
       const LaneKey* kp = grow.top().second;
       grow.pop();
@@ -1068,8 +1066,6 @@ void Engine::upload_layer_sync(std::size_t d) {
     // lanes + local roles never exceed the co-resident capacity.
     std::vector<std::uint32_t> n(nl);
     for (std::size_t li = 0; li < nl; ++li) n[li] = static_cast<std::uint32_t>(std::max(1, cap - active[li]));
-    if (std::getenv("RS_STRICT_UNIFORM_LOCAL"))  // diagnostic: one count for every layer
-      std::fill(n.begin(), n.end(), static_cast<std::uint32_t>(std::max(1, cap - p.strict_max_active)));
     std::vector<std::pair<int, std::uint32_t>> order_all;  // (sort key, role)
     const std::uint32_t m = *std::max_element(n.begin(), n.end());
     for (std::uint32_t jj = 0; jj < m; ++jj)
