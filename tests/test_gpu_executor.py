@@ -861,11 +861,14 @@ def _random_aligned_resizes(n=10, seed=11):
     return out
 
 
-@pytest.mark.parametrize("strict", [False, True])
-def test_stream_lanes_random_aligned_resizes(strict, oracle_c):
+@pytest.mark.parametrize("strict,lanes", [(False, 2), (True, 2), (False, 0), (True, 0)])
+def test_stream_lanes_random_aligned_resizes(strict, lanes, oracle_c):
+    """lanes 0: the engine's own allocation -- proportional + water-filled
+    lanes, and under strict layers per-(layer, slot) lane caps with the local
+    copies split into run-segmented roles (uneven PP stages included)."""
     for layers, co, cn in _random_aligned_resizes():
         sp = specs.llama("llama-mini-a16", layers)
-        eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=2, ring_slot_kib=16, strict_layers=strict)
+        eng = make_engine(sp, co, cn, "staged", 1 << 20, lanes_per_link=lanes, ring_slot_kib=16, strict_layers=strict)
         plan = R.compute_transfer_plan(co, cn, sp)
         rep = R.execute_plan(plan, eng)
         assert rep["ok"], (co, cn, rep)
