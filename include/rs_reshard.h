@@ -335,11 +335,16 @@ int rs_store_swap(rs_engine* e);
  * round r: step 1 (pack r), moves each tx link's round_bytes[r] from its
  * buffer to the peer's matching rx link buffer (ncclSend/ncclRecv, links in
  * index order on both sides), then step 2 (unpack r).  Steps synchronise the
- * engine stream before returning.  dir: 0 tx, 1 rx. */
+ * engine stream before returning, unless `what` carries RS_XFER_ASYNC: then
+ * the step is only enqueued on the stream rs_xfer_stream returns and the
+ * caller orders its NCCL calls against it with events (no host round trip
+ * per round).  dir: 0 tx, 1 rx. */
+#define RS_XFER_ASYNC 16
 int rs_xfer_info(rs_engine* e, int32_t* rounds, int32_t* ntx, int32_t* nrx);
 int rs_xfer_link(rs_engine* e, int32_t dir, int32_t index, int32_t* peer_slot, int32_t* src_rank,
                  int32_t* dst_rank, void** buffer, int64_t* buffer_bytes, int64_t* round_bytes);
 int rs_xfer_step(rs_engine* e, int32_t what, int32_t round);
+int rs_xfer_stream(rs_engine* e, void** stream); /* the engine stream xfer steps run on (cudaStream_t) */
 
 /* Transport trace of the last STAGED run on local device `device` (engine
  * created with trace = 1): the RecordingTransport of the reference

@@ -562,4 +562,8 @@ int rs_xfer_step(rs_engine* e, int32_t what, int32_t round) {
   return guarded([&] { e->impl.xfer_step(what, round); });
 }
 
+int rs_xfer_stream(rs_engine* e, void** stream) {
+  return guarded([&] { *stream = e->impl.xfer_stream(); });
+}
+
 }  // extern "C"

@@ -191,7 +191,8 @@ class Engine {
   };
   int xfer_rounds() const { return xfer_rounds_; }
   const std::vector<XferLink>& xfer_links(int dir) const { return dir ? xfer_rx_ : xfer_tx_; }
-  void xfer_step(int what, int round);  // 0 local copies, 1 pack round, 2 unpack round
+  void xfer_step(int what, int round);  // 0 local copies, 1 pack round, 2 unpack round (| RS_XFER_ASYNC)
+  void* xfer_stream() const;            // the stream xfer steps run on (cudaStream_t)
 
  private:
   void compile_xfer(const reshard::TransferPlan& plan);

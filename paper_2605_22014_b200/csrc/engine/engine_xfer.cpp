@@ -257,8 +257,16 @@ void Engine::compile_xfer(const reshard::TransferPlan& plan) {
   cuda_check(cudaStreamSynchronize(dv.stream), "xfer upload");
 }
 
+void* Engine::xfer_stream() const {
+  if (!prepared_ || opts_.mode != RS_MODE_XFER) throw DomainError("xfer: prepare a plan in RS_MODE_XFER first");
+  return devices_[0].stream;
+}
+
 void Engine::xfer_step(int what, int round) {
   if (!prepared_ || opts_.mode != RS_MODE_XFER) throw DomainError("xfer: prepare a plan in RS_MODE_XFER first");
+  const bool async = (what & RS_XFER_ASYNC) != 0;  // enqueue only: the caller orders NCCL by events
+  what &= ~RS_XFER_ASYNC;
+  if (what < 0 || what > 2) throw DomainError("xfer: step must be 0 (local), 1 (pack) or 2 (unpack)");
   const Device& dv = devices_[0];
   Guard g(dv.ordinal);
   if (what == 0) {
@@ -280,7 +288,7 @@ void Engine::xfer_step(int what, int round) {
                               dv.stream),
                what == 1 ? "xfer pack" : "xfer unpack");
   }
-  cuda_check(cudaStreamSynchronize(dv.stream), "xfer step");
+  if (!async) cuda_check(cudaStreamSynchronize(dv.stream), "xfer step");
 }
 
 }  // namespace rsb

@@ -17,6 +17,7 @@ RS_OK, RS_EDOMAIN, RS_EINTEGRITY, RS_ESYSTEM = 0, 1, 2, 3
 RS_SRC, RS_DST, RS_COMM = 0, 1, 2
 RS_IPC_HANDLE_BYTES = 64
 RS_MODE_DIRECT, RS_MODE_STAGED, RS_MODE_XFER = 0, 1, 2
+RS_XFER_ASYNC = 16  # rs_xfer_step: enqueue only (rs_reshard.h)
 RS_TRAFFIC_RELAY = 1
 
 EXPORTS = [
@@ -28,7 +29,7 @@ EXPORTS = [
     "rs_store_write", "rs_store_free", "rs_fill_pattern", "rs_verify_pattern", "rs_prepare",
     "rs_run", "rs_execute", "rs_execute_host", "rs_host_alloc", "rs_host_free", "rs_comm_alloc",
     "rs_arena_export", "rs_arena_import", "rs_plan_traffic", "rs_plan_traffic_ex", "rs_xfer_info", "rs_xfer_link",
-    "rs_xfer_step", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan", "rs_trace_read",
+    "rs_xfer_step", "rs_xfer_stream", "rs_switch", "rs_store_swap", "rs_plan_placement", "rs_comm_alloc_plan", "rs_trace_read",
 ]
 
 
@@ -195,6 +196,7 @@ def lib() -> C.CDLL:
         L.rs_xfer_info.argtypes = [VP, P(I32), P(I32), P(I32)]
         L.rs_xfer_link.argtypes = [VP, I32, I32, P(I32), P(I32), P(I32), P(VP), P(I64), P(I64)]
         L.rs_xfer_step.argtypes = [VP, I32, I32]
+        L.rs_xfer_stream.argtypes = [VP, P(VP)]
         L.rs_switch.argtypes = [VP, VP, P(VP), I32, P(SwitchStats)]
         L.rs_store_swap.argtypes = [VP]
         L.rs_plan_placement.argtypes = [C.c_char_p, P(Config), P(Config), P(I32), I32, P(PlacementOptions),

@@ -283,8 +283,13 @@ class Engine:
         return {"peer_slot": peer.value, "src_rank": s.value, "dst_rank": d.value, "ptr": buf.value or 0,
                 "nbytes": nb.value, "round_bytes": [rb[i] for i in range(rounds)]}
 
-    def xfer_step(self, what: int, rnd: int = 0):
-        N.check(N.lib().rs_xfer_step(self._h, what, rnd))
+    def xfer_step(self, what: int, rnd: int = 0, sync: bool = True):
+        N.check(N.lib().rs_xfer_step(self._h, what | (0 if sync else N.RS_XFER_ASYNC), rnd))
+
+    def xfer_stream(self) -> int:
+        s = C.c_void_p()
+        N.check(N.lib().rs_xfer_stream(self._h, C.byref(s)))
+        return s.value or 0
 
     def trace(self, device: int = 0):
         """STAGED transport trace of the last run (engine built with trace=True):

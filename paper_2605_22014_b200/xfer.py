@@ -180,11 +180,18 @@ class Nccl:
             self.comm = C.c_void_p()
 
 
-def run_local_slots(engines, nccl: Nccl, device: int) -> dict:
+def run_local_slots(engines, nccl: Nccl, device: int, stream_ordered: bool = False) -> dict:
     """One handoff across virtual slots on one GPU: engines[k] drives slot k
     (RS_MODE_XFER, prepared); NCCL moves every link's round buffer.  Send and
     receive lists are both ordered by (src rank, dst rank), so the k-th send
-    to peer 0 matches the k-th receive from peer 0."""
+    to peer 0 matches the k-th receive from peer 0.
+
+    stream_ordered: the rounds are enqueued without a host round trip -- each
+    engine's pack, the NCCL group and each engine's unpack are ordered by CUDA
+    events (the strongest NCCL baseline; the default is the paper's
+    host-driven loop)."""
+    if stream_ordered:
+        return _run_local_slots_events(engines, nccl, device)
     rounds = engines[0].xfer_info()[0]
     tx, rx = [], []
     for e in engines:
@@ -214,3 +221,42 @@ def run_local_slots(engines, nccl: Nccl, device: int) -> dict:
             e.xfer_step(2, r)
     torch.cuda.synchronize(device)
     return {"rounds": rounds, "links": len(tx), "bytes_sent": moved, "seconds": time.perf_counter() - t0}
+
+
+def _run_local_slots_events(engines, nccl: Nccl, device: int) -> dict:
+    rounds = engines[0].xfer_info()[0]
+    tx, rx = [], []
+    for e in engines:
+        _, ntx, nrx = e.xfer_info()
+        tx += [e.xfer_link(0, i, rounds) for i in range(ntx)]
+        rx += [e.xfer_link(1, i, rounds) for i in range(nrx)]
+    key = lambda l: (l["src_rank"], l["dst_rank"])  # noqa: E731
+    tx.sort(key=key)
+    rx.sort(key=key)
+    assert [key(l) for l in tx] == [key(l) for l in rx], "xfer links do not pair up"
+    streams = [torch.cuda.ExternalStream(e.xfer_stream(), device=device) for e in engines]
+    comm = torch.cuda.Stream(device)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for e in engines:
+        e.xfer_step(0, sync=False)
+    moved = 0
+    for r in range(rounds):
+        sends = [(l["ptr"], l["round_bytes"][r]) for l in tx if l["round_bytes"][r]]
+        recvs = [(l["ptr"], l["round_bytes"][r]) for l in rx if l["round_bytes"][r]]
+        for e, st in zip(engines, streams):
+            e.xfer_step(1, r, sync=False)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            comm.wait_event(ev)
+        if sends:
+            nccl.group(sends, recvs, comm.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(comm)
+        for e, st in zip(engines, streams):
+            st.wait_event(done)  # the round's bytes landed (and its send buffers were read)
+            e.xfer_step(2, r, sync=False)
+        moved += sum(n for _, n in sends)
+    torch.cuda.synchronize(device)
+    return {"rounds": rounds, "links": len(tx), "bytes_sent": moved, "seconds": time.perf_counter() - t0,
+            "stream_ordered": True}

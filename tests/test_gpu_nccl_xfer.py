@@ -56,18 +56,19 @@ def digest(engs, slot_of, sp, owners):
     return h.hexdigest()
 
 
-def run_case(nccl, sp, co, cn, nslots, slot_of, B, reps=1):
+def run_case(nccl, sp, co, cn, nslots, slot_of, B, reps=1, stream_ordered=False):
     from paper_2605_22014_b200 import xfer
     engs = slot_engines(sp, co, cn, nslots, slot_of, B)
     plan = R.compute_transfer_plan(co, cn, sp)
     for e in engs:
         e.prepare(plan)
     for _ in range(reps):
-        info = xfer.run_local_slots(engs, nccl, 0)
+        info = xfer.run_local_slots(engs, nccl, 0, stream_ordered=stream_ordered)
     return engs, plan, info
 
 
-def test_random_pairs_nccl_bitexact(nccl, golden, oracle_c):
+@pytest.mark.parametrize("stream_ordered", [False, True])
+def test_random_pairs_nccl_bitexact(nccl, golden, oracle_c, stream_ordered):
     rows = {r["seed"]: r for r in golden["random_pairs"]["cases"]}
     n = 0
     for seed, sp, co, cn in specs.iter_random_cases(200, golden["random_pairs"]["base_seed"]):
@@ -75,7 +76,7 @@ def test_random_pairs_nccl_bitexact(nccl, golden, oracle_c):
             continue
         nslots = 1 + seed % 4
         slot_of = lambda r, k=nslots: (r * 7) % k  # noqa: E731  scattered placement
-        engs, plan, info = run_case(nccl, sp, co, cn, nslots, slot_of, 64 << 10)
+        engs, plan, info = run_case(nccl, sp, co, cn, nslots, slot_of, 64 << 10, stream_ordered=stream_ordered)
         owners = sorted(oracle_c.store_pattern(sp, cn, 0, fill=False).entries.keys())
         assert digest(engs, slot_of, sp, owners) == rows[seed]["exec"]["4096"]["dst_sha"], seed
         for e in engs:
@@ -85,10 +86,14 @@ def test_random_pairs_nccl_bitexact(nccl, golden, oracle_c):
     assert n >= 30
 
 
-def test_c1_gpt2_nccl_bitexact_idempotent(nccl, golden, oracle_c):
+@pytest.mark.parametrize("stream_ordered", [False, True])
+def test_c1_gpt2_nccl_bitexact_idempotent(nccl, golden, oracle_c, stream_ordered):
+    """Full GPT-2 C1 through the NCCL path twice -- host-driven rounds (the
+    paper's loop) and rounds ordered by CUDA events (no host round trip) --
+    equal to the reference executor's digest."""
     sp, co, cn = specs.baseline_case("c1")
     slot_of = lambda r: r  # noqa: E731  one virtual GPU per rank
-    engs, plan, info = run_case(nccl, sp, co, cn, 8, slot_of, 256 << 20, reps=2)
+    engs, plan, info = run_case(nccl, sp, co, cn, 8, slot_of, 256 << 20, reps=2, stream_ordered=stream_ordered)
     assert info["bytes_sent"] > 0 and info["links"] > 0
     owners = sorted(oracle_c.store_pattern(sp, cn, 0, fill=False).entries.keys())
     assert digest(engs, slot_of, sp, owners) == golden["c1_exec"]["1073741824"]["dst_sha"]

@@ -51,7 +51,7 @@ def staged(sp, co, cn, plan, B, mode, steps, warmup):
             "mismatches": bad}
 
 
-def nccl_path(sp, co, cn, plan, B, nccl, steps, warmup):
+def nccl_path(sp, co, cn, plan, B, nccl, steps, warmup, stream_ordered=False):
     nslots = max(max(co.ranks), max(cn.ranks)) + 1
     engs = []
     for s in range(nslots):
@@ -66,8 +66,8 @@ def nccl_path(sp, co, cn, plan, B, nccl, steps, warmup):
     for e in engs:
         e.prepare(plan)
     for _ in range(warmup):
-        xfer.run_local_slots(engs, nccl, 0)
-    infos = [xfer.run_local_slots(engs, nccl, 0) for _ in range(steps)]
+        xfer.run_local_slots(engs, nccl, 0, stream_ordered=stream_ordered)
+    infos = [xfer.run_local_slots(engs, nccl, 0, stream_ordered=stream_ordered) for _ in range(steps)]
     bad = sum(e.verify_pattern(RS_DST, SEED)[0] for e in engs)
     for e in engs:
         e.close()
@@ -91,14 +91,14 @@ def main():
     print(json.dumps({**base, "path": "direct", "B_MiB": 0, **r,
                       "reshard_GBps": round(s["total_bytes"] / r["device_ms"] / 1e6, 1)}), flush=True)
     for B in budgets:
-        for path in ("staged", "nccl"):
+        for path in ("staged", "nccl", "nccl-stream"):
             t0 = time.time()
             try:
                 if path == "staged":
                     r = staged(sp, co, cn, plan, B, "staged", steps, 2)
                     ms = r["device_ms"]
-                else:
-                    r = nccl_path(sp, co, cn, plan, B, nccl, steps, 1)
+                else:  # nccl: the paper's host-driven rounds; nccl-stream: rounds ordered by events
+                    r = nccl_path(sp, co, cn, plan, B, nccl, steps, 1, stream_ordered=path == "nccl-stream")
                     ms = r["host_ms"]
                 print(json.dumps({**base, "path": path, "B_MiB": B >> 20, **r,
                                   "reshard_GBps": round(s["total_bytes"] / ms / 1e6, 1),
