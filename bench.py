@@ -294,9 +294,10 @@ def xfer_one_gpu(args) -> None:
     for e in engs:
         e.prepare(plan)
     for _ in range(args.warmup):
-        xfer.run_local_slots(engs, nccl, 0)
+        xfer.run_local_slots(engs, nccl, 0, stream_ordered=bool(args.xfer_stream_ordered))
     with ClockSampler(0) as clk:
-        infos = [xfer.run_local_slots(engs, nccl, 0) for _ in range(args.steps)]
+        infos = [xfer.run_local_slots(engs, nccl, 0, stream_ordered=bool(args.xfer_stream_ordered))
+                 for _ in range(args.steps)]
     bad = sum(e.verify_pattern(RS_DST, SEED)[0] for e in engs)
     step_ms = statistics.mean(i["seconds"] for i in infos) * 1e3
     pk = peaks()
@@ -309,6 +310,8 @@ def xfer_one_gpu(args) -> None:
             "data": "synthetic: reference pattern state (shard_store.cpp:51-85)",
             "config": {"workload": desc + " -- NCCL comparator: one virtual slot per rank",
                        "plan_bytes": total, "carryover_bytes": summ["carryover_bytes"], "mode": "xfer",
+                       "xfer_rounds": "stream-ordered (CUDA events)" if args.xfer_stream_ordered
+                       else "host-driven (the paper's loop)",
                        "transport": f"ncclSend/ncclRecv self-loop, NCCL {nccl.version}",
                        "staging_bytes": args.staging_bytes, "rounds": infos[0]["rounds"],
                        "links": infos[0]["links"], "bytes_through_nccl": infos[0]["bytes_sent"],
@@ -756,6 +759,8 @@ def main() -> None:
     ap.add_argument("--placement", default="iota", choices=["iota", "searched"],
                     help="destination rank list: BASELINE iota, or rs_plan_placement's choice")
     ap.add_argument("--ring-slot-kib", type=int, default=0, help="STAGED ring slot cap (0: default, -1: none)")
+    ap.add_argument("--xfer-stream-ordered", type=int, default=0,
+                    help="--mode xfer on one GPU: order the NCCL rounds by CUDA events instead of the host")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
