@@ -70,6 +70,10 @@ def _dp_scaleout_cases():
                 "slot_old": [0, 1], "slot_new": [2, 2, 0, 2], "world": 3, "lanes": 2})
     # the same with the reference's layer barriers (strict layers on the stream lanes)
     out.append(dict(out[0], name="c5b-mini-strict", strict=True))
+    # the engine's own lane allocation (water-filled lanes; strict: per-layer
+    # caps and run-segmented local roles), fused and strict
+    out.append(dict(out[0], name="c5b-mini-auto", lanes=0))
+    out.append(dict(out[0], name="c5b-mini-strict-auto", strict=True, lanes=0))
     # TP2 -> TP1PP1DP4 (a box fans out to 3 new replicas: chains of length 3)
     out.append({"name": "tp2-dp4", "layers": 2, "bpe": 4, "old": [2, 1, 1], "new": [1, 1, 4],
                 "slot_old": [0, 1], "slot_new": [2, 3, 0, 1], "world": 4, "staging": 256 << 10})
