@@ -159,9 +159,11 @@ Engine::RingGeometry Engine::ring_geometry(const reshard::TransferPlan& plan) co
   for (const auto& [key, lk] : links)
     for (int r : lk.rx_ranks) inbound[r].insert(key);
 
-  // Lanes per link.  Throughput of a lane is one 8-warp CTA's worth of bytes
-  // in flight, so more lanes is faster (profiles/r1/staged_sweep.jsonl) until
-  // the sender + receiver CTAs of the busiest slot stop being co-resident.
+  // Lanes per link.  Throughput of a lane is one lane-end CTA's worth of
+  // bytes in flight (a 1-warp stream-lane CTA, or an 8-warp classic one), so
+  // more lanes is faster (profiles/r1/staged_sweep.jsonl,
+  // profiles/r2/stream_lane_share_sweep.jsonl) until the sender + receiver
+  // CTAs of the busiest slot stop being co-resident.
   // Automatic choice: lanes proportional to each link's bytes (a link's
   // lanes finish together, so the launch ends when the heaviest link does),
   // scaled so every slot's sender + receiver lanes fit a share of one
